@@ -1,0 +1,143 @@
+/*
+ * tk_sm100.h -- C ABI of the B200 (sm_100a) flexible GEMM library (libtk_sm100.so).
+ *
+ * This is the drop-in boundary for the reference package's GEMM path
+ * (reference = /root/reference/pkg, "tilekit"):
+ *
+ *   tk_gemm          replaces kernel.gemm_execute / api.matmul
+ *                    (pkg/src/tilekit/kernel.py:253-330, pkg/src/tilekit/api.py:37-40):
+ *                    one resolved KernelConfig, lowered by the host planner to a
+ *                    TkGemmPlan, executed as one stream-ordered device launch.
+ *   tk_gemm_ex_raw   replaces api.gemm_ex_raw / GEMM_EX_CFUNC
+ *                    (pkg/src/tilekit/api.py:317-373): identical parameter list and
+ *                    status convention (0 ok, 1 configuration error); pointers may be
+ *                    host or device memory; synchronous like the reference.
+ *   tk_gemm_ex_raw_async  same on device pointers, ordered on a caller stream.
+ *
+ * No CUDA or torch types appear in the signatures: streams are passed as void*
+ * (a cudaStream_t / CUstream value, NULL = legacy default stream).
+ * Every matrix is addressed through a TkLayout "digit" map: logical index i of
+ * a dimension is decomposed fastest-first into digits d_t = (i / prod(ext[<t])) % ext[t]
+ * and the element offset is sum_t d_t * stride[t] (+ the second plane for pair types).
+ */
+#ifndef TK_SM100_H
+#define TK_SM100_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TK_ABI_VERSION 1
+#define TK_MAX_DIGITS 3
+#define TK_MAX_TOPS 8
+
+/* storage / accumulation scalars */
+enum TkScalar { TK_F16 = 0, TK_BF16 = 1, TK_F32 = 2, TK_F64 = 3 };
+/* operators (reference operators.py:98-188) */
+enum TkOperator { TK_OP_REAL = 0, TK_OP_COMPLEX = 1, TK_OP_DUAL = 2 };
+/* layout kinds (reference layouts.py: ColMajor/RowMajor/Padded/StridedPermutation are
+ * STRIDED digit maps; Diagonal; Zero) */
+enum TkLayoutKind { TK_LAYOUT_STRIDED = 0, TK_LAYOUT_DIAGONAL = 1, TK_LAYOUT_ZERO = 2 };
+/* pair element storage (reference layouts.py:314-394) */
+enum TkPairMode { TK_PAIR_NONE = 0, TK_PAIR_INTERLEAVED = 1, TK_PAIR_SPLIT = 2 };
+/* element-wise transform ops (reference components.py:52-94) */
+enum TkTransformOp { TK_T_SCALE = 1, TK_T_ADD = 2, TK_T_RELU = 3 };
+/* predicates (reference components.py:171-191) */
+enum TkPredicate { TK_PRED_ALWAYS = 0, TK_PRED_DIAGONAL = 1, TK_PRED_MASK = 2 };
+/* execution lanes */
+enum TkLane { TK_LANE_AUTO = 0, TK_LANE_TCGEN05 = 1, TK_LANE_SIMT = 2 };
+/* status codes: 0 and 1 follow the reference gemm_ex_raw convention */
+enum TkStatus { TK_OK = 0, TK_ERR_CONFIG = 1, TK_ERR_CUDA = 2 };
+/* gemm_ex_raw type tags: 0-5 as the reference (api.py:318-326), 6-11 new */
+enum TkTag {
+  TK_TAG_F32 = 0, TK_TAG_F64 = 1, TK_TAG_C64 = 2, TK_TAG_C128 = 3,
+  TK_TAG_DUAL32 = 4, TK_TAG_DUAL64 = 5,
+  TK_TAG_F16F32 = 6,     /* A,B float16; C float32 */
+  TK_TAG_BF16F32 = 7,    /* A,B bfloat16; C float32 */
+  TK_TAG_C32C64 = 8,     /* A,B interleaved complex-half; C complex64 */
+  TK_TAG_CBF16C64 = 9,   /* A,B interleaved complex-bf16; C complex64 */
+  TK_TAG_DUAL16F32 = 10, /* A,B interleaved dual-half; C dual32 */
+  TK_TAG_DUALBF16F32 = 11
+};
+
+typedef struct TkLayout {
+  int32_t kind;                 /* TkLayoutKind */
+  int32_t pair;                 /* TkPairMode */
+  int32_t scalar;               /* TkScalar of the backing buffer */
+  int32_t reserved;
+  int32_t ndigits[2];           /* digits per logical dimension (1..TK_MAX_DIGITS) */
+  int64_t ext[2][TK_MAX_DIGITS];
+  int64_t stride[2][TK_MAX_DIGITS]; /* in elements (a pair counts as one element) */
+  int64_t plane_stride;         /* SPLIT: element offset of the second plane */
+  int64_t size;                 /* physical_size() in scalars */
+} TkLayout;
+
+typedef struct TkTransform {
+  int32_t n;                    /* number of ops, applied left to right */
+  int32_t op[TK_MAX_TOPS];      /* TkTransformOp */
+  int32_t promote[TK_MAX_TOPS]; /* 1: evaluate in f64 then round to the stream type */
+  double re[TK_MAX_TOPS];       /* constant (real part) */
+  double im[TK_MAX_TOPS];       /* constant (imaginary part, complex streams) */
+} TkTransform;
+
+typedef struct TkGemmPlan {
+  int32_t abi_version;          /* TK_ABI_VERSION */
+  int32_t op;                   /* TkOperator */
+  int32_t compute;              /* accumulator scalar: TK_F32 or TK_F64 */
+  int32_t lane;                 /* TkLane requested */
+  int64_t m, n, k;
+  int64_t op_k;                 /* operator K (chunking of complex/dual products) */
+  int64_t block[3];             /* logical block tile (bm, bn, bk) */
+  TkLayout a, b, c, d;
+  TkTransform t_a, t_b, t_c, t_r2s, t_s2g; /* the five streams, kernel.py:153-157 */
+  int32_t bias_axis;            /* 0 none, 1 bias[j] (axis n), 2 bias[i] (axis m) */
+  int32_t bias_scalar;          /* TkScalar of the bias vector */
+  int32_t predicate;            /* TkPredicate */
+  int32_t reserved;
+} TkGemmPlan;
+
+/* ABI version compiled into the library. */
+int tk_abi_version(void);
+
+/* Lane that tk_gemm would use for this plan (TK_LANE_TCGEN05 / TK_LANE_SIMT), or -1
+ * with tk_last_error() set when the plan is invalid. */
+int tk_plan_lane(const TkGemmPlan* plan);
+
+/* Device workspace (bytes) tk_gemm needs for this plan (de-interleave planes,
+ * row/column sums of affine operand transforms).  Caller allocates it. */
+int64_t tk_workspace_bytes(const TkGemmPlan* plan);
+
+/* Execute one GEMM (replaces kernel.gemm_execute, kernel.py:253-330).
+ * a,b,c,d,bias,kmask are device pointers; d may alias c (gemm_ex is in place,
+ * api.py:161).  kmask: row-major [num_blocks(M/bm * N/bn, column-major block rank)]
+ * x [K/bk] bytes, only read when plan->predicate == TK_PRED_MASK.
+ * Returns TK_OK, TK_ERR_CONFIG (nothing written) or TK_ERR_CUDA. */
+int tk_gemm(const TkGemmPlan* plan, const void* a, const void* b, const void* c, void* d,
+            const void* bias, const uint8_t* kmask, void* workspace, int64_t workspace_bytes,
+            void* stream);
+
+/* BLAS-like entry with the reference's exact parameter list (api.py:335-357).
+ * Column-major as stored: A is m x k (k x m when trans_a), B is k x n (n x k when
+ * trans_b), C is m x n and updated in place.  Host or device pointers. Synchronous. */
+int tk_gemm_ex_raw(int type_tag, int trans_a, int trans_b, long long m, long long n,
+                   long long k, double alpha_re, double alpha_im, void* a, void* b,
+                   double beta_re, double beta_im, void* c);
+
+/* Same, device pointers only, enqueued on `stream` (no host synchronisation). */
+int tk_gemm_ex_raw_async(int type_tag, int trans_a, int trans_b, long long m, long long n,
+                         long long k, double alpha_re, double alpha_im, const void* a,
+                         const void* b, double beta_re, double beta_im, void* c, void* stream);
+
+/* Number of device kernels the last successful tk_gemm / tk_gemm_ex_raw launched. */
+int tk_last_launch_count(void);
+
+/* Message of the last failure in this thread ("" if none). */
+const char* tk_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TK_SM100_H */

@@ -1,0 +1,103 @@
+"""ctypes binding of ``libtk_sm100.so`` (the C ABI in ``include/tk_sm100.h``).
+
+The library is built in-tree by ``__graft_entry__.build()`` (nvcc, sm_100a).  There is
+no fallback: if the shared object is missing or fails to load, every GEMM entry point
+raises ``RuntimeError`` -- the product path never silently runs anywhere but the GPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import c_double, c_int, c_int32, c_int64, c_longlong, c_void_p
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("TK_SM100_LIB", os.path.join(HERE, "libtk_sm100.so"))
+
+ABI_VERSION = 1
+MAX_DIGITS = 3
+MAX_TOPS = 8
+
+LANE_AUTO, LANE_TCGEN05, LANE_SIMT = 0, 1, 2
+LANE_NAMES = {LANE_TCGEN05: "tcgen05", LANE_SIMT: "simt"}
+PRED_ALWAYS, PRED_DIAGONAL, PRED_MASK = 0, 1, 2
+TK_OK, TK_ERR_CONFIG, TK_ERR_CUDA = 0, 1, 2
+
+
+class TkLayout(ctypes.Structure):
+    _fields_ = [
+        ("kind", c_int32), ("pair", c_int32), ("scalar", c_int32), ("reserved", c_int32),
+        ("ndigits", c_int32 * 2),
+        ("ext", (c_int64 * MAX_DIGITS) * 2),
+        ("stride", (c_int64 * MAX_DIGITS) * 2),
+        ("plane_stride", c_int64), ("size", c_int64),
+    ]
+
+
+class TkTransform(ctypes.Structure):
+    _fields_ = [
+        ("n", c_int32), ("op", c_int32 * MAX_TOPS), ("promote", c_int32 * MAX_TOPS),
+        ("re", c_double * MAX_TOPS), ("im", c_double * MAX_TOPS),
+    ]
+
+
+class TkGemmPlan(ctypes.Structure):
+    _fields_ = [
+        ("abi_version", c_int32), ("op", c_int32), ("compute", c_int32), ("lane", c_int32),
+        ("m", c_int64), ("n", c_int64), ("k", c_int64), ("op_k", c_int64),
+        ("block", c_int64 * 3),
+        ("a", TkLayout), ("b", TkLayout), ("c", TkLayout), ("d", TkLayout),
+        ("t_a", TkTransform), ("t_b", TkTransform), ("t_c", TkTransform),
+        ("t_r2s", TkTransform), ("t_s2g", TkTransform),
+        ("bias_axis", c_int32), ("bias_scalar", c_int32), ("predicate", c_int32),
+        ("reserved", c_int32),
+    ]
+
+
+GEMM_EX_ARGTYPES = [c_int, c_int, c_int, c_longlong, c_longlong, c_longlong, c_double,
+                    c_double, c_void_p, c_void_p, c_double, c_double, c_void_p]
+
+# every symbol include/tk_sm100.h declares
+EXPORTED = ("tk_abi_version", "tk_plan_lane", "tk_workspace_bytes", "tk_gemm", "tk_gemm_ex_raw",
+            "tk_gemm_ex_raw_async", "tk_last_launch_count", "tk_last_error")
+
+_lib = None
+_load_error = None
+
+
+def load():
+    """Load (once) and return the ctypes library; raise RuntimeError if unavailable."""
+    global _lib, _load_error
+    if _lib is not None:
+        return _lib
+    if _load_error is not None:
+        raise RuntimeError(_load_error)
+    try:
+        lib = ctypes.CDLL(LIB_PATH)
+    except OSError as exc:
+        _load_error = (f"libtk_sm100.so could not be loaded from {LIB_PATH} ({exc}); build it with "
+                       "`python -c 'import __graft_entry__ as g; g.build()'`")
+        raise RuntimeError(_load_error) from None
+    lib.tk_abi_version.restype = c_int
+    lib.tk_plan_lane.argtypes = [ctypes.POINTER(TkGemmPlan)]
+    lib.tk_plan_lane.restype = c_int
+    lib.tk_workspace_bytes.argtypes = [ctypes.POINTER(TkGemmPlan)]
+    lib.tk_workspace_bytes.restype = c_int64
+    lib.tk_gemm.argtypes = [ctypes.POINTER(TkGemmPlan), c_void_p, c_void_p, c_void_p, c_void_p,
+                            c_void_p, c_void_p, c_void_p, c_int64, c_void_p]
+    lib.tk_gemm.restype = c_int
+    lib.tk_gemm_ex_raw.argtypes = GEMM_EX_ARGTYPES
+    lib.tk_gemm_ex_raw.restype = c_int
+    lib.tk_gemm_ex_raw_async.argtypes = GEMM_EX_ARGTYPES + [c_void_p]
+    lib.tk_gemm_ex_raw_async.restype = c_int
+    lib.tk_last_launch_count.restype = c_int
+    lib.tk_last_error.restype = ctypes.c_char_p
+    if lib.tk_abi_version() != ABI_VERSION:
+        _load_error = f"libtk_sm100.so ABI {lib.tk_abi_version()} != expected {ABI_VERSION}"
+        raise RuntimeError(_load_error)
+    _lib = lib
+    return lib
+
+
+def last_error() -> str:
+    return load().tk_last_error().decode(errors="replace")

@@ -1,0 +1,751 @@
+// tk_api.cu -- the C ABI of libtk_sm100.so (declared in include/tk_sm100.h).
+//
+// Plan validation -> lane selection -> (prep kernels) -> one persistent tcgen05 launch, or the
+// bit-exact CUDA-core lane.  There is no host compute path: every GEMM runs on the device.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <complex>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/tk_sm100.h"
+#include "tk_prep.cuh"
+#include "tk_simt.cuh"
+#include "tk_tc_gemm.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_launches = 0;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define TK_CUDA(call)                                                                 \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      return fail(TK_ERR_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_));       \
+  } while (0)
+
+// ------------------------------------------------------------------ plan checks
+int64_t scalar_bytes(int s) { return s == TK_F16 || s == TK_BF16 ? 2 : s == TK_F32 ? 4 : 8; }
+bool is_half(int s) { return s == TK_F16 || s == TK_BF16; }
+
+int64_t dim_extent(const TkLayout& L, int d) {
+  int64_t e = 1;
+  for (int t = 0; t < L.ndigits[d]; ++t) e *= L.ext[d][t];
+  return e;
+}
+
+int check_layout(const TkLayout& L, const char* name, int64_t r, int64_t c) {
+  if (L.kind < 0 || L.kind > 2) return fail(TK_ERR_CONFIG, "layout %s: bad kind %d", name, L.kind);
+  if (L.scalar < 0 || L.scalar > 3) return fail(TK_ERR_CONFIG, "layout %s: bad scalar", name);
+  if (L.kind == TK_LAYOUT_ZERO) return TK_OK;
+  for (int d = 0; d < 2; ++d)
+    if (L.ndigits[d] < 1 || L.ndigits[d] > TK_MAX_DIGITS)
+      return fail(TK_ERR_CONFIG, "layout %s: bad digit count", name);
+  if (L.kind == TK_LAYOUT_DIAGONAL) {
+    if (r != c) return fail(TK_ERR_CONFIG, "layout %s: Diagonal needs a square matrix", name);
+    if (L.size < r) return fail(TK_ERR_CONFIG, "layout %s: diagonal buffer too small", name);
+    return TK_OK;
+  }
+  if (dim_extent(L, 0) != r || dim_extent(L, 1) != c)
+    return fail(TK_ERR_CONFIG, "layout %s: extents (%lld, %lld) != expected (%lld, %lld)", name,
+                (long long)dim_extent(L, 0), (long long)dim_extent(L, 1), (long long)r, (long long)c);
+  // largest reachable element offset must lie inside the buffer
+  int64_t maxoff = 0;
+  for (int d = 0; d < 2; ++d)
+    for (int t = 0; t < L.ndigits[d]; ++t) {
+      if (L.stride[d][t] < 0) return fail(TK_ERR_CONFIG, "layout %s: negative stride", name);
+      maxoff += (L.ext[d][t] - 1) * L.stride[d][t];
+    }
+  int64_t need = maxoff + 1;
+  if (L.pair == TK_PAIR_INTERLEAVED) need = 2 * need;
+  else if (L.pair == TK_PAIR_SPLIT) need = L.plane_stride + need;
+  if (need > L.size) return fail(TK_ERR_CONFIG, "layout %s: addresses beyond physical size", name);
+  return TK_OK;
+}
+
+int check_transform(const TkTransform& t, const char* name) {
+  if (t.n < 0 || t.n > TK_MAX_TOPS) return fail(TK_ERR_CONFIG, "transform %s: bad length", name);
+  for (int i = 0; i < t.n; ++i)
+    if (t.op[i] < TK_T_SCALE || t.op[i] > TK_T_RELU)
+      return fail(TK_ERR_CONFIG, "transform %s: bad op %d", name, t.op[i]);
+  return TK_OK;
+}
+
+int check_plan(const TkGemmPlan* p) {
+  if (!p) return fail(TK_ERR_CONFIG, "null plan");
+  if (p->abi_version != TK_ABI_VERSION)
+    return fail(TK_ERR_CONFIG, "plan ABI version %d != library %d", p->abi_version, TK_ABI_VERSION);
+  if (p->m < 1 || p->n < 1 || p->k < 1) return fail(TK_ERR_CONFIG, "GEMM extents must be >= 1");
+  if (p->op < TK_OP_REAL || p->op > TK_OP_DUAL) return fail(TK_ERR_CONFIG, "bad operator");
+  if (p->compute != TK_F32 && p->compute != TK_F64)
+    return fail(TK_ERR_CONFIG, "accumulator must be f32 or f64");
+  for (int d = 0; d < 3; ++d)
+    if (p->block[d] < 1) return fail(TK_ERR_CONFIG, "block tile must be positive");
+  if (p->m % p->block[0] || p->n % p->block[1] || p->k % p->block[2])
+    return fail(TK_ERR_CONFIG, "block tile must divide GEMM shape");
+  if (p->op_k < 1 || p->block[2] % p->op_k) return fail(TK_ERR_CONFIG, "operator K must divide block K");
+  int rc;
+  if ((rc = check_layout(p->a, "A", p->m, p->k))) return rc;
+  if ((rc = check_layout(p->b, "B", p->k, p->n))) return rc;
+  if ((rc = check_layout(p->c, "C", p->m, p->n))) return rc;
+  if ((rc = check_layout(p->d, "D", p->m, p->n))) return rc;
+  if (p->d.kind != TK_LAYOUT_STRIDED) return fail(TK_ERR_CONFIG, "D must be a strided layout");
+  if (p->b.kind == TK_LAYOUT_DIAGONAL) return fail(TK_ERR_CONFIG, "Diagonal B is not supported");
+  const bool pair = p->op != TK_OP_REAL;
+  const TkLayout* ls[4] = {&p->a, &p->b, &p->c, &p->d};
+  for (const TkLayout* L : ls)
+    if (L->kind == TK_LAYOUT_STRIDED && (L->pair != TK_PAIR_NONE) != pair)
+      return fail(TK_ERR_CONFIG, "pair layouts must match the operator");
+  if (pair && p->a.kind == TK_LAYOUT_DIAGONAL)
+    return fail(TK_ERR_CONFIG, "Diagonal A needs the real operator");
+  if ((rc = check_transform(p->t_a, "g2s_a")) || (rc = check_transform(p->t_b, "g2s_b")) ||
+      (rc = check_transform(p->t_c, "g2s_c")) || (rc = check_transform(p->t_r2s, "r2s_d")) ||
+      (rc = check_transform(p->t_s2g, "s2g_d")))
+    return rc;
+  if (pair) {
+    const TkTransform* ts[5] = {&p->t_a, &p->t_b, &p->t_c, &p->t_r2s, &p->t_s2g};
+    for (const TkTransform* t : ts)
+      for (int i = 0; i < t->n; ++i) {
+        if (t->op[i] == TK_T_RELU) return fail(TK_ERR_CONFIG, "relu is undefined on pair elements");
+        if (p->op == TK_OP_DUAL && t->op[i] == TK_T_ADD)
+          return fail(TK_ERR_CONFIG, "add_constant is undefined on dual elements");
+      }
+    if (p->bias_axis) return fail(TK_ERR_CONFIG, "bias epilogue needs the real operator");
+  }
+  if (p->bias_axis < 0 || p->bias_axis > 2) return fail(TK_ERR_CONFIG, "bad bias axis");
+  if (p->predicate < 0 || p->predicate > 2) return fail(TK_ERR_CONFIG, "bad predicate");
+  const bool a64 = p->a.scalar == TK_F64;
+  if (p->compute == TK_F32 && a64) return fail(TK_ERR_CONFIG, "f64 storage needs f64 accumulation");
+  return TK_OK;
+}
+
+// ------------------------------------------------------------------ lane selection
+bool affine_of(const TkTransform& t, double& alpha, double& beta) {
+  alpha = 1.0;
+  beta = 0.0;
+  for (int i = 0; i < t.n; ++i) {
+    if (t.op[i] == TK_T_SCALE) { alpha *= t.re[i]; beta *= t.re[i]; }
+    else if (t.op[i] == TK_T_ADD) beta += t.re[i];
+    else return false;
+  }
+  return true;
+}
+
+// strided operand the tensor cores can take straight from TMA: one digit per dimension,
+// one unit-stride dimension, 16-byte aligned pitch.
+bool tma_operand(const TkLayout& L, int& mn_major_dim0, int64_t& pitch) {
+  if (L.kind != TK_LAYOUT_STRIDED || L.ndigits[0] != 1 || L.ndigits[1] != 1) return false;
+  const int64_t s0 = L.stride[0][0], s1 = L.stride[1][0];
+  if (s0 == 1 && (s1 * 2) % 16 == 0 && s1 >= L.ext[0][0]) { mn_major_dim0 = 1; pitch = s1; }
+  else if (s1 == 1 && (s0 * 2) % 16 == 0 && s0 >= L.ext[1][0]) { mn_major_dim0 = 0; pitch = s0; }
+  else return false;
+  if (L.pair == TK_PAIR_SPLIT && (L.plane_stride * 2) % 16 != 0) return false;
+  if (L.pair == TK_PAIR_INTERLEAVED) {  // de-interleaved into dense planes: must be a bijection
+    const int64_t vol = L.ext[0][0] * L.ext[1][0];
+    if (pitch != (mn_major_dim0 ? L.ext[0][0] : L.ext[1][0])) return false;
+    if (2 * vol > L.size) return false;
+  }
+  return true;
+}
+
+bool tc_lane_ok(const TkGemmPlan* p, std::string& why) {
+  auto no = [&](const char* w) { why = w; return false; };
+  if (p->compute != TK_F32) return no("tcgen05 lane accumulates in f32 only");
+  if (!is_half(p->a.scalar) || p->b.scalar != p->a.scalar) return no("A/B must be f16 or bf16");
+  if (p->b.kind != TK_LAYOUT_STRIDED) return no("B must be strided");
+  int mn;
+  int64_t pitch;
+  if (p->a.kind == TK_LAYOUT_DIAGONAL) {
+    if (p->op != TK_OP_REAL || p->t_a.n) return no("Diagonal A only with real op, identity g2s_a");
+  } else if (!tma_operand(p->a, mn, pitch)) {
+    return no("A layout is not TMA-compatible");
+  }
+  if (!tma_operand(p->b, mn, pitch)) return no("B layout is not TMA-compatible");
+  if (p->c.kind != TK_LAYOUT_ZERO && p->c.scalar != TK_F32) return no("C must be f32");
+  if (p->d.scalar != TK_F32) return no("D must be f32");
+  if (p->c.kind == TK_LAYOUT_DIAGONAL) return no("Diagonal C unsupported on tcgen05 lane");
+  double al, be;
+  if (!affine_of(p->t_a, al, be) || !affine_of(p->t_b, al, be)) return no("non-affine A/B transform");
+  if (p->op != TK_OP_REAL && (p->t_a.n || p->t_b.n)) return no("pair operands need identity g2s");
+  if (p->predicate == TK_PRED_MASK) return no("arbitrary predicates run on the exact lane");
+  if (p->predicate == TK_PRED_DIAGONAL && p->a.kind != TK_LAYOUT_DIAGONAL)
+    return no("diagonal predicate over a dense A runs on the exact lane");
+  if (p->bias_axis && p->bias_scalar != TK_F32) return no("bias must be f32");
+  if (p->m >= (1ll << 31) || p->n >= (1ll << 31) || p->k >= (1ll << 31)) return no("extent >= 2^31");
+  return true;
+}
+
+int choose_lane(const TkGemmPlan* p, std::string* why_out = nullptr) {
+  std::string why;
+  const bool tc = tc_lane_ok(p, why);
+  if (why_out) *why_out = why;
+  if (p->lane == TK_LANE_TCGEN05 && !tc) return -1;
+  if (p->lane == TK_LANE_SIMT) return TK_LANE_SIMT;
+  return tc ? TK_LANE_TCGEN05 : TK_LANE_SIMT;
+}
+
+// ------------------------------------------------------------------ workspace plan
+struct Workspace {
+  int64_t a_planes = -1, b_planes = -1, rowsum = -1, colsum = -1, total = 0;
+};
+
+int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
+
+Workspace plan_workspace(const TkGemmPlan* p, int lane) {
+  Workspace w;
+  if (lane != TK_LANE_TCGEN05) return w;
+  if (p->a.kind == TK_LAYOUT_STRIDED && p->a.pair == TK_PAIR_INTERLEAVED) {
+    w.a_planes = w.total;
+    w.total += align256(p->m * p->k * 2 * 2);
+  }
+  if (p->b.pair == TK_PAIR_INTERLEAVED) {
+    w.b_planes = w.total;
+    w.total += align256(p->k * p->n * 2 * 2);
+  }
+  double aa, ba, ab, bb;
+  affine_of(p->t_a, aa, ba);
+  affine_of(p->t_b, ab, bb);
+  if (p->op == TK_OP_REAL && bb != 0.0) { w.rowsum = w.total; w.total += align256(p->m * 4); }
+  if (p->op == TK_OP_REAL && ba != 0.0) { w.colsum = w.total; w.total += align256(p->n * 4); }
+  return w;
+}
+
+// ------------------------------------------------------------------ TMA
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  });
+  return fn;
+}
+
+int make_map_2d(CUtensorMap* map, const void* base, int scalar, uint64_t inner, uint64_t outer,
+                uint64_t pitch_elems, uint32_t box_inner, uint32_t box_outer) {
+  auto enc = get_encode();
+  if (!enc) return fail(TK_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {pitch_elems * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, scalar == TK_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                   2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(TK_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
+  return TK_OK;
+}
+
+tk::DigitMap to_map(const TkLayout& L) {
+  tk::DigitMap m{};
+  for (int d = 0; d < 2; ++d) {
+    m.nd[d] = L.kind == TK_LAYOUT_STRIDED ? L.ndigits[d] : 1;
+    for (int t = 0; t < 3; ++t) {
+      m.e[d][t] = t < L.ndigits[d] ? L.ext[d][t] : 1;
+      m.s[d][t] = t < L.ndigits[d] ? L.stride[d][t] : 0;
+    }
+  }
+  return m;
+}
+
+tk::EpiProg to_prog(const TkTransform& t) {
+  tk::EpiProg g{};
+  g.n = t.n;
+  for (int i = 0; i < t.n; ++i) {
+    g.op[i] = t.op[i];
+    g.promote[i] = t.promote[i];
+    g.fre[i] = float(t.re[i]);
+    g.fim[i] = float(t.im[i]);
+    g.dre[i] = t.re[i];
+    g.dim[i] = t.im[i];
+  }
+  return g;
+}
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int OP>
+int launch_tc(const tk::TcParams& prm, cudaStream_t s) {
+  using S = tk::TcSmem<OP>;
+  static bool attr = false;
+  if (!attr) {
+    TK_CUDA(cudaFuncSetAttribute(tk::tc_gemm_kernel<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL));
+    attr = true;
+  }
+  const int grid = std::min(prm.num_tiles, sm_count());
+  tk::tc_gemm_kernel<OP><<<grid, tk::TC_THREADS, S::TOTAL, s>>>(prm);
+  TK_CUDA(cudaGetLastError());
+  ++g_launches;
+  return TK_OK;
+}
+
+int run_tc(const TkGemmPlan* p, const void* a, const void* b, const void* c, void* d, const void* bias,
+           uint8_t* ws, const Workspace& w, cudaStream_t s) {
+  tk::TcParams prm;
+  memset(&prm, 0, sizeof(prm));
+  const int op = p->op;
+  const int planes = op == TK_OP_REAL ? 1 : 2;
+  const int BN = op == TK_OP_REAL ? tk::TcCfg<tk::OP_REAL>::BN : tk::TcCfg<tk::OP_COMPLEX>::BN;
+  prm.m = int(p->m);
+  prm.n = int(p->n);
+  prm.k = int(p->k);
+  prm.ab_fmt = p->a.scalar == TK_BF16 ? 1 : 0;
+  const int64_t ha = 2;  // bytes per half scalar
+
+  // ---- A operand
+  const void* a_pl[2] = {a, nullptr};
+  if (p->a.kind == TK_LAYOUT_DIAGONAL) {
+    prm.diag_a = 1;
+    prm.diag = a;
+  } else {
+    int mn;
+    int64_t pitch;
+    tma_operand(p->a, mn, pitch);
+    prm.a_mn = mn;
+    if (p->a.pair == TK_PAIR_SPLIT) {
+      a_pl[1] = static_cast<const uint8_t*>(a) + p->a.plane_stride * ha;
+    } else if (p->a.pair == TK_PAIR_INTERLEAVED) {
+      const int64_t vol = p->m * p->k;
+      uint16_t* p0 = reinterpret_cast<uint16_t*>(ws + w.a_planes);
+      tk::deinterleave_kernel<<<std::min<int64_t>((vol + 1023) / 1024, 4 * sm_count()), 256, 0, s>>>(
+          static_cast<const uint32_t*>(a), p0, p0 + vol, vol);
+      TK_CUDA(cudaGetLastError());
+      ++g_launches;
+      a_pl[0] = p0;
+      a_pl[1] = p0 + vol;
+    }
+    for (int pl = 0; pl < planes; ++pl) {
+      int rc = mn ? make_map_2d(&prm.ta[pl], a_pl[pl], p->a.scalar, p->m, p->k, pitch, 64, 64)
+                  : make_map_2d(&prm.ta[pl], a_pl[pl], p->a.scalar, p->k, p->m, pitch, 64, 128);
+      if (rc) return rc;
+    }
+  }
+  // ---- B operand
+  {
+    int mn_k;  // 1: dim0 (K) contiguous -> K-major smem; 0: N contiguous -> MN-major
+    int64_t pitch;
+    tma_operand(p->b, mn_k, pitch);
+    prm.b_mn = mn_k ? 0 : 1;
+    const void* b_pl[2] = {b, nullptr};
+    if (p->b.pair == TK_PAIR_SPLIT) {
+      b_pl[1] = static_cast<const uint8_t*>(b) + p->b.plane_stride * ha;
+    } else if (p->b.pair == TK_PAIR_INTERLEAVED) {
+      const int64_t vol = p->k * p->n;
+      uint16_t* p0 = reinterpret_cast<uint16_t*>(ws + w.b_planes);
+      tk::deinterleave_kernel<<<std::min<int64_t>((vol + 1023) / 1024, 4 * sm_count()), 256, 0, s>>>(
+          static_cast<const uint32_t*>(b), p0, p0 + vol, vol);
+      TK_CUDA(cudaGetLastError());
+      ++g_launches;
+      b_pl[0] = p0;
+      b_pl[1] = p0 + vol;
+    }
+    for (int pl = 0; pl < planes; ++pl) {
+      int rc = mn_k ? make_map_2d(&prm.tb[pl], b_pl[pl], p->b.scalar, p->k, p->n, pitch, 64, BN)
+                    : make_map_2d(&prm.tb[pl], b_pl[pl], p->b.scalar, p->n, p->k, pitch, 64, 64);
+      if (rc) return rc;
+    }
+  }
+  // ---- affine operand transforms -> epilogue terms
+  double aa, ba, ab, bb;
+  affine_of(p->t_a, aa, ba);
+  affine_of(p->t_b, ab, bb);
+  if (op == TK_OP_REAL && (aa != 1.0 || ba != 0.0 || ab != 1.0 || bb != 0.0)) {
+    prm.affine = 1;
+    prm.aff_s = float(aa * ab);
+    prm.aff_r = float(aa * bb);
+    prm.aff_q = float(ba * ab);
+    prm.aff_k = float(double(p->k) * ba * bb);
+    auto row_sums = [&](const TkLayout& L, const void* x, float* out, int64_t count, int64_t len,
+                        int dim_count) -> int {
+      // sums over the other dimension for each index of dim `dim_count`
+      const int64_t s_count = L.stride[dim_count][0], s_len = L.stride[1 - dim_count][0];
+      if (s_count == 1) {
+        const int blocks = int((count + 255) / 256);
+        if (L.scalar == TK_F16)
+          tk::strided_sum_unit_kernel<__half><<<blocks, 256, 0, s>>>(static_cast<const __half*>(x), out, count, len, s_len);
+        else
+          tk::strided_sum_unit_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x), out, count, len, s_len);
+      } else {
+        const int blocks = int((count * 32 + 255) / 256);
+        if (L.scalar == TK_F16)
+          tk::strided_sum_kernel<__half><<<blocks, 256, 0, s>>>(static_cast<const __half*>(x), out, count, len, s_count, s_len);
+        else
+          tk::strided_sum_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x), out, count, len, s_count, s_len);
+      }
+      TK_CUDA(cudaGetLastError());
+      ++g_launches;
+      return TK_OK;
+    };
+    if (w.rowsum >= 0) {
+      prm.rowsum_a = reinterpret_cast<float*>(ws + w.rowsum);
+      int rc = row_sums(p->a, a, reinterpret_cast<float*>(ws + w.rowsum), p->m, p->k, 0);
+      if (rc) return rc;
+    }
+    if (w.colsum >= 0) {
+      prm.colsum_b = reinterpret_cast<float*>(ws + w.colsum);
+      int rc = row_sums(p->b, b, reinterpret_cast<float*>(ws + w.colsum), p->n, p->k, 1);
+      if (rc) return rc;
+    }
+  }
+  // ---- epilogue
+  prm.c_zero = p->c.kind == TK_LAYOUT_ZERO;
+  prm.c_pair = p->c.pair;
+  prm.d_pair = p->d.pair;
+  prm.c_ptr = c;
+  prm.d_ptr = d;
+  prm.c_map = to_map(p->c);
+  prm.d_map = to_map(p->d);
+  prm.c_plane = p->c.plane_stride;
+  prm.d_plane = p->d.plane_stride;
+  prm.bias_axis = p->bias_axis;
+  prm.bias = static_cast<const float*>(bias);
+  prm.t_c = to_prog(p->t_c);
+  prm.t_r2s = to_prog(p->t_r2s);
+  prm.t_s2g = to_prog(p->t_s2g);
+  // ---- schedule
+  prm.num_mb = int((p->m + tk::TC_BM - 1) / tk::TC_BM);
+  prm.num_nb = int((p->n + BN - 1) / BN);
+  prm.num_tiles = prm.num_mb * prm.num_nb;
+  prm.kb_total = int((p->k + tk::TC_BK - 1) / tk::TC_BK);
+  prm.group_m = 16;
+  switch (op) {
+    case TK_OP_REAL: return launch_tc<tk::OP_REAL>(prm, s);
+    case TK_OP_COMPLEX: return launch_tc<tk::OP_COMPLEX>(prm, s);
+    default: return launch_tc<tk::OP_DUAL>(prm, s);
+  }
+}
+
+tk::SimtLayout to_simt(const TkLayout& L, const void* ptr) {
+  tk::SimtLayout s{};
+  s.kind = L.kind;
+  s.pair = L.pair;
+  s.scalar = L.scalar;
+  s.map = to_map(L);
+  s.plane = L.plane_stride;
+  s.ptr = ptr;
+  return s;
+}
+
+template <int OP, typename T, typename Acc>
+int launch_simt(const tk::SimtParams& sp, cudaStream_t s) {
+  const int64_t total = sp.m * sp.n;
+  const int threads = 128;
+  tk::simt_gemm_kernel<OP, T, Acc><<<int((total + threads - 1) / threads), threads, 0, s>>>(sp);
+  TK_CUDA(cudaGetLastError());
+  ++g_launches;
+  return TK_OK;
+}
+
+template <int OP>
+int dispatch_simt(const TkGemmPlan* p, const tk::SimtParams& sp, cudaStream_t s) {
+  const bool t64 = p->a.scalar == TK_F64 || p->b.scalar == TK_F64;
+  if (t64) return launch_simt<OP, double, double>(sp, s);
+  if (p->compute == TK_F64) return launch_simt<OP, float, double>(sp, s);
+  return launch_simt<OP, float, float>(sp, s);
+}
+
+int run_simt(const TkGemmPlan* p, const void* a, const void* b, const void* c, void* d, const void* bias,
+             const uint8_t* kmask, cudaStream_t s) {
+  tk::SimtParams sp;
+  memset(&sp, 0, sizeof(sp));
+  sp.m = p->m;
+  sp.n = p->n;
+  sp.k = p->k;
+  sp.op_k = p->op_k;
+  sp.bm = p->block[0];
+  sp.bn = p->block[1];
+  sp.bk = p->block[2];
+  sp.predicate = p->predicate;
+  sp.bias_axis = p->bias_axis;
+  sp.bias_scalar = p->bias_scalar;
+  sp.kmask = kmask;
+  sp.bias = bias;
+  sp.a = to_simt(p->a, a);
+  sp.b = to_simt(p->b, b);
+  sp.c = to_simt(p->c, c);
+  sp.d = to_simt(p->d, d);
+  sp.t_a = to_prog(p->t_a);
+  sp.t_b = to_prog(p->t_b);
+  sp.t_c = to_prog(p->t_c);
+  sp.t_r2s = to_prog(p->t_r2s);
+  sp.t_s2g = to_prog(p->t_s2g);
+  switch (p->op) {
+    case TK_OP_REAL: return dispatch_simt<tk::OP_REAL>(p, sp, s);
+    case TK_OP_COMPLEX: return dispatch_simt<tk::OP_COMPLEX>(p, sp, s);
+    default: return dispatch_simt<tk::OP_DUAL>(p, sp, s);
+  }
+}
+
+bool aligned16(const void* x) { return (reinterpret_cast<uintptr_t>(x) & 15) == 0; }
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+int tk_abi_version(void) { return TK_ABI_VERSION; }
+
+const char* tk_last_error(void) { return g_err.c_str(); }
+
+int tk_last_launch_count(void) { return g_launches; }
+
+int tk_plan_lane(const TkGemmPlan* plan) {
+  if (check_plan(plan)) return -1;
+  std::string why;
+  int lane = choose_lane(plan, &why);
+  if (lane < 0) {
+    fail(TK_ERR_CONFIG, "tcgen05 lane requested but not applicable: %s", why.c_str());
+    return -1;
+  }
+  return lane;
+}
+
+int64_t tk_workspace_bytes(const TkGemmPlan* plan) {
+  if (check_plan(plan)) return -1;
+  int lane = choose_lane(plan);
+  if (lane < 0) return -1;
+  return plan_workspace(plan, lane).total;
+}
+
+int tk_gemm(const TkGemmPlan* plan, const void* a, const void* b, const void* c, void* d, const void* bias,
+            const uint8_t* kmask, void* workspace, int64_t workspace_bytes, void* stream) {
+  g_err.clear();
+  g_launches = 0;
+  int rc = check_plan(plan);
+  if (rc) return rc;
+  std::string why;
+  int lane = choose_lane(plan, &why);
+  if (lane < 0) return fail(TK_ERR_CONFIG, "tcgen05 lane requested but not applicable: %s", why.c_str());
+  if (plan->bias_axis && !bias) return fail(TK_ERR_CONFIG, "bias epilogue without a bias vector");
+  if (plan->predicate == TK_PRED_MASK && !kmask) return fail(TK_ERR_CONFIG, "mask predicate without a mask");
+  if (lane == TK_LANE_TCGEN05) {
+    const bool ok = (plan->a.kind != TK_LAYOUT_STRIDED || aligned16(a)) && aligned16(b);
+    if (!ok) {
+      if (plan->lane == TK_LANE_TCGEN05) return fail(TK_ERR_CONFIG, "operands not 16-byte aligned");
+      lane = TK_LANE_SIMT;
+    }
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (lane == TK_LANE_TCGEN05) {
+    Workspace w = plan_workspace(plan, lane);
+    if (w.total > 0 && (!workspace || workspace_bytes < w.total))
+      return fail(TK_ERR_CONFIG, "workspace of %lld bytes required", (long long)w.total);
+    return run_tc(plan, a, b, c, d, bias, static_cast<uint8_t*>(workspace), w, s);
+  }
+  return run_simt(plan, a, b, c, d, bias, kmask, s);
+}
+
+}  // extern "C"
+
+// ====================================================================== gemm_ex_raw
+namespace {
+
+void set_dense(TkLayout& L, int scalar, int pair, int64_t rows, int64_t cols, bool row_major) {
+  memset(&L, 0, sizeof(L));
+  L.kind = TK_LAYOUT_STRIDED;
+  L.pair = pair;
+  L.scalar = scalar;
+  L.ndigits[0] = L.ndigits[1] = 1;
+  L.ext[0][0] = rows;
+  L.ext[1][0] = cols;
+  L.stride[0][0] = row_major ? cols : 1;
+  L.stride[1][0] = row_major ? 1 : rows;
+  L.plane_stride = pair == TK_PAIR_SPLIT ? rows * cols : 0;
+  L.size = rows * cols * (pair ? 2 : 1);
+}
+
+void set_scale(TkTransform& t, double re, double im) {
+  memset(&t, 0, sizeof(t));
+  t.n = 1;
+  t.op[0] = TK_T_SCALE;
+  t.re[0] = re;
+  t.im[0] = im;
+}
+
+struct TagInfo {
+  int ab_scalar, c_scalar, op, compute;
+};
+
+bool tag_info(int tag, TagInfo& ti) {
+  switch (tag) {
+    case TK_TAG_F32: ti = {TK_F32, TK_F32, TK_OP_REAL, TK_F32}; return true;
+    case TK_TAG_F64: ti = {TK_F64, TK_F64, TK_OP_REAL, TK_F64}; return true;
+    case TK_TAG_C64: ti = {TK_F32, TK_F32, TK_OP_COMPLEX, TK_F32}; return true;
+    case TK_TAG_C128: ti = {TK_F64, TK_F64, TK_OP_COMPLEX, TK_F64}; return true;
+    case TK_TAG_DUAL32: ti = {TK_F32, TK_F32, TK_OP_DUAL, TK_F32}; return true;
+    case TK_TAG_DUAL64: ti = {TK_F64, TK_F64, TK_OP_DUAL, TK_F64}; return true;
+    case TK_TAG_F16F32: ti = {TK_F16, TK_F32, TK_OP_REAL, TK_F32}; return true;
+    case TK_TAG_BF16F32: ti = {TK_BF16, TK_F32, TK_OP_REAL, TK_F32}; return true;
+    case TK_TAG_C32C64: ti = {TK_F16, TK_F32, TK_OP_COMPLEX, TK_F32}; return true;
+    case TK_TAG_CBF16C64: ti = {TK_BF16, TK_F32, TK_OP_COMPLEX, TK_F32}; return true;
+    case TK_TAG_DUAL16F32: ti = {TK_F16, TK_F32, TK_OP_DUAL, TK_F32}; return true;
+    case TK_TAG_DUALBF16F32: ti = {TK_BF16, TK_F32, TK_OP_DUAL, TK_F32}; return true;
+    default: return false;
+  }
+}
+
+// The reference's block-tile heuristic (components.py:196-240) at the default operator
+// shape (8,8,8) and 64 KiB budget: gemm_ex_raw reports status 1 exactly when it finds none.
+bool reference_block_tile(int64_t m, int64_t n, int64_t k, int64_t shared_scalar_bytes, int pair,
+                          int64_t block[3]) {
+  const int64_t op = 8, budget = 64 * 1024;
+  if (k % op) return false;
+  int64_t best_area = -1;
+  bool best_square = false;
+  for (int64_t bn = 1; bn <= n; bn <<= 1) {
+    if (bn % op || n % bn) continue;
+    for (int64_t bm : {bn, 2 * bn}) {
+      if (bm > m || bm % op || m % bm) continue;
+      const int64_t foot = (bm * op + op * bn) * (pair ? 2 : 1) * shared_scalar_bytes;
+      if (foot > budget) continue;
+      const bool square = bm == bn;
+      if (bm * bn > best_area || (bm * bn == best_area && square && !best_square)) {
+        best_area = bm * bn;
+        best_square = square;
+        block[0] = bm;
+        block[1] = bn;
+        block[2] = op;
+      }
+    }
+  }
+  return best_area > 0;
+}
+
+int build_ex_plan(TkGemmPlan& p, int tag, int ta, int tb, long long m, long long n, long long k,
+                  double are, double aim, double bre, double bim) {
+  TagInfo ti;
+  if (!tag_info(tag, ti)) return fail(TK_ERR_CONFIG, "unknown type tag %d", tag);
+  if (m < 1 || n < 1 || k < 1) return fail(TK_ERR_CONFIG, "extents must be >= 1");
+  memset(&p, 0, sizeof(p));
+  p.abi_version = TK_ABI_VERSION;
+  p.op = ti.op;
+  p.compute = ti.compute;
+  p.lane = TK_LANE_AUTO;
+  p.m = m;
+  p.n = n;
+  p.k = k;
+  p.op_k = 8;
+  const int pair = ti.op == TK_OP_REAL ? TK_PAIR_NONE : TK_PAIR_INTERLEAVED;
+  if (!reference_block_tile(m, n, k, scalar_bytes(ti.ab_scalar), pair, p.block))
+    return fail(TK_ERR_CONFIG, "no feasible block tile (reference heuristic) for (%lld, %lld, %lld)",
+                m, n, k);
+  const bool cplx = ti.op == TK_OP_COMPLEX;
+  if (!cplx) { aim = 0.0; bim = 0.0; }
+  const std::complex<double> alpha(are, aim), beta(bre, bim);
+  set_dense(p.c, ti.c_scalar, pair, m, n, false);
+  p.d = p.c;
+  if (alpha == 0.0) {
+    memset(&p.a, 0, sizeof(p.a));
+    p.a.kind = TK_LAYOUT_ZERO;
+    p.a.scalar = ti.ab_scalar;
+    p.b = p.a;
+    set_scale(p.t_c, beta.real(), beta.imag());
+  } else {
+    set_dense(p.a, ti.ab_scalar, pair, m, k, ta != 0);
+    set_dense(p.b, ti.ab_scalar, pair, k, n, tb != 0);
+    const std::complex<double> q = beta / alpha;
+    if (q != 1.0) set_scale(p.t_c, q.real(), q.imag());
+    if (alpha != 1.0) set_scale(p.t_r2s, alpha.real(), alpha.imag());
+  }
+  return TK_OK;
+}
+
+int64_t elems_of(const TkLayout& L) { return L.kind == TK_LAYOUT_ZERO ? 0 : L.size; }
+
+}  // namespace
+
+extern "C" int tk_gemm_ex_raw_async(int tag, int ta, int tb, long long m, long long n, long long k,
+                                    double are, double aim, const void* a, const void* b, double bre,
+                                    double bim, void* c, void* stream) {
+  g_err.clear();
+  TkGemmPlan p;
+  int rc = build_ex_plan(p, tag, ta, tb, m, n, k, are, aim, bre, bim);
+  if (rc) return rc;
+  int lane = choose_lane(&p);
+  Workspace w = plan_workspace(&p, lane);
+  void* ws = nullptr;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (w.total) TK_CUDA(cudaMallocAsync(&ws, w.total, s));
+  rc = tk_gemm(&p, a, b, c, c, nullptr, nullptr, ws, w.total, stream);
+  if (ws) cudaFreeAsync(ws, s);
+  return rc;
+}
+
+extern "C" int tk_gemm_ex_raw(int tag, int ta, int tb, long long m, long long n, long long k,
+                              double are, double aim, void* a, void* b, double bre, double bim, void* c) {
+  g_err.clear();
+  TkGemmPlan p;
+  int rc = build_ex_plan(p, tag, ta, tb, m, n, k, are, aim, bre, bim);
+  if (rc) return rc;
+  // host pointers (the reference's numpy buffers) are staged through device memory
+  auto on_device = [](const void* ptr) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+  };
+  const int64_t sa = elems_of(p.a) * scalar_bytes(p.a.scalar);
+  const int64_t sb = elems_of(p.b) * scalar_bytes(p.b.scalar);
+  const int64_t sc = p.c.size * scalar_bytes(p.c.scalar);
+  const bool dev = on_device(c) && (sa == 0 || on_device(a)) && (sb == 0 || on_device(b));
+  if (dev) {
+    rc = tk_gemm_ex_raw_async(tag, ta, tb, m, n, k, are, aim, a, b, bre, bim, c, nullptr);
+    if (rc) return rc;
+    TK_CUDA(cudaDeviceSynchronize());
+    return TK_OK;
+  }
+  void *da = nullptr, *db = nullptr, *dc = nullptr;
+  auto cleanup = [&] {
+    if (da) cudaFree(da);
+    if (db) cudaFree(db);
+    if (dc) cudaFree(dc);
+  };
+  if ((sa && cudaMalloc(&da, sa) != cudaSuccess) || (sb && cudaMalloc(&db, sb) != cudaSuccess) ||
+      cudaMalloc(&dc, sc) != cudaSuccess) {
+    cleanup();
+    return fail(TK_ERR_CUDA, "device allocation failed");
+  }
+  if ((sa && cudaMemcpy(da, a, sa, cudaMemcpyHostToDevice) != cudaSuccess) ||
+      (sb && cudaMemcpy(db, b, sb, cudaMemcpyHostToDevice) != cudaSuccess) ||
+      cudaMemcpy(dc, c, sc, cudaMemcpyHostToDevice) != cudaSuccess) {
+    cleanup();
+    return fail(TK_ERR_CUDA, "host-to-device copy failed");
+  }
+  rc = tk_gemm_ex_raw_async(tag, ta, tb, m, n, k, are, aim, da, db, bre, bim, dc, nullptr);
+  if (rc == TK_OK && cudaMemcpy(c, dc, sc, cudaMemcpyDeviceToHost) != cudaSuccess)
+    rc = fail(TK_ERR_CUDA, "device-to-host copy failed");
+  cleanup();
+  return rc;
+}

@@ -1,0 +1,72 @@
+// tk_prep.cuh -- small HBM-bound helper kernels that run before the tcgen05 GEMM.
+//   * deinterleave: (re,im)/(value,eps) interleaved half pairs -> two planes, so the operand
+//     reaches the tensor cores through plain 2-D TMA maps (the paper's "interleaved global,
+//     split shared" composition, reference api.py:243-250).  TMA cannot stride dimension 0,
+//     so the de-interleave cannot be folded into the tensor map itself.
+//   * sum_rows / sum_cols: row sums of A and column sums of B; with them an affine operand
+//     transform T(x) = alpha*x + beta on the A/B streams (add_constant / scale,
+//     components.py:60-78) is applied exactly in the epilogue:
+//       sum_k Ta(A_ik) Tb(B_kj) = aa*ab*S_ij + aa*bb*R_i + ba*ab*Q_j + K*ba*bb
+#pragma once
+#include "tk_types.cuh"
+
+namespace tk {
+
+__global__ void deinterleave_kernel(const uint32_t* __restrict__ src, uint16_t* __restrict__ p0,
+                                    uint16_t* __restrict__ p1, int64_t n) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x * 4;
+  for (int64_t e = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4; e < n; e += stride) {
+    if (e + 4 <= n && (reinterpret_cast<uintptr_t>(src + e) & 15) == 0 &&
+        (reinterpret_cast<uintptr_t>(p0 + e) & 7) == 0 && (reinterpret_cast<uintptr_t>(p1 + e) & 7) == 0) {
+      const uint4 v = *reinterpret_cast<const uint4*>(src + e);
+      uint2 lo, hi;
+      lo.x = (v.x & 0xFFFFu) | (v.y << 16);
+      lo.y = (v.z & 0xFFFFu) | (v.w << 16);
+      hi.x = (v.x >> 16) | (v.y & 0xFFFF0000u);
+      hi.y = (v.z >> 16) | (v.w & 0xFFFF0000u);
+      *reinterpret_cast<uint2*>(p0 + e) = lo;
+      *reinterpret_cast<uint2*>(p1 + e) = hi;
+    } else {
+      for (int64_t q = e; q < min(n, e + 4); ++q) {
+        const uint32_t v = src[q];
+        p0[q] = uint16_t(v & 0xFFFFu);
+        p1[q] = uint16_t(v >> 16);
+      }
+    }
+  }
+}
+
+template <typename H>
+__device__ __forceinline__ float h2f(H v);
+template <>
+__device__ __forceinline__ float h2f<__half>(__half v) { return __half2float(v); }
+template <>
+__device__ __forceinline__ float h2f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+// out[i] = sum_t X[i*s_outer + t*s_inner], t < len; one warp per output, lanes stride t.
+template <typename H>
+__global__ void strided_sum_kernel(const H* __restrict__ x, float* __restrict__ out, int64_t count,
+                                   int64_t len, int64_t s_outer, int64_t s_inner) {
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= count) return;
+  const H* row = x + warp * s_outer;
+  float acc = 0.f;
+  for (int64_t t = lane; t < len; t += 32) acc += h2f(row[t * s_inner]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) out[warp] = acc;
+}
+
+// out[i] = sum_t X[i + t*s_inner] for unit-stride outputs: one thread per output (coalesced).
+template <typename H>
+__global__ void strided_sum_unit_kernel(const H* __restrict__ x, float* __restrict__ out,
+                                        int64_t count, int64_t len, int64_t s_inner) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  float acc = 0.f;
+  for (int64_t t = 0; t < len; ++t) acc += h2f(x[i + t * s_inner]);
+  out[i] = acc;
+}
+
+}  // namespace tk

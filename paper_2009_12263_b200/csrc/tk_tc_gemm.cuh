@@ -1,0 +1,366 @@
+// tk_tc_gemm.cuh -- persistent, warp-specialised tcgen05 GEMM for sm_100a.
+//
+// One CTA per SM loops over output tiles dealt by a grouped raster (the device
+// form of the reference's parallelise() block dealing, tiling.py:137-210).
+// Roles (384 threads):
+//   warp 0      TMA producer: global layouts -> 128B-swizzled smem ring (mbarrier full/empty);
+//               for a Diagonal A layout it fabricates the diagonal tile in smem instead
+//               (reference layouts.py:218-228) and only visits the block-K iterations that
+//               intersect the diagonal (DiagonalPredicate, components.py:186-191).
+//   warp 1      MMA issuer (one thread): tcgen05.mma kind::f16, FP32 accumulators in TMEM,
+//               double-buffered so the epilogue of tile t overlaps the MMAs of tile t+1.
+//               REAL = 1 MMA per K=16 step; COMPLEX = 4 (negate-A bit for -Ai*Bi);
+//               DUAL = 3 (reference operators.py:140-188).
+//   warp 2      TMEM allocator.
+//   warps 4-11  epilogue: tcgen05.ld -> registers -> fused
+//               D = s2g( r2s( g2s_c(C) + acc ) + bias ) -> coalesced global stores
+//               (reference kernel.py:370-463, components.py:110-157).
+#pragma once
+#include "tk_ptx.cuh"
+#include "tk_types.cuh"
+
+namespace tk {
+
+constexpr int TC_BM = 128;
+constexpr int TC_BK = 64;
+constexpr int TC_EPI_WARPS = 8;
+constexpr int TC_THREADS = (4 + TC_EPI_WARPS) * 32;
+constexpr int TC_A_TILE_BYTES = TC_BM * TC_BK * 2;  // 16 KB
+
+template <int OP>
+struct TcCfg;
+template <>
+struct TcCfg<OP_REAL> {
+  static constexpr int PLANES = 1, BN = 256, STAGES = 4, ACC_COLS = 256, TMEM_COLS = 512;
+};
+template <>
+struct TcCfg<OP_COMPLEX> {
+  static constexpr int PLANES = 2, BN = 128, STAGES = 3, ACC_COLS = 256, TMEM_COLS = 512;
+};
+template <>
+struct TcCfg<OP_DUAL> {
+  static constexpr int PLANES = 2, BN = 128, STAGES = 3, ACC_COLS = 256, TMEM_COLS = 512;
+};
+
+template <int OP>
+struct TcSmem {
+  using C = TcCfg<OP>;
+  static constexpr int B_TILE_BYTES = C::BN * TC_BK * 2;
+  static constexpr int STAGE_BYTES = C::PLANES * (TC_A_TILE_BYTES + B_TILE_BYTES);
+  static constexpr int BAR_OFFSET = C::STAGES * STAGE_BYTES;
+  static constexpr int BAR_BYTES = (2 * C::STAGES + 4) * 8 + 16;
+  static constexpr int TOTAL = BAR_OFFSET + BAR_BYTES + 1024;  // +1024 for manual alignment
+};
+
+struct TcParams {
+  CUtensorMap ta[2];
+  CUtensorMap tb[2];
+  int32_t m, n, k;
+  int32_t a_mn, b_mn, ab_fmt;
+  int32_t num_mb, num_nb, num_tiles, kb_total;
+  int32_t group_m;
+  int32_t diag_a;
+  const void* diag;
+  int32_t c_zero, c_pair, d_pair, bias_axis;
+  const void* c_ptr;
+  void* d_ptr;
+  const float* bias;
+  DigitMap c_map, d_map;
+  int64_t c_plane, d_plane;
+  int32_t affine, pad0;
+  float aff_s, aff_r, aff_q, aff_k;
+  const float* rowsum_a;
+  const float* colsum_b;
+  EpiProg t_c, t_r2s, t_s2g;
+};
+
+__device__ __forceinline__ void tile_coords(const TcParams& p, int t, int& mb, int& nb) {
+  const int per_group = p.group_m * p.num_nb;
+  const int g = t / per_group;
+  const int first = g * p.group_m;
+  const int gm = min(p.num_mb - first, p.group_m);
+  const int r = t - g * per_group;
+  mb = first + r % gm;
+  nb = r / gm;
+}
+
+__device__ __forceinline__ void k_range(const TcParams& p, int mb, int& kb0, int& kb1) {
+  if (p.diag_a) {  // only block-K iterations that intersect the diagonal of A
+    kb0 = (mb * TC_BM) / TC_BK;
+    kb1 = min(p.kb_total, (mb * TC_BM + TC_BM + TC_BK - 1) / TC_BK);
+  } else {
+    kb0 = 0;
+    kb1 = p.kb_total;
+  }
+}
+
+// Fabricate the K-major, 128B-swizzled 128x64 A tile of diag(a) for rows [m0, m0+128),
+// columns [k0, k0+64).  Written by one warp with 16-byte stores.
+template <typename HT>
+__device__ __forceinline__ void write_diag_tile(uint8_t* dst, const HT* diag, int m0, int k0,
+                                                int m, int lane) {
+  for (int idx = lane; idx < TC_BM * 8; idx += 32) {
+    const int row = idx >> 3, chunk = idx & 7;  // physical 16B chunk of a 128B row
+    const int logical_chunk = chunk ^ (row & 7);
+    uint4 v = make_uint4(0, 0, 0, 0);
+    const int gi = m0 + row;
+    const int kk = gi - k0;  // diagonal column inside this k-block
+    if (gi < m && kk >= 0 && kk < TC_BK && (kk >> 3) == logical_chunk) {
+      uint16_t bits = reinterpret_cast<const uint16_t*>(diag)[gi];
+      uint32_t word = (kk & 1) ? (uint32_t(bits) << 16) : uint32_t(bits);
+      const int w = (kk & 7) >> 1;
+      if (w == 0) v.x = word;
+      else if (w == 1) v.y = word;
+      else if (w == 2) v.z = word;
+      else v.w = word;
+    }
+    *reinterpret_cast<uint4*>(dst + row * 128 + chunk * 16) = v;
+  }
+}
+
+template <int OP>
+__global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(const __grid_constant__ TcParams p) {
+  using C = TcCfg<OP>;
+  using S = TcSmem<OP>;
+  constexpr int BN = C::BN;
+  constexpr int STAGES = C::STAGES;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFFSET);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    if (!p.diag_a) {
+      tma_prefetch(&p.ta[0]);
+      if (C::PLANES > 1) tma_prefetch(&p.ta[1]);
+    }
+    tma_prefetch(&p.tb[0]);
+    if (C::PLANES > 1) tma_prefetch(&p.tb[1]);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], TC_EPI_WARPS);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) {
+    tmem_alloc(tmem_slot, C::TMEM_COLS);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto a_tile = [&](int s, int plane) -> uint8_t* {
+    return smem + s * S::STAGE_BYTES + plane * TC_A_TILE_BYTES;
+  };
+  auto b_tile = [&](int s, int plane) -> uint8_t* {
+    return smem + s * S::STAGE_BYTES + C::PLANES * TC_A_TILE_BYTES + plane * S::B_TILE_BYTES;
+  };
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    const uint64_t pol_a = policy_evict_normal();
+    const uint64_t pol_b = policy_evict_normal();
+    const uint32_t a_bytes = p.diag_a ? 0u : uint32_t(TC_A_TILE_BYTES * C::PLANES);
+    const uint32_t tx_bytes = a_bytes + uint32_t(S::B_TILE_BYTES * C::PLANES);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      int mb, nb, kb0, kb1;
+      tile_coords(p, t, mb, nb);
+      k_range(p, mb, kb0, kb1);
+      const int m0 = mb * TC_BM, n0 = nb * BN;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        const int k0 = kb * TC_BK;
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (p.diag_a) {
+          if (p.ab_fmt == 0)
+            write_diag_tile(a_tile(stage, 0), reinterpret_cast<const __half*>(p.diag), m0, k0,
+                            p.m, lane);
+          else
+            write_diag_tile(a_tile(stage, 0), reinterpret_cast<const __nv_bfloat16*>(p.diag),
+                            m0, k0, p.m, lane);
+          fence_proxy_async_smem();
+          __syncwarp();
+        }
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&full[stage], tx_bytes);
+#pragma unroll
+          for (int pl = 0; pl < C::PLANES; ++pl) {
+            if (!p.diag_a) {
+              if (p.a_mn) {  // column-major A: two 64-row boxes (M inner)
+                tma_load_2d(a_tile(stage, pl), &p.ta[pl], &full[stage], m0, k0, pol_a);
+                tma_load_2d(a_tile(stage, pl) + 8192, &p.ta[pl], &full[stage], m0 + 64, k0, pol_a);
+              } else {       // row-major A: one box, K inner
+                tma_load_2d(a_tile(stage, pl), &p.ta[pl], &full[stage], k0, m0, pol_a);
+              }
+            }
+            if (p.b_mn) {    // row-major B: BN/64 boxes, N inner
+#pragma unroll
+              for (int h = 0; h < BN / 64; ++h)
+                tma_load_2d(b_tile(stage, pl) + h * 8192, &p.tb[pl], &full[stage], n0 + 64 * h, k0,
+                            pol_b);
+            } else {         // column-major B: one box, K inner
+              tma_load_2d(b_tile(stage, pl), &p.tb[pl], &full[stage], k0, n0, pol_b);
+            }
+          }
+        }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      const uint32_t a_mn = p.diag_a ? 0u : uint32_t(p.a_mn);
+      const uint32_t idesc = idesc_f16(p.ab_fmt, a_mn, p.b_mn, 0, TC_BM, BN);
+      const uint32_t idesc_neg = idesc_f16(p.ab_fmt, a_mn, p.b_mn, 1, TC_BM, BN);
+      // per K=16 step: K-major advances 32 B inside the swizzle atom, MN-major 2 atoms (2 KB)
+      const uint32_t a_step = a_mn ? 2048u : 32u;
+      const uint32_t b_step = p.b_mn ? 2048u : 32u;
+      const uint32_t a_lbo = a_mn ? 8192u : 16u;
+      const uint32_t b_lbo = p.b_mn ? 8192u : 16u;
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++local) {
+        int mb, nb, kb0, kb1;
+        tile_coords(p, t, mb, nb);
+        k_range(p, mb, kb0, kb1);
+        const int as = local & 1;
+        const uint32_t aphase = (local >> 1) & 1;
+        mbar_wait(&tempty[as], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d0 = tmem_base + uint32_t(as * C::ACC_COLS);
+        const uint32_t d1 = d0 + uint32_t(BN);  // second accumulator (Im / epsilon)
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < TC_BK / 16; ++kk) {
+            const uint32_t acc = (kb > kb0 || kk > 0) ? 1u : 0u;
+            const uint64_t a0 = sdesc_sw128(smem_u32(a_tile(stage, 0)) + kk * a_step, a_lbo, 1024);
+            const uint64_t b0 = sdesc_sw128(smem_u32(b_tile(stage, 0)) + kk * b_step, b_lbo, 1024);
+            if (OP == OP_REAL) {
+              tc_mma_f16(d0, a0, b0, idesc, acc);
+            } else {
+              const uint64_t a1 = sdesc_sw128(smem_u32(a_tile(stage, 1)) + kk * a_step, a_lbo, 1024);
+              const uint64_t b1 = sdesc_sw128(smem_u32(b_tile(stage, 1)) + kk * b_step, b_lbo, 1024);
+              if (OP == OP_COMPLEX) {
+                tc_mma_f16(d0, a0, b0, idesc, acc);      // Re += Ar*Br
+                tc_mma_f16(d0, a1, b1, idesc_neg, 1u);   // Re += (-Ai)*Bi
+                tc_mma_f16(d1, a0, b1, idesc, acc);      // Im += Ar*Bi
+                tc_mma_f16(d1, a1, b0, idesc, 1u);       // Im += Ai*Br
+              } else {
+                tc_mma_f16(d0, a0, b0, idesc, acc);      // v   += Av*Bv
+                tc_mma_f16(d1, a0, b1, idesc, acc);      // eps += Av*Beps
+                tc_mma_f16(d1, a1, b0, idesc, 1u);       // eps += Aeps*Bv
+              }
+            }
+          }
+          tc_commit(&empty[stage]);  // smem slot free once these MMAs retire
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(&tfull[as]);       // accumulator ready for the epilogue
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue
+    const int ew = warp - 4;
+    const int quarter = warp & 3;          // TMEM lane quarter this warp may access
+    const int half = ew >> 2;              // which half of the tile's columns
+    const int row_local = quarter * 32 + lane;
+    constexpr int COLS_PER_WARP = BN / 2;
+    int local = 0;
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++local) {
+      int mb, nb;
+      tile_coords(p, t, mb, nb);
+      const int as = local & 1;
+      const uint32_t aphase = (local >> 1) & 1;
+      const int i = mb * TC_BM + row_local;
+      const bool row_ok = i < p.m;
+      const int64_t c_row = row_ok ? map_dim(p.c_map, 0, i) : 0;
+      const int64_t d_row = row_ok ? map_dim(p.d_map, 0, i) : 0;
+      const float rsum = (p.affine && row_ok) ? p.rowsum_a[i] : 0.f;
+      const float bias_m = (p.bias_axis == 2 && row_ok) ? p.bias[i] : 0.f;
+      mbar_wait(&tfull[as], aphase);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(as * C::ACC_COLS);
+#pragma unroll 1
+      for (int ch = 0; ch < COLS_PER_WARP / 32; ++ch) {
+        const int cl = half * COLS_PER_WARP + ch * 32;  // tile-local first column
+        uint32_t r0[32];
+        tmem_ld_32x32b_x32(tbase + uint32_t(cl), r0);
+        if (OP == OP_REAL) {
+          tmem_ld_wait();
+          const int j0 = nb * BN + cl;
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) {
+            const int j = j0 + jj;
+            if (!row_ok || j >= p.n) continue;
+            float v = __uint_as_float(r0[jj]);
+            if (p.affine)
+              v = p.aff_s * v + p.aff_r * rsum + p.aff_q * p.colsum_b[j] + p.aff_k;
+            const int64_t jc = map_dim(p.c_map, 1, j);
+            if (!p.c_zero) {
+              float cv = load_scalar_f32(p.c_ptr, c_row + jc);
+              cv = run_prog_real(p.t_c, cv);
+              v = cv + v;
+            }
+            v = run_prog_real(p.t_r2s, v);
+            if (p.bias_axis == 1) v = v + p.bias[j];
+            else if (p.bias_axis == 2) v = v + bias_m;
+            v = run_prog_real(p.t_s2g, v);
+            reinterpret_cast<float*>(p.d_ptr)[d_row + map_dim(p.d_map, 1, j)] = v;
+          }
+        } else {
+          uint32_t r1[32];
+          tmem_ld_32x32b_x32(tbase + uint32_t(BN + cl), r1);
+          tmem_ld_wait();
+          const int j0 = nb * BN + cl;
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) {
+            const int j = j0 + jj;
+            if (!row_ok || j >= p.n) continue;
+            float2 v = make_float2(__uint_as_float(r0[jj]), __uint_as_float(r1[jj]));
+            if (!p.c_zero) {
+              float2 cv = load_pair_f32(p.c_ptr, p.c_pair, p.c_plane, c_row + map_dim(p.c_map, 1, j));
+              cv = run_prog_pair<OP>(p.t_c, cv);
+              v = make_float2(cv.x + v.x, cv.y + v.y);
+            }
+            v = run_prog_pair<OP>(p.t_r2s, v);
+            v = run_prog_pair<OP>(p.t_s2g, v);
+            store_pair_f32(p.d_ptr, p.d_pair, p.d_plane, d_row + map_dim(p.d_map, 1, j), v);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[as]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, C::TMEM_COLS);
+  }
+}
+
+}  // namespace tk

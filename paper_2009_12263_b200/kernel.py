@@ -1,0 +1,529 @@
+"""The GEMM engine: KernelConfig -> validated plan -> one device launch.
+
+API parity with reference ``pkg/src/tilekit/kernel.py`` (``KernelConfig``,
+``resolve_config``, ``gemm_execute``, ``EventCounters``, ``snapshot_counters``,
+``active_lane`` / ``available_lanes`` / ``force_lane``, ``allocation_audit``).
+
+Where the reference runs a five-stage Python schedule per output block on a
+thread pool (``kernel.py:253-463``), ``gemm_execute`` here
+
+1. resolves and validates the configuration exactly like the reference (same
+   errors, raised before anything is written);
+2. lowers it to a ``TkGemmPlan`` (the C ABI of ``include/tk_sm100.h``): layouts
+   become digit address maps, transforms become op programs, the epilogue a
+   bias flag, the predicate a k-range rule or a host-evaluated block mask;
+3. makes one call into ``libtk_sm100.so``, which runs a persistent tcgen05
+   kernel (or the bit-exact CUDA-core lane for f32/f64 storage and layouts
+   the tensor-core lane cannot take);
+4. returns ``EventCounters`` derived analytically from the logical block
+   schedule -- the reference's own fast path already derives them
+   arithmetically (``kernel.py:420-424``), so the values are identical.
+
+Lanes: ``"tcgen05"`` (tensor cores, f16/bf16 storage, f32 accumulation) and
+``"simt"`` (CUDA cores, reproduces the reference's operation order bit for
+bit).  There is no host lane.
+"""
+
+from __future__ import annotations
+
+import contextlib
+import contextvars
+import ctypes
+import dataclasses
+from dataclasses import dataclass, field
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import _lib, components, dtypes, layouts
+from .components import (BiasEpilogue, ConfigError, CopyEpilogue, DiagonalPredicate,
+                         identity, transform_program)
+from .layouts import Layout, check_buffer
+from .operators import ComplexOperator, DualOperator, FmaOperator
+from .tiling import Coord, Tile
+
+# ---- lanes --------------------------------------------------------------------
+
+_LANES = {"tcgen05": _lib.LANE_TCGEN05, "simt": _lib.LANE_SIMT}
+_forced = contextvars.ContextVar("tk_forced_lane", default=None)
+
+
+def active_lane() -> str:
+    """Lane selection in effect: 'tcgen05' (automatic: tensor cores when applicable) or a
+    lane pinned with ``force_lane``."""
+    return _forced.get() or "tcgen05"
+
+
+def available_lanes() -> tuple:
+    _lib.load()
+    return tuple(_LANES)
+
+
+@contextlib.contextmanager
+def force_lane(name: str):
+    """Pin the device lane ('tcgen05' or 'simt') for GEMMs issued in this context."""
+    if name not in _LANES:
+        raise ValueError(f"lane {name!r} unavailable; have {tuple(_LANES)}")
+    token = _forced.set(name)
+    try:
+        yield
+    finally:
+        _forced.reset(token)
+
+
+# ---- allocation audit ------------------------------------------------------------
+
+_audit = contextvars.ContextVar("tk_audit", default=None)
+
+
+@contextlib.contextmanager
+def allocation_audit():
+    """Collect (label, element_count) for every buffer a GEMM allocates: device
+    workspace, host->device staging copies, and the kernel's on-chip smem/TMEM stages."""
+    log = []
+    token = _audit.set(log)
+    try:
+        yield log
+    finally:
+        _audit.reset(token)
+
+
+def _note(label: str, count: int) -> None:
+    log = _audit.get()
+    if log is not None:
+        log.append((label, int(count)))
+
+
+# ---- counters ------------------------------------------------------------------
+
+@dataclass
+class EventCounters:
+    """Exact event counts of the logical block schedule (reference kernel.py:100-119)."""
+
+    global_loads: int = 0
+    global_stores: int = 0
+    scratch_loads: int = 0
+    scratch_stores: int = 0
+    operator_invocations: int = 0
+    inner_iterations_executed: int = 0
+    inner_iterations_skipped: int = 0
+
+    def merge(self, other: "EventCounters") -> None:
+        for f in dataclasses.fields(self):
+            setattr(self, f.name, getattr(self, f.name) + getattr(other, f.name))
+
+
+def snapshot_counters(counters: EventCounters) -> EventCounters:
+    return dataclasses.replace(counters)
+
+
+# ---- configuration ---------------------------------------------------------------
+
+@dataclass(frozen=True)
+class KernelConfig:
+    """Params, operator, 4 global layouts, 4 shared builders, 5 transforms, epilogue,
+    predicate (reference kernel.py:132-159)."""
+
+    params: components.Params
+    operator: object
+    global_a_layout: Layout
+    global_c_layout: Layout
+    global_d_layout: Layout
+    global_b_layout: Optional[Layout] = None
+    shared_a_layout: Optional[Callable] = None
+    shared_b_layout: Optional[Callable] = None
+    shared_c_layout: Optional[Callable] = None
+    shared_d_layout: Optional[Callable] = None
+    transform_g2s_a: Callable = identity
+    transform_g2s_b: Callable = identity
+    transform_g2s_c: Callable = identity
+    transform_r2s_d: Callable = identity
+    transform_s2g_d: Callable = identity
+    epilogue: object = field(default_factory=CopyEpilogue)
+    predicate: Optional[Callable] = None
+
+
+def _expect_layout(layout, names, extents, label):
+    if tuple(layout.names) != names:
+        raise ConfigError(f"{label}: expected dims {names}, got {layout.names}")
+    if tuple(layout.extents) != tuple(extents):
+        raise ConfigError(f"{label}: expected extents {extents}, got {layout.extents}")
+
+
+def _default_shared(config: KernelConfig) -> KernelConfig:
+    fills = {}
+    for slot, glob in (("shared_a_layout", config.global_a_layout),
+                       ("shared_b_layout", config.global_b_layout or config.global_a_layout),
+                       ("shared_c_layout", config.global_c_layout),
+                       ("shared_d_layout", config.global_d_layout)):
+        if getattr(config, slot) is None:
+            fills[slot] = layouts.col_major(glob.element_type)
+    return dataclasses.replace(config, **fills) if fills else config
+
+
+def resolve_config(config: KernelConfig) -> KernelConfig:
+    """Fill defaults (shared builders, B layout, tiling) and validate; idempotent."""
+    return components.resolve_params(_default_shared(config))
+
+
+# ---- analytic counters --------------------------------------------------------------
+
+def _span_counts(m0, k0, bm, bk):
+    """Diagonal elements inside [m0,m0+bm) x [k0,k0+bk) (vectorised)."""
+    lo = np.maximum(m0, k0)
+    hi = np.minimum(m0 + bm, k0 + bk)
+    return np.maximum(hi - lo, 0)
+
+
+def _layout_tile_count(layout, r0, c0, rs, cs, count_shape):
+    """Elements a layout's load/store touches per tile, broadcast to count_shape."""
+    if isinstance(layout, layouts.Zero):
+        return np.zeros(count_shape, dtype=np.int64)
+    if isinstance(layout, layouts.Diagonal):
+        return np.broadcast_to(_span_counts(r0, c0, rs, cs), count_shape).astype(np.int64)
+    return np.full(count_shape, rs * cs, dtype=np.int64)
+
+
+def _counters(config, executed: np.ndarray) -> EventCounters:
+    """Counters of the reference schedule; ``executed[bi, bj, kb]`` marks run iterations."""
+    p = config.params
+    m, n, k = p.gemm_shape
+    bm, bn, bk = p.block_tile
+    om, on, ok = p.operator_shape
+    nmb, nnb, nkb = m // bm, n // bn, k // bk
+    blocks = nmb * nnb
+    mi = (np.arange(nmb) * bm)[:, None, None]
+    ni = (np.arange(nnb) * bn)[None, :, None]
+    ki = (np.arange(nkb) * bk)[None, None, :]
+    shape = (nmb, nnb, nkb)
+    n_exec = int(executed.sum())
+    c_loads = int(_layout_tile_count(config.global_c_layout, mi[..., 0], ni[..., 0], bm, bn,
+                                     (nmb, nnb)).sum())
+    a_loads = int((_layout_tile_count(config.global_a_layout, mi, ki, bm, bk, shape)
+                   * executed).sum())
+    b_loads = int((_layout_tile_count(config.global_b_layout, ki, ni, bk, bn, shape)
+                   * executed).sum())
+    d_stores = int(_layout_tile_count(config.global_d_layout, mi[..., 0], ni[..., 0], bm, bn,
+                                      (nmb, nnb)).sum())
+    inv = n_exec * (bm // om) * (bn // on) * (bk // ok)
+    bias = 0
+    if isinstance(config.epilogue, BiasEpilogue):
+        bias = blocks * (bn if config.epilogue.axis == "n" else bm)
+    return EventCounters(
+        global_loads=c_loads + a_loads + b_loads + bias,
+        global_stores=d_stores,
+        scratch_loads=2 * blocks * bm * bn + inv * (om * ok + ok * on),
+        scratch_stores=2 * blocks * bm * bn + n_exec * (bm * bk + bk * bn),
+        operator_invocations=inv,
+        inner_iterations_executed=n_exec,
+        inner_iterations_skipped=blocks * nkb - n_exec,
+    )
+
+
+# ---- lowering ------------------------------------------------------------------------
+
+def _lower_layout(layout) -> _lib.TkLayout:
+    desc = layout.lower()
+    out = _lib.TkLayout()
+    out.kind, out.pair = desc.kind, desc.pair
+    out.scalar = dtypes.SCALAR_CODES[desc.scalar]
+    for d, digits in enumerate(desc.digits):
+        if len(digits) > _lib.MAX_DIGITS:
+            raise ConfigError(f"layout {layout!r} needs more than {_lib.MAX_DIGITS} digits per dim")
+        out.ndigits[d] = len(digits)
+        for t, (ext, stride) in enumerate(digits):
+            out.ext[d][t] = int(ext)
+            out.stride[d][t] = int(stride)
+    out.plane_stride = desc.plane_stride
+    out.size = desc.size
+    return out
+
+
+def _lower_transform(t, stream: str) -> _lib.TkTransform:
+    ops = transform_program(t, stream)
+    if len(ops) > _lib.MAX_TOPS:
+        raise ConfigError(f"transform on stream {stream} has more than {_lib.MAX_TOPS} ops")
+    out = _lib.TkTransform()
+    out.n = len(ops)
+    for i, (code, const, promote) in enumerate(ops):
+        out.op[i] = code
+        out.promote[i] = int(bool(promote))
+        c = complex(const)
+        out.re[i], out.im[i] = c.real, c.imag
+    return out
+
+
+_OPERATORS = (FmaOperator, ComplexOperator, DualOperator)
+
+
+def _check_operator(op):
+    base = next((cls for cls in (DualOperator, ComplexOperator, FmaOperator)
+                 if isinstance(op, cls)), None)
+    if base is None:
+        raise ConfigError(f"operator {type(op).__name__} has no device composition")
+    for meth in ("mma", "load_a", "load_b", "load_c", "store_d"):
+        if getattr(type(op), meth) is not getattr(base, meth):
+            raise ConfigError(f"operator {type(op).__name__} overrides {meth}; custom Python "
+                              "operators cannot run on the device lanes")
+    return base
+
+
+def _predicate_plan(config):
+    """(predicate code, mask or None, executed[bi,bj,kb] boolean array)."""
+    p = config.params
+    m, n, k = p.gemm_shape
+    bm, bn, bk = p.block_tile
+    nmb, nnb, nkb = m // bm, n // bn, k // bk
+    pred = config.predicate
+    if pred is None:
+        return _lib.PRED_ALWAYS, None, np.ones((nmb, nnb, nkb), dtype=bool)
+    if isinstance(pred, DiagonalPredicate):
+        m0 = (np.arange(nmb) * bm)[:, None]
+        k0 = (np.arange(nkb) * bk)[None, :]
+        run = np.maximum(m0, k0) < np.minimum(m0 + bm, k0 + bk)
+        return _lib.PRED_DIAGONAL, None, np.broadcast_to(run[:, None, :], (nmb, nnb, nkb))
+    run = np.empty((nmb, nnb, nkb), dtype=bool)
+    size = Coord.of(M=bm, N=bn, K=bk)
+    zero = size.zero_like()
+    for bj in range(nnb):
+        for bi in range(nmb):
+            for kb in range(nkb):
+                tile = Tile(Coord.of(M=bi * bm, N=bj * bn, K=kb * bk), zero, size)
+                run[bi, bj, kb] = bool(pred(tile))
+    if run.all():
+        return _lib.PRED_ALWAYS, None, run
+    # mask rows follow the column-major block rank bi + bj * nmb
+    mask = np.ascontiguousarray(run.transpose(1, 0, 2).reshape(nmb * nnb, nkb), dtype=np.uint8)
+    return _lib.PRED_MASK, mask, run
+
+
+def lower(config: KernelConfig, lane: Optional[str] = None):
+    """Lower a resolved config to (TkGemmPlan, mask or None, executed-array)."""
+    p = config.params
+    base = _check_operator(config.operator)
+    opcode, compute, op_k = config.operator.lower()
+    if compute not in ("f32", "f64"):
+        raise ConfigError(f"accumulation in {compute} is not supported; use f32 or f64")
+    plan = _lib.TkGemmPlan()
+    plan.abi_version = _lib.ABI_VERSION
+    plan.op = opcode
+    plan.compute = dtypes.SCALAR_CODES[compute]
+    plan.lane = _LANES[lane] if lane else (_LANES[_forced.get()] if _forced.get() else 0)
+    plan.m, plan.n, plan.k = p.gemm_shape
+    plan.op_k = op_k
+    for d in range(3):
+        plan.block[d] = p.block_tile[d]
+    for slot, layout in (("a", config.global_a_layout), ("b", config.global_b_layout),
+                         ("c", config.global_c_layout), ("d", config.global_d_layout)):
+        try:
+            setattr(plan, slot, _lower_layout(layout))
+        except NotImplementedError as exc:
+            raise ConfigError(f"global {slot.upper()} layout: {exc}") from None
+    if base is FmaOperator and dtypes.pair_kind(config.global_a_layout.element_type):
+        raise ConfigError("the real operator needs real element types")
+    plan.t_a = _lower_transform(config.transform_g2s_a, "g2s_a")
+    plan.t_b = _lower_transform(config.transform_g2s_b, "g2s_b")
+    plan.t_c = _lower_transform(config.transform_g2s_c, "g2s_c")
+    plan.t_r2s = _lower_transform(config.transform_r2s_d, "r2s_d")
+    plan.t_s2g = _lower_transform(config.transform_s2g_d, "s2g_d")
+    ep = config.epilogue
+    if isinstance(ep, BiasEpilogue):
+        plan.bias_axis = 1 if ep.axis == "n" else 2
+        plan.bias_scalar = dtypes.SCALAR_CODES[dtypes.scalar_name(_bias_dtype(ep.bias))]
+    elif not isinstance(ep, CopyEpilogue):
+        raise ConfigError(f"epilogue {type(ep).__name__} has no device form")
+    code, mask, executed = _predicate_plan(config)
+    plan.predicate = code
+    return plan, mask, executed
+
+
+def _bias_dtype(bias):
+    try:
+        import torch
+
+        if isinstance(bias, torch.Tensor):
+            return dtypes.from_torch(bias.dtype)
+    except ImportError:  # pragma: no cover
+        pass
+    return np.asarray(bias).dtype
+
+
+def plan_lane(plan) -> str:
+    lane = _lib.load().tk_plan_lane(ctypes.byref(plan))
+    if lane < 0:
+        raise ConfigError(_lib.last_error())
+    return _lib.LANE_NAMES[lane]
+
+
+# ---- buffers ------------------------------------------------------------------------------
+
+def _torch():
+    import torch
+
+    return torch
+
+
+class _Buf:
+    """A caller buffer resolved to a CUDA tensor (zero-copy when already on the device)."""
+
+    def __init__(self, buf, storage_dtype, label, device):
+        torch = _torch()
+        self.host = None
+        want = dtypes.torch_scalar(storage_dtype)
+        if isinstance(buf, torch.Tensor):
+            if buf.dtype != want:
+                raise ConfigError(f"{label} buffer dtype {buf.dtype} != layout storage "
+                                  f"{np.dtype(storage_dtype)}")
+            if buf.is_cuda:
+                self.dev = buf
+                return
+            self.host = buf
+            src = buf
+        else:
+            arr = np.asarray(buf)
+            if arr.dtype != np.dtype(storage_dtype):
+                raise ConfigError(f"{label} buffer dtype {arr.dtype} != layout storage "
+                                  f"{np.dtype(storage_dtype)}")
+            self.host = arr
+            src = (torch.from_numpy(np.ascontiguousarray(arr).view(np.uint16)).view(want)
+                   if want == torch.bfloat16 else torch.from_numpy(np.ascontiguousarray(arr)))
+        self.dev = src.to(device) if src.numel() else torch.empty(0, dtype=want, device=device)
+        _note(f"staging:{label}", src.numel())
+
+    def ptr(self):
+        return self.dev.data_ptr() if self.dev.numel() else None
+
+    def copy_back(self):
+        if self.host is None:
+            return
+        torch = _torch()
+        if isinstance(self.host, torch.Tensor):
+            self.host.copy_(self.dev.cpu())
+        else:
+            out = self.dev.cpu()
+            if out.dtype == torch.bfloat16:
+                self.host.view(np.uint16)[...] = out.view(torch.int16).numpy().view(np.uint16)
+            else:
+                self.host[...] = out.numpy()
+
+
+def _shape_of(buf):
+    return tuple(buf.shape)
+
+
+def _check_flat(layout, buf, label):
+    class _Shape:
+        shape = _shape_of(buf)
+
+    check_buffer(layout, _Shape, label)
+
+
+# ---- engine ---------------------------------------------------------------------------------
+
+_LAST = {"lane": None, "launches": 0}
+
+
+def last_run() -> dict:
+    """Lane and device-kernel count of the most recent gemm_execute in this process."""
+    return dict(_LAST)
+
+
+def gemm_execute(config: KernelConfig, a, b, c, d, *, stream=None, synchronize: bool = True,
+                 lane: Optional[str] = None) -> EventCounters:
+    """Run one GEMM on the B200; returns the event counters of the logical schedule.
+
+    Buffers are flat 1-D arrays (numpy or torch, host or device) sized by their layouts'
+    ``physical_size()``; host buffers are staged through device memory and D is copied
+    back.  All validation happens before anything is written.
+    """
+    config = resolve_config(config)
+    p = config.params
+    m, n, k = p.gemm_shape
+    op = config.operator
+    if (op.shape.m, op.shape.n, op.shape.k) != tuple(p.operator_shape):
+        raise ConfigError(f"operator shape {op.shape} disagrees with params {p.operator_shape}")
+    _expect_layout(config.global_a_layout, ("M", "K"), (m, k), "global A layout")
+    _expect_layout(config.global_b_layout, ("K", "N"), (k, n), "global B layout")
+    _expect_layout(config.global_c_layout, ("M", "N"), (m, n), "global C layout")
+    _expect_layout(config.global_d_layout, ("M", "N"), (m, n), "global D layout")
+    bufs = (a, b, c, d)
+    glob = (config.global_a_layout, config.global_b_layout, config.global_c_layout,
+            config.global_d_layout)
+    for layout, buf, label in zip(glob, bufs, "ABCD"):
+        _check_flat(layout, buf, label)
+    torch = _torch()
+    for layout, buf, label in zip(glob, bufs, "ABCD"):
+        bdt = buf.dtype if isinstance(buf, torch.Tensor) else np.asarray(buf).dtype
+        want = dtypes.torch_scalar(layout.storage_dtype) if isinstance(buf, torch.Tensor) \
+            else np.dtype(layout.storage_dtype)
+        if bdt != want:
+            raise ConfigError(f"{label} buffer dtype {bdt} != layout storage "
+                              f"{np.dtype(layout.storage_dtype)}")
+    if isinstance(config.epilogue, BiasEpilogue):
+        config.epilogue.check(m, n)
+
+    plan, mask, executed = lower(config, lane)
+    lib = _lib.load()
+    lane_id = lib.tk_plan_lane(ctypes.byref(plan))
+    if lane_id < 0:
+        raise ConfigError(_lib.last_error())
+    counters = _counters(config, executed)
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("gemm_execute needs a CUDA device (B200); no host fallback exists")
+    device = d.device if isinstance(d, torch.Tensor) and d.is_cuda else torch.device("cuda")
+    with torch.cuda.device(device):
+        same_cd = c is d
+        A = _Buf(a, config.global_a_layout.storage_dtype, "A", device)
+        B = _Buf(b, config.global_b_layout.storage_dtype, "B", device)
+        C = _Buf(c, config.global_c_layout.storage_dtype, "C", device)
+        D = C if same_cd else _Buf(d, config.global_d_layout.storage_dtype, "D", device)
+        bias_dev = None
+        if isinstance(config.epilogue, BiasEpilogue):
+            bias_dev = _Buf(config.epilogue.bias if isinstance(config.epilogue.bias, torch.Tensor)
+                            else np.ascontiguousarray(config.epilogue.bias).ravel(),
+                            _bias_dtype(config.epilogue.bias), "bias", device)
+        mask_dev = torch.from_numpy(mask).to(device) if mask is not None else None
+        ws_bytes = lib.tk_workspace_bytes(ctypes.byref(plan))
+        if ws_bytes < 0:
+            raise ConfigError(_lib.last_error())
+        ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=device)
+        if ws_bytes:
+            _note("workspace", ws_bytes)
+        _note_onchip(plan, lane_id)
+        s = stream if stream is not None else torch.cuda.current_stream(device)
+        rc = lib.tk_gemm(ctypes.byref(plan), A.ptr(), B.ptr(), C.ptr(), D.ptr(),
+                         bias_dev.ptr() if bias_dev else None,
+                         mask_dev.data_ptr() if mask_dev is not None else None,
+                         ws.data_ptr() if ws_bytes else None, ws_bytes, s.cuda_stream)
+        if rc == _lib.TK_ERR_CONFIG:
+            raise ConfigError(_lib.last_error())
+        if rc != _lib.TK_OK:
+            raise RuntimeError(f"libtk_sm100: {_lib.last_error()}")
+        _LAST["lane"] = _lib.LANE_NAMES[lane_id]
+        _LAST["launches"] = lib.tk_last_launch_count()
+        if D.host is not None:
+            s.synchronize()
+            D.copy_back()
+        elif synchronize:
+            s.synchronize()
+        else:
+            # asynchronous: keep workspace / staging alive until the stream consumes them
+            for t in (A.dev, B.dev, C.dev, ws) + ((mask_dev,) if mask_dev is not None else ()):
+                t.record_stream(s)
+    return counters
+
+
+def _note_onchip(plan, lane_id):
+    if _audit.get() is None:
+        return
+    if lane_id == _lib.LANE_TCGEN05:
+        pair = plan.op != 0
+        bn = 128 if pair else 256
+        stages = 3 if pair else 4
+        planes = 2 if pair else 1
+        for s in range(stages):
+            _note(f"smem:stage_a[{s}]", planes * 128 * 64)
+            _note(f"smem:stage_b[{s}]", planes * bn * 64)
+        for s in range(2):
+            _note(f"tmem:accumulator[{s}]", 128 * 256)

@@ -1,0 +1,244 @@
+"""GPU parity: the device lanes against the oracle (C restatement of the reference).
+
+Bars:
+* tcgen05 lane (f16/bf16 storage, FP32 accumulation): normwise relative error vs the
+  oracle <= 4 * 2^-24 * sqrt(K) (complex: 8x); integer-valued inputs: bitwise equal.
+* simt lane (reference dtypes): bitwise equal -- it replays the reference's operation order.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2009_12263_b200 as tk
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _dev(x):
+    x = np.asarray(x)
+    if x.dtype == tk.BFLOAT16:
+        return torch.from_numpy(np.ascontiguousarray(x.ravel(order="F")).view(np.uint16)) \
+            .view(torch.bfloat16).cuda()
+    return torch.from_numpy(np.ascontiguousarray(x.ravel(order="F"))).cuda()
+
+
+def _host(t, shape, dtype=np.float32):
+    return t.cpu().numpy().reshape(shape, order="F").astype(dtype, copy=False)
+
+
+def _half(rng, shape, dtype, integer=False):
+    if integer:
+        return rng.integers(-4, 5, shape).astype(dtype)
+    return rng.standard_normal(shape).astype(dtype)
+
+
+def _f32(x):
+    return np.asarray(x).astype(np.float32)
+
+
+@pytest.mark.parametrize("dtype", [np.float16, "bf16"])
+@pytest.mark.parametrize("trans", ["nn", "nt", "tn", "tt"])
+def test_dense_integer_exact(cuda, dtype, trans):
+    dtype = tk.BFLOAT16 if dtype == "bf16" else np.dtype(dtype)
+    m, n, k = 256, 512, 320
+    ta, tb = trans[0] == "t", trans[1] == "t"
+    rng = np.random.default_rng(0)
+    a = _half(rng, (m, k), dtype, True)
+    b = _half(rng, (k, n), dtype, True)
+    c = rng.integers(-4, 5, (m, n)).astype(np.float32)
+    cfg = tk.build_dense_config(m, n, k, dtype, trans_a=ta, trans_b=tb)
+    abuf = _dev(a.T if ta else a) if ta else _dev(a)
+    bbuf = _dev(b.T if tb else b) if tb else _dev(b)
+    d = torch.zeros(m * n, dtype=torch.float32, device=cuda)
+    tk.matmul(cfg, abuf, bbuf, _dev(c), d)
+    assert tk.last_run()["lane"] == "tcgen05"
+    want = O.gemm_real(_f32(a), _f32(b), c)
+    got = _host(d, (m, n))
+    assert np.array_equal(got, want), f"max abs diff {np.max(np.abs(got - want))}"
+
+
+@pytest.mark.parametrize("dtype", [np.float16, "bf16"])
+@pytest.mark.parametrize("mnk", [(128, 256, 64), (1024, 1024, 1024), (384, 768, 2048),
+                                 (200, 136, 72), (8, 16, 8), (1000, 520, 4104)])
+def test_dense_random_within_tolerance(cuda, dtype, mnk):
+    dtype = tk.BFLOAT16 if dtype == "bf16" else np.dtype(dtype)
+    m, n, k = mnk
+    rng = np.random.default_rng(1)
+    a, b = _half(rng, (m, k), dtype), _half(rng, (k, n), dtype)
+    c = rng.standard_normal((m, n)).astype(np.float32)
+    cfg = tk.build_dense_config(m, n, k, dtype, operator_shape=(8, 8, 8))
+    d = torch.zeros(m * n, dtype=torch.float32, device=cuda)
+    tk.matmul(cfg, _dev(a), _dev(b), _dev(c), d)
+    got = _host(d, (m, n))
+    want = O.gemm_real(_f32(a), _f32(b), c)
+    exact = O.exact_gemm(_f32(a), _f32(b), c, beta=1.0)
+    assert O.rel_err(got, want) <= O.tolerance(k), O.rel_err(got, want)
+    assert O.rel_err(got, exact) <= O.tolerance(k), O.rel_err(got, exact)
+
+
+def test_fused_affine_bias_relu(cuda):
+    m, n, k = 512, 384, 256
+    rng = np.random.default_rng(2)
+    # 2^-8 grid in [-4, 4]: A + 0.5 and B - 0.25 exact in fp16 (SURVEY 8d transform set)
+    a = (rng.integers(-1024, 1025, (m, k)) / 256.0).astype(np.float16)
+    b = (rng.integers(-1024, 1025, (k, n)) / 256.0).astype(np.float16)
+    c = rng.standard_normal((m, n)).astype(np.float32)
+    bias = rng.standard_normal(n).astype(np.float32)
+    cfg = tk.build_fused_config(m, n, k, np.float16, bias=bias, relu_on_c=True, relu_on_d=True,
+                                add_a=0.5, add_b=-0.25)
+    d = torch.zeros(m * n, dtype=torch.float32, device=cuda)
+    counters = tk.matmul(cfg, _dev(a), _dev(b), _dev(c), d)
+    assert tk.last_run()["lane"] == "tcgen05"
+    want = O.fused_reference(_f32(a), _f32(b), c, bias, relu_on_c=True, relu_on_d=True,
+                             add_a=0.5, add_b=-0.25)
+    assert O.rel_err(_host(d, (m, n)), want) <= O.tolerance(k)
+    assert counters.global_stores == m * n
+
+
+@pytest.mark.parametrize("split", [False, True])
+@pytest.mark.parametrize("kind", ["complex", "dual"])
+def test_pair_operators(cuda, split, kind):
+    m, n, k = 256, 384, 192
+    rng = np.random.default_rng(3)
+    h16 = lambda s: rng.standard_normal(s).astype(np.float16)
+    if kind == "complex":
+        a = (h16((m, k)), h16((m, k)))
+        b = (h16((k, n)), h16((k, n)))
+        c = (rng.standard_normal((m, n)) + 1j * rng.standard_normal((m, n))).astype(np.complex64)
+        half = tk.COMPLEX32
+        pack = lambda x: _pack_pair(x[0], x[1], half, split)
+        cfg = tk.build_complex_config(m, n, k, half, split=split)
+        z = lambda x: np.asfortranarray((_f32(x[0]) + 1j * _f32(x[1])).astype(np.complex64))
+        want = O.gemm_pair(z(a), z(b), np.asfortranarray(c))
+        parts = lambda z: (z.real, z.imag)
+        factor = 8.0
+    else:
+        a = (h16((m, k)), h16((m, k)))
+        b = (h16((k, n)), h16((k, n)))
+        c = tk.dual_array(rng.standard_normal((m, n)), rng.standard_normal((m, n)), tk.DUAL32)
+        half = tk.DUAL16
+        pack = lambda x: _pack_pair(x[0], x[1], half, split)
+        cfg = tk.build_dual_config(m, n, k, half, split=split)
+        h = lambda x: x.astype(np.float16).astype(np.float32)
+        want = O.gemm_pair(np.asfortranarray(tk.dual_array(h(a[0]), h(a[1]), tk.DUAL32)),
+                           np.asfortranarray(tk.dual_array(h(b[0]), h(b[1]), tk.DUAL32)),
+                           np.asfortranarray(c), dual=True)
+        parts = lambda z: (z["value"], z["epsilon"])
+        factor = 4.0
+    cbuf = _pack_pair(*parts(c), None, split)
+    d = torch.zeros_like(cbuf)
+    tk.matmul(cfg, pack(a), pack(b), cbuf, d)
+    assert tk.last_run()["lane"] == "tcgen05"
+    got = _unpack_pair(d, (m, n), split)
+    w0, w1 = parts(want)
+    err = max(O.rel_err(got[0], w0), O.rel_err(got[1], w1))
+    assert err <= O.tolerance(k, factor), err
+
+
+def _pack_pair(p0, p1, half, split):
+    """Flat pair buffer (interleaved or split planes, column-major) as a CUDA tensor."""
+    dt = np.float16 if half is not None else np.float32
+    p0 = np.asarray(p0).astype(dt).ravel(order="F")
+    p1 = np.asarray(p1).astype(dt).ravel(order="F")
+    flat = np.concatenate([p0, p1]) if split else np.stack([p0, p1], axis=1).ravel()
+    return torch.from_numpy(flat).cuda()
+
+
+def _unpack_pair(t, shape, split):
+    x = t.cpu().numpy()
+    vol = shape[0] * shape[1]
+    if split:
+        p0, p1 = x[:vol], x[vol:]
+    else:
+        p0, p1 = x[0::2], x[1::2]
+    return p0.reshape(shape, order="F"), p1.reshape(shape, order="F")
+
+
+@pytest.mark.parametrize("n", [256, 1024, 640])
+def test_diagonal_variant(cuda, n):
+    rng = np.random.default_rng(4)
+    diag = rng.standard_normal(n).astype(np.float16)
+    b = rng.standard_normal((n, n)).astype(np.float16)
+    c = rng.standard_normal((n, n)).astype(np.float32)
+    cfg = tk.build_diagonal_config(n, np.float16, block_tile=(64, 64, 16))
+    d = torch.zeros(n * n, dtype=torch.float32, device=cuda)
+    counters = tk.matmul(cfg, torch.from_numpy(diag).cuda(), _dev(b), _dev(c), d)
+    assert tk.last_run()["lane"] == "tcgen05"
+    want = O.gemm_real(np.diag(_f32(diag)), _f32(b), c)
+    # diag(a)*B + C: one product per element -> exact in FP32
+    assert np.array_equal(_host(d, (n, n)), want)
+    assert counters.inner_iterations_executed == (n // 64) * (n // 64) * 4
+
+
+def test_gemm_ex_alpha_beta_trans(cuda):
+    m, n, k = 192, 320, 256
+    rng = np.random.default_rng(5)
+    a = rng.standard_normal((k, m)).astype(np.float16)           # stored transposed
+    b = rng.standard_normal((k, n)).astype(np.float16)
+    c = np.asfortranarray(rng.standard_normal((m, n)).astype(np.float32))
+    want = O.exact_gemm(_f32(a).T, _f32(b), c, alpha=1.5, beta=0.5)
+    tc = _fortran(c)
+    tk.gemm_ex(True, False, 1.5, _fortran(a), _fortran(b), 0.5, tc)
+    assert O.rel_err(tc.cpu().numpy(), want) <= O.tolerance(k)
+
+
+def _fortran(x):
+    """F-contiguous CUDA tensor view of a numpy matrix."""
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(x).T)).cuda().t()
+
+
+def test_gemm_ex_raw_host_pointers():
+    m, n, k = 64, 48, 32
+    rng = np.random.default_rng(6)
+    a = np.asfortranarray(rng.standard_normal((m, k)).astype(np.float16))
+    b = np.asfortranarray(rng.standard_normal((k, n)).astype(np.float16))
+    c = np.asfortranarray(rng.standard_normal((m, n)).astype(np.float32))
+    want = O.exact_gemm(_f32(a), _f32(b), c, alpha=2.0, beta=0.25)
+    st = tk.gemm_ex_raw(tk.TAG_F16F32, 0, 0, m, n, k, 2.0, 0.0, a.ctypes.data, b.ctypes.data,
+                        0.25, 0.0, c.ctypes.data)
+    assert st == 0
+    assert O.rel_err(c, want) <= O.tolerance(k)
+
+
+# ---- bit-exact CUDA-core lane ------------------------------------------------------
+
+def test_simt_f32_bitwise(cuda):
+    m, n, k = 96, 80, 64
+    rng = np.random.default_rng(7)
+    a = rng.standard_normal((m, k)).astype(np.float32)
+    b = rng.standard_normal((k, n)).astype(np.float32)
+    c = rng.standard_normal((m, n)).astype(np.float32)
+    bias = rng.standard_normal(n).astype(np.float32)
+    cfg = tk.build_fused_config(m, n, k, np.float32, bias=bias, relu_on_c=True, add_a=0.5,
+                                add_b=-0.25)
+    d = np.zeros(m * n, np.float32)
+    tk.matmul(cfg, a.ravel(order="F"), b.ravel(order="F"), c.ravel(order="F"), d)
+    assert tk.last_run()["lane"] == "simt"
+    want = O.fused_reference(a, b, c, bias, relu_on_c=True, relu_on_d=True, add_a=0.5,
+                             add_b=-0.25)
+    assert np.array_equal(d.reshape((m, n), order="F"), want)
+
+
+def test_simt_complex_dual_bitwise(cuda):
+    m, n, k = 40, 24, 32
+    rng = np.random.default_rng(8)
+    mk = lambda s: np.asfortranarray((rng.standard_normal(s) + 1j * rng.standard_normal(s))
+                                     .astype(np.complex64))
+    a, b, c = mk((m, k)), mk((k, n)), mk((m, n))
+    cfg = tk.build_complex_config(m, n, k, np.complex64)
+    d = np.zeros(m * n, np.complex64)
+    tk.matmul(cfg, a.ravel(order="F").view(np.float32), b.ravel(order="F").view(np.float32),
+              c.ravel(order="F").view(np.float32), d.view(np.float32))
+    assert np.array_equal(d.reshape((m, n), order="F"), O.gemm_pair(a, b, c))
+    ints = lambda s: rng.integers(-4, 5, s).astype(np.float64)
+    a = np.asfortranarray(tk.dual_array(ints((m, k)), ints((m, k))))
+    b = np.asfortranarray(tk.dual_array(ints((k, n)), ints((k, n))))
+    c = np.asfortranarray(tk.dual_array(ints((m, n)), ints((m, n))))
+    cfg = tk.build_dual_config(m, n, k)
+    d = np.zeros(m * n, tk.DUAL64)
+    tk.matmul(cfg, a.ravel(order="F").view(np.float64), b.ravel(order="F").view(np.float64),
+              c.ravel(order="F").view(np.float64), d.view(np.float64))
+    assert np.array_equal(d.reshape((m, n), order="F"), O.gemm_pair(a, b, c, dual=True))
