@@ -1,0 +1,337 @@
+"""Benchmark: FP16 -> FP32 GEMM TFLOPS on B200 (BASELINE.json metric), one JSON line.
+
+Workload (BASELINE.json configs[1], the north-star point): D = A*B + C, column-major,
+M = K = 8192, fp16 A/B, fp32 C/D, reference `build_dense_config` semantics.  Multi-GPU:
+one process per GPU, C sharded by column slabs of B with A replicated (no data-path
+collective): every rank owns an M x n slab, so the global problem is M x (n*G) x K and
+`scaling` is "weak".
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--n 8192] [--dtype fp16|bf16]
+  python bench.py --impl reference ...   # the reference's own CPU implementation
+
+Timing: W untimed steps, then K steps bracketed by barrier + cuda synchronize, CUDA events
+on the launching stream, max over ranks.  Inputs (768 MiB at n=8192) exceed the 126 MB L2.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GEMM TFLOPS (FP16/BF16 in, FP32 acc) vs N; % of B200 dense tensor-core peak"
+UNIT = "TFLOPS"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["bf16_tflops"]), float(p.get("bf16_tflops_sustained", 0) or 0), \
+            float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """NVML SM clock / throttle-reason sampler running during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.max_mhz = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            pass
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                util = self.nv.nvmlDeviceGetUtilizationRates(self.h).gpu
+                mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                if util > 0:
+                    self.samples.append(mhz)
+                    for bit, name in self.REASONS.items():
+                        if mask & bit and name != "gpu_idle":
+                            self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---- reference CPU implementation -------------------------------------------------------
+
+def _reference_module():
+    """The reference package (oracle/_ref, built from /root/reference by oracle/Makefile)."""
+    path = os.path.join(ROOT, "oracle", "_ref")
+    if os.path.isdir(os.path.join(path, "tilekit")):
+        sys.path.insert(0, path)
+        import tilekit
+
+        return tilekit, "reference"
+    return None, "port"
+
+
+def cpu_sample(m, k, threads, seed=0):
+    """Time the reference CPU path on an m x s x k slab of the workload; returns a dict.
+
+    Inputs are fp16-valued float32 (the reference has no fp16 type; SURVEY 8c protocol).
+    The slab width s is sized for a bounded run (~2-10 s on the host cores).
+    """
+    tilekit, kind = _reference_module()
+    s = 512 * max(1, min(8, threads // 8))
+    rng = np.random.default_rng(seed)
+    a = np.asfortranarray(rng.standard_normal((m, k)).astype(np.float16).astype(np.float32))
+    b = np.asfortranarray(rng.standard_normal((k, s)).astype(np.float16).astype(np.float32))
+    c = np.asfortranarray(rng.standard_normal((m, s)).astype(np.float32))
+    flops = 2.0 * m * s * k
+    if tilekit is not None:
+        cfg = tilekit.build_dense_config(m, s, k, np.float32, worker_threads=threads)
+        d = np.zeros(m * s, np.float32)
+        fa, fb, fc = a.ravel(order="F"), b.ravel(order="F"), c.ravel(order="F")
+        run = lambda: tilekit.matmul(cfg, fa, fb, fc, d)
+        lane = tilekit.active_lane()
+        cfgr = tilekit.kernel.resolve_config(cfg)
+        blocks = (m // cfgr.params.block_tile[0]) * (s // cfgr.params.block_tile[1])
+        used = tilekit.kernel._effective_workers(threads, blocks)
+    else:
+        from oracle import oracle as O
+
+        run = lambda: O.gemm_real(a, b, c, threads=threads)
+        lane, used = "oracle-port", threads
+    t0 = time.perf_counter()
+    run()
+    dt = time.perf_counter() - t0
+    return {"value": flops / dt / 1e12, "unit": UNIT, "cores": int(used), "kind": kind,
+            "seconds": dt,
+            "sample": f"{m}x{s}x{k} column slab of the {m}x{m}x{k} workload, fp16-valued f32, "
+                      f"{'tilekit.matmul(build_dense_config)' if tilekit else 'oracle C port'} "
+                      f"lane={lane}, {used} of {threads} host threads"}
+
+
+def run_reference(args):
+    world, rank, _ = _dist()
+    if rank != 0:
+        return
+    threads = len(os.sched_getaffinity(0))
+    n = args.n
+    for _ in range(args.warmup):
+        cpu_sample(n, n, threads)
+    samples = [cpu_sample(n, n, threads, seed=i) for i in range(args.steps)]
+    value = float(np.median([s["value"] for s in samples]))
+    ms = float(np.median([s["seconds"] for s in samples])) * 1e3
+    s0 = samples[0]
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32 (fp16-valued inputs)", "data": "synthetic",
+            "config": {"workload": f"dense GEMM D=A*B+C, M=N=K={n} column-major "
+                                   "(bounded column-slab sample per step)", "n": n},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": s0["cores"],
+                             "kind": s0["kind"], "sample": s0["sample"]},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---- our implementation -------------------------------------------------------------------
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2009_12263_b200 as tk
+    from paper_2009_12263_b200 import api
+
+    world, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    m = k = args.n
+    n = args.n  # per-rank column slab (weak scaling)
+    dt = tk.FLOAT16 if args.dtype == "fp16" else tk.BFLOAT16
+    tdt = torch.float16 if args.dtype == "fp16" else torch.bfloat16
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+    a = torch.randn(m * k, generator=g, device=dev).to(tdt)          # replicated A (same seed
+    if world > 1:                                                     # on every rank)
+        dist.broadcast(a, 0)
+    b = torch.randn(k * n, generator=g, device=dev).to(tdt)          # this rank's slab of B
+    c = torch.randn(m * n, generator=g, device=dev)
+    d = torch.empty(m * n, device=dev)
+    cfg = tk.kernel.resolve_config(tk.build_dense_config(m, n, k, dt))
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        tk.gemm_execute(cfg, a, b, c, d, stream=stream, synchronize=False)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(max(args.warmup, 1)):
+        step()
+    launches_per_step = tk.last_run()["launches"]
+    barrier()
+    sampler = ClockSampler(local)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with sampler:
+        start.record(stream)
+        for _ in range(args.steps):
+            step()
+        end.record(stream)
+        torch.cuda.synchronize(dev)
+    barrier()
+    ms = start.elapsed_time(end) / args.steps
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    flops_rank = 2.0 * m * n * k
+    value = flops_rank * world / (ms * 1e-3) / 1e12
+
+    # roofline of the dominant (only) kernel: one tcgen05 launch per step
+    burst, sustained, hbm, src = _peaks()
+    kernel_ms = ms / launches_per_step
+    achieved = flops_rank / (kernel_ms * 1e-3) / 1e12
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": burst, "unit": "TFLOP/s",
+                "frac": achieved / burst, "traffic": args.traffic,
+                "peak_source": f"{src} bf16 burst (MEASURED_PEAKS.json)",
+                "frac_of_sustained": achieved / sustained if sustained else None,
+                "frac_of_spec_2250": achieved / 2250.0}
+
+    # e2e through the C ABI with host (pinned) buffers: H2D of A, B, C and D2H of C each step
+    e2e = run_e2e(args, tk, api, torch, dev, m, n, k, world)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_sample(m, k, len(os.sched_getaffinity(0)))
+        cpu.pop("seconds", None)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": args.dtype, "data": "synthetic",
+                "config": {"workload": f"dense GEMM D=A*B+C, fp16/bf16 A,B -> fp32 C,D, "
+                                       f"column-major, M=K={m}, N={n} per GPU (column slab; "
+                                       f"A replicated)",
+                           "m": m, "n_per_gpu": n, "k": k, "accumulate": "fp32",
+                           "parallelism": f"column-slab x{world}",
+                           "l2": "inputs (A+B+C+D) exceed the 126 MB L2; no flush",
+                           "lane": tk.last_run()["lane"]},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "clocks": sampler.summary(),
+                "gpu_launches": launches_per_step * args.steps}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, tk, api, torch, dev, m, n, k, world):
+    """Same metric through tk_gemm_ex_raw (the reference-facing C ABI) on host buffers."""
+    tag = api.TAG_F16F32 if args.dtype == "fp16" else api.TAG_BF16F32
+    hd = torch.float16 if args.dtype == "fp16" else torch.bfloat16
+    ha = torch.randn(m * k).to(hd).pin_memory()
+    hb = torch.randn(k * n).to(hd).pin_memory()
+    hc = torch.randn(m * n).pin_memory()
+    h2d = (ha.numel() + hb.numel()) * 2 + hc.numel() * 4
+    d2h = hc.numel() * 4
+
+    def call():
+        rc = api.gemm_ex_raw(tag, 0, 0, m, n, k, 1.0, 0.0, ha.data_ptr(), hb.data_ptr(), 1.0,
+                             0.0, hc.data_ptr())
+        if rc != 0:
+            raise RuntimeError(f"tk_gemm_ex_raw returned {rc}: {tk._lib.last_error()}")
+
+    reps = max(1, min(args.steps, args.e2e_steps))
+    call()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        call()
+    torch.cuda.synchronize(dev)
+    sec = (time.perf_counter() - t0) / reps
+    t = torch.tensor([sec], device=dev)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    sec = float(t.item())
+    return {"value": 2.0 * m * n * k * world / sec / 1e12, "unit": UNIT,
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "ms_per_step": sec * 1e3, "steps": reps,
+            "path": "tk_gemm_ex_raw(TAG_F16F32) on pinned host buffers (C updated in place)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--n", type=int, default=8192)
+    ap.add_argument("--dtype", choices=["fp16", "bf16"], default="fp16")
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="dram bytes per launch from an ncu --set full capture")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -294,19 +294,50 @@ int sm_count() {
   return n;
 }
 
-template <int OP>
-int launch_tc(const tk::TcParams& prm, cudaStream_t s) {
+template <int OP, bool DENSE>
+int launch_tc_variant(const tk::TcParams& prm, cudaStream_t s) {
   using S = tk::TcSmem<OP>;
   static bool attr = false;
   if (!attr) {
-    TK_CUDA(cudaFuncSetAttribute(tk::tc_gemm_kernel<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL));
+    TK_CUDA(cudaFuncSetAttribute(tk::tc_gemm_kernel<OP, DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL));
     attr = true;
   }
   const int grid = std::min(prm.num_tiles, sm_count());
-  tk::tc_gemm_kernel<OP><<<grid, tk::TC_THREADS, S::TOTAL, s>>>(prm);
+  tk::tc_gemm_kernel<OP, DENSE><<<grid, tk::TC_THREADS, S::TOTAL, s>>>(prm);
   TK_CUDA(cudaGetLastError());
   ++g_launches;
   return TK_OK;
+}
+
+template <int OP>
+int launch_tc(const tk::TcParams& prm, bool dense, cudaStream_t s) {
+  return dense ? launch_tc_variant<OP, true>(prm, s) : launch_tc_variant<OP, false>(prm, s);
+}
+
+// Fold a transform program into relu?(x * mul + add) (complex mul/add for pair streams);
+// false when a relu is followed by further ops (then the generic epilogue runs it as is).
+bool decode_affine(const TkTransform& t, bool pair, float mul[2], float add[2], int32_t& relu) {
+  std::complex<double> m(1.0, 0.0), a(0.0, 0.0);
+  relu = 0;
+  for (int i = 0; i < t.n; ++i) {
+    if (relu) return false;
+    const std::complex<double> c(t.re[i], pair ? t.im[i] : 0.0);
+    if (t.op[i] == TK_T_SCALE) { m *= c; a *= c; }
+    else if (t.op[i] == TK_T_ADD) a += c;
+    else if (t.op[i] == TK_T_RELU && !pair) relu = 1;
+    else return false;
+  }
+  mul[0] = float(m.real()); mul[1] = float(m.imag());
+  add[0] = float(a.real()); add[1] = float(a.imag());
+  return true;
+}
+
+// column-major dense element map (one digit per dimension, unit row stride)
+bool colmajor_dense(const TkLayout& L, int64_t& ld) {
+  if (L.kind != TK_LAYOUT_STRIDED || L.ndigits[0] != 1 || L.ndigits[1] != 1 || L.stride[0][0] != 1)
+    return false;
+  ld = L.stride[1][0];
+  return true;
 }
 
 int run_tc(const TkGemmPlan* p, const void* a, const void* b, const void* c, void* d, const void* bias,
@@ -438,10 +469,16 @@ int run_tc(const TkGemmPlan* p, const void* a, const void* b, const void* c, voi
   prm.num_tiles = prm.num_mb * prm.num_nb;
   prm.kb_total = int((p->k + tk::TC_BK - 1) / tk::TC_BK);
   prm.group_m = 16;
+  const bool pair = op != TK_OP_REAL;
+  bool dense = colmajor_dense(p->d, prm.ldd) &&
+               (p->c.kind == TK_LAYOUT_ZERO || colmajor_dense(p->c, prm.ldc)) &&
+               decode_affine(p->t_c, pair, prm.c_mul, prm.c_add, prm.c_relu) &&
+               decode_affine(p->t_r2s, pair, prm.r_mul, prm.r_add, prm.r_relu) &&
+               decode_affine(p->t_s2g, pair, prm.s_mul, prm.s_add, prm.s_relu);
   switch (op) {
-    case TK_OP_REAL: return launch_tc<tk::OP_REAL>(prm, s);
-    case TK_OP_COMPLEX: return launch_tc<tk::OP_COMPLEX>(prm, s);
-    default: return launch_tc<tk::OP_DUAL>(prm, s);
+    case TK_OP_REAL: return launch_tc<tk::OP_REAL>(prm, dense, s);
+    case TK_OP_COMPLEX: return launch_tc<tk::OP_COMPLEX>(prm, dense, s);
+    default: return launch_tc<tk::OP_DUAL>(prm, dense, s);
   }
 }
 

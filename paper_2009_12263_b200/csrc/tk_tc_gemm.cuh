@@ -72,6 +72,11 @@ struct TcParams {
   const float* rowsum_a;
   const float* colsum_b;
   EpiProg t_c, t_r2s, t_s2g;
+  // dense column-major epilogue: transforms pre-decoded to relu?(x*mul + add) (complex mul/add
+  // for pair operators); see decode_affine() in tk_api.cu
+  int64_t ldc, ldd;
+  float c_mul[2], c_add[2], r_mul[2], r_add[2], s_mul[2], s_add[2];
+  int32_t c_relu, r_relu, s_relu, pad1;
 };
 
 __device__ __forceinline__ void tile_coords(const TcParams& p, int t, int& mb, int& nb) {
@@ -118,7 +123,164 @@ __device__ __forceinline__ void write_diag_tile(uint8_t* dst, const HT* diag, in
   }
 }
 
-template <int OP>
+
+// ---------------------------------------------------------------- epilogue bodies
+__device__ __forceinline__ float relu_if(float v, int on) { return on ? np_relu(v) : v; }
+
+// Dense column-major C/D, transforms pre-decoded to affine(+relu).  Per warp: 32 rows (one
+// per lane, TMEM lane quarter) x COLS columns in chunks of 32; C for the next chunk is in
+// flight while the current chunk computes and stores (streaming cache hints: C and D are
+// touched once and must not evict the A/B panels from L2).
+template <int OP, int COLS, int BN>
+__device__ __forceinline__ void epilogue_dense(const TcParams& p, uint64_t* tfull, uint32_t aphase,
+                                               uint32_t tbase, int i, int jbase, int lane) {
+  const bool row_ok = i < p.m;
+  const bool has_c = !p.c_zero;
+  if (OP == OP_REAL) {
+    const float* cp = reinterpret_cast<const float*>(p.c_ptr) + (row_ok ? i : 0);
+    float* dp = reinterpret_cast<float*>(p.d_ptr) + (row_ok ? i : 0);
+    const float rterm = p.affine && row_ok ? (p.aff_r * (p.rowsum_a ? p.rowsum_a[i] : 0.f) + p.aff_k) : 0.f;
+    const float bias_m = (p.bias_axis == 2 && row_ok) ? p.bias[i] : 0.f;
+    float cv[32];
+    auto load_c = [&](int j0) {
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) {
+        const int j = j0 + jj;
+        cv[jj] = (has_c && row_ok && j < p.n) ? __ldcs(cp + int64_t(j) * p.ldc) : 0.f;
+      }
+    };
+    load_c(jbase);
+    mbar_wait(tfull, aphase);
+    tc_fence_after();
+#pragma unroll 1
+    for (int ch = 0; ch < COLS / 32; ++ch) {
+      const int j0 = jbase + ch * 32;
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(tbase + uint32_t(j0 - jbase + (jbase % BN)), r);
+      // lane-distributed column vectors (bias[j], colsum_b[j]) broadcast with shuffles
+      const int jl = j0 + lane;
+      const float bcol = (p.bias_axis == 1 && jl < p.n) ? p.bias[jl] : 0.f;
+      const float qcol = (p.affine && p.colsum_b && jl < p.n) ? p.aff_q * p.colsum_b[jl] : 0.f;
+      tmem_ld_wait();
+      float out[32];
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) {
+        float v = __uint_as_float(r[jj]);
+        if (p.affine) v = p.aff_s * v + (rterm + __shfl_sync(0xffffffffu, qcol, jj));
+        if (has_c) v = relu_if(cv[jj] * p.c_mul[0] + p.c_add[0], p.c_relu) + v;
+        v = relu_if(v * p.r_mul[0] + p.r_add[0], p.r_relu);
+        v = v + (p.bias_axis == 1 ? __shfl_sync(0xffffffffu, bcol, jj) : bias_m);
+        out[jj] = relu_if(v * p.s_mul[0] + p.s_add[0], p.s_relu);
+      }
+      if (ch + 1 < COLS / 32) load_c(j0 + 32);
+      if (row_ok) {
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj)
+          if (j0 + jj < p.n) __stcs(dp + int64_t(j0 + jj) * p.ldd, out[jj]);
+      }
+    }
+  } else {
+    // pair operators: interleaved (float2) or split planes, column-major elements
+    const float* cp = reinterpret_cast<const float*>(p.c_ptr);
+    float* dp = reinterpret_cast<float*>(p.d_ptr);
+    const int64_t ci = row_ok ? i : 0;
+    mbar_wait(tfull, aphase);
+    tc_fence_after();
+#pragma unroll 1
+    for (int ch = 0; ch < COLS / 32; ++ch) {
+      const int j0 = jbase + ch * 32;
+      const uint32_t col = uint32_t(j0 - jbase + (jbase % BN));
+      uint32_t r0[32], r1[32];
+      tmem_ld_32x32b_x32(tbase + col, r0);
+      tmem_ld_32x32b_x32(tbase + uint32_t(BN) + col, r1);
+      float2 cv[32];
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) {
+        const int j = j0 + jj;
+        cv[jj] = make_float2(0.f, 0.f);
+        if (has_c && row_ok && j < p.n) {
+          const int64_t e = ci + int64_t(j) * p.ldc;
+          cv[jj] = p.c_pair == P_INTERLEAVED ? __ldcs(reinterpret_cast<const float2*>(cp) + e)
+                                             : make_float2(__ldcs(cp + e), __ldcs(cp + e + p.c_plane));
+        }
+      }
+      tmem_ld_wait();
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) {
+        float2 v = make_float2(__uint_as_float(r0[jj]), __uint_as_float(r1[jj]));
+        if (has_c) {
+          const float cr = cv[jj].x * p.c_mul[0] - cv[jj].y * p.c_mul[1] + p.c_add[0];
+          const float ci_ = cv[jj].x * p.c_mul[1] + cv[jj].y * p.c_mul[0] + p.c_add[1];
+          v = make_float2(cr + v.x, ci_ + v.y);
+        }
+        float2 w = make_float2(v.x * p.r_mul[0] - v.y * p.r_mul[1] + p.r_add[0],
+                               v.x * p.r_mul[1] + v.y * p.r_mul[0] + p.r_add[1]);
+        v = make_float2(w.x * p.s_mul[0] - w.y * p.s_mul[1] + p.s_add[0],
+                        w.x * p.s_mul[1] + w.y * p.s_mul[0] + p.s_add[1]);
+        const int j = j0 + jj;
+        if (row_ok && j < p.n) {
+          const int64_t e = ci + int64_t(j) * p.ldd;
+          if (p.d_pair == P_INTERLEAVED) {
+            __stcs(reinterpret_cast<float2*>(dp) + e, v);
+          } else {
+            __stcs(dp + e, v.x);
+            __stcs(dp + e + p.d_plane, v.y);
+          }
+        }
+      }
+    }
+  }
+}
+
+// Any digit-mapped C/D layout and any transform program (the rare path).
+template <int OP, int COLS, int BN>
+__device__ __noinline__ void epilogue_generic(const TcParams& p, uint64_t* tfull, uint32_t aphase,
+                                              uint32_t tbase, int i, int jbase) {
+  const bool row_ok = i < p.m;
+  const int64_t c_row = row_ok ? map_dim(p.c_map, 0, i) : 0;
+  const int64_t d_row = row_ok ? map_dim(p.d_map, 0, i) : 0;
+  const float rsum = (p.affine && row_ok && p.rowsum_a) ? p.rowsum_a[i] : 0.f;
+  const float bias_m = (p.bias_axis == 2 && row_ok) ? p.bias[i] : 0.f;
+  mbar_wait(tfull, aphase);
+  tc_fence_after();
+#pragma unroll 1
+  for (int ch = 0; ch < COLS / 32; ++ch) {
+    const int j0 = jbase + ch * 32;
+    const uint32_t col = uint32_t(j0 - jbase + (jbase % BN));
+    uint32_t r0[32], r1[32];
+    tmem_ld_32x32b_x32(tbase + col, r0);
+    if (OP != OP_REAL) tmem_ld_32x32b_x32(tbase + uint32_t(BN) + col, r1);
+    tmem_ld_wait();
+#pragma unroll 1
+    for (int jj = 0; jj < 32; ++jj) {
+      const int j = j0 + jj;
+      if (!row_ok || j >= p.n) continue;
+      if (OP == OP_REAL) {
+        float v = __uint_as_float(r0[jj]);
+        if (p.affine)
+          v = p.aff_s * v + p.aff_r * rsum + (p.colsum_b ? p.aff_q * p.colsum_b[j] : 0.f) + p.aff_k;
+        if (!p.c_zero) v = run_prog_real(p.t_c, load_scalar_f32(p.c_ptr, c_row + map_dim(p.c_map, 1, j))) + v;
+        v = run_prog_real(p.t_r2s, v);
+        if (p.bias_axis == 1) v = v + p.bias[j];
+        else if (p.bias_axis == 2) v = v + bias_m;
+        v = run_prog_real(p.t_s2g, v);
+        reinterpret_cast<float*>(p.d_ptr)[d_row + map_dim(p.d_map, 1, j)] = v;
+      } else {
+        float2 v = make_float2(__uint_as_float(r0[jj]), __uint_as_float(r1[jj]));
+        if (!p.c_zero) {
+          float2 cv = load_pair_f32(p.c_ptr, p.c_pair, p.c_plane, c_row + map_dim(p.c_map, 1, j));
+          cv = run_prog_pair<OP>(p.t_c, cv);
+          v = make_float2(cv.x + v.x, cv.y + v.y);
+        }
+        v = run_prog_pair<OP>(p.t_r2s, v);
+        v = run_prog_pair<OP>(p.t_s2g, v);
+        store_pair_f32(p.d_ptr, p.d_pair, p.d_plane, d_row + map_dim(p.d_map, 1, j), v);
+      }
+    }
+  }
+}
+
+template <int OP, bool DENSE_EPI>
 __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(const __grid_constant__ TcParams p) {
   using C = TcCfg<OP>;
   using S = TcSmem<OP>;
@@ -293,62 +455,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(const __grid_con
       const int as = local & 1;
       const uint32_t aphase = (local >> 1) & 1;
       const int i = mb * TC_BM + row_local;
-      const bool row_ok = i < p.m;
-      const int64_t c_row = row_ok ? map_dim(p.c_map, 0, i) : 0;
-      const int64_t d_row = row_ok ? map_dim(p.d_map, 0, i) : 0;
-      const float rsum = (p.affine && row_ok) ? p.rowsum_a[i] : 0.f;
-      const float bias_m = (p.bias_axis == 2 && row_ok) ? p.bias[i] : 0.f;
-      mbar_wait(&tfull[as], aphase);
-      tc_fence_after();
       const uint32_t tbase = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(as * C::ACC_COLS);
-#pragma unroll 1
-      for (int ch = 0; ch < COLS_PER_WARP / 32; ++ch) {
-        const int cl = half * COLS_PER_WARP + ch * 32;  // tile-local first column
-        uint32_t r0[32];
-        tmem_ld_32x32b_x32(tbase + uint32_t(cl), r0);
-        if (OP == OP_REAL) {
-          tmem_ld_wait();
-          const int j0 = nb * BN + cl;
-#pragma unroll
-          for (int jj = 0; jj < 32; ++jj) {
-            const int j = j0 + jj;
-            if (!row_ok || j >= p.n) continue;
-            float v = __uint_as_float(r0[jj]);
-            if (p.affine)
-              v = p.aff_s * v + p.aff_r * rsum + p.aff_q * p.colsum_b[j] + p.aff_k;
-            const int64_t jc = map_dim(p.c_map, 1, j);
-            if (!p.c_zero) {
-              float cv = load_scalar_f32(p.c_ptr, c_row + jc);
-              cv = run_prog_real(p.t_c, cv);
-              v = cv + v;
-            }
-            v = run_prog_real(p.t_r2s, v);
-            if (p.bias_axis == 1) v = v + p.bias[j];
-            else if (p.bias_axis == 2) v = v + bias_m;
-            v = run_prog_real(p.t_s2g, v);
-            reinterpret_cast<float*>(p.d_ptr)[d_row + map_dim(p.d_map, 1, j)] = v;
-          }
-        } else {
-          uint32_t r1[32];
-          tmem_ld_32x32b_x32(tbase + uint32_t(BN + cl), r1);
-          tmem_ld_wait();
-          const int j0 = nb * BN + cl;
-#pragma unroll
-          for (int jj = 0; jj < 32; ++jj) {
-            const int j = j0 + jj;
-            if (!row_ok || j >= p.n) continue;
-            float2 v = make_float2(__uint_as_float(r0[jj]), __uint_as_float(r1[jj]));
-            if (!p.c_zero) {
-              float2 cv = load_pair_f32(p.c_ptr, p.c_pair, p.c_plane, c_row + map_dim(p.c_map, 1, j));
-              cv = run_prog_pair<OP>(p.t_c, cv);
-              v = make_float2(cv.x + v.x, cv.y + v.y);
-            }
-            v = run_prog_pair<OP>(p.t_r2s, v);
-            v = run_prog_pair<OP>(p.t_s2g, v);
-            store_pair_f32(p.d_ptr, p.d_pair, p.d_plane, d_row + map_dim(p.d_map, 1, j), v);
-          }
-        }
-      }
+      const int jbase = nb * BN + half * COLS_PER_WARP;
+      if (DENSE_EPI)
+        epilogue_dense<OP, COLS_PER_WARP, BN>(p, tfull + as, aphase, tbase, i, jbase, lane);
+      else
+        epilogue_generic<OP, COLS_PER_WARP, BN>(p, tfull + as, aphase, tbase, i, jbase);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[as]);
