@@ -18,6 +18,7 @@
 #include "tk_prep.cuh"
 #include "tk_simt.cuh"
 #include "tk_tc_gemm.cuh"
+#include "tk_tc_gemm2.cuh"
 
 namespace {
 
@@ -309,6 +310,30 @@ int launch_tc_variant(const tk::TcParams& prm, cudaStream_t s) {
   return TK_OK;
 }
 
+template <bool DENSE>
+int launch_tc_pair(const tk::TcParams& prm, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    TK_CUDA(cudaFuncSetAttribute(tk::tc_gemm_pair_kernel<DENSE>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, tk::TC2_SMEM));
+    attr = true;
+  }
+  const int grid = 2 * std::min(prm.num_tiles, sm_count() / 2);
+  tk::tc_gemm_pair_kernel<DENSE><<<grid, tk::TC_THREADS, tk::TC2_SMEM, s>>>(prm);
+  TK_CUDA(cudaGetLastError());
+  ++g_launches;
+  return TK_OK;
+}
+
+// TK_TC_KERNEL=pair|single forces the CTA-pair / single-CTA tcgen05 kernel (tests, tuning)
+int tc_kernel_override() {
+  const char* e = getenv("TK_TC_KERNEL");
+  if (!e) return 0;
+  if (!strcmp(e, "pair")) return 2;
+  if (!strcmp(e, "single")) return 1;
+  return 0;
+}
+
 template <int OP>
 int launch_tc(const tk::TcParams& prm, bool dense, cudaStream_t s) {
   return dense ? launch_tc_variant<OP, true>(prm, s) : launch_tc_variant<OP, false>(prm, s);
@@ -355,6 +380,8 @@ int run_tc(const TkGemmPlan* p, const void* a, const void* b, const void* c, voi
 
   // ---- A operand
   const void* a_pl[2] = {a, nullptr};
+  const void* a_plane0 = a;
+  const void* b_plane0 = b;
   if (p->a.kind == TK_LAYOUT_DIAGONAL) {
     prm.diag_a = 1;
     prm.diag = a;
@@ -375,6 +402,7 @@ int run_tc(const TkGemmPlan* p, const void* a, const void* b, const void* c, voi
       a_pl[0] = p0;
       a_pl[1] = p0 + vol;
     }
+    a_plane0 = a_pl[0];
     for (int pl = 0; pl < planes; ++pl) {
       int rc = mn ? make_map_2d(&prm.ta[pl], a_pl[pl], p->a.scalar, p->m, p->k, pitch, 64, 64)
                   : make_map_2d(&prm.ta[pl], a_pl[pl], p->a.scalar, p->k, p->m, pitch, 64, 128);
@@ -400,6 +428,7 @@ int run_tc(const TkGemmPlan* p, const void* a, const void* b, const void* c, voi
       b_pl[0] = p0;
       b_pl[1] = p0 + vol;
     }
+    b_plane0 = b_pl[0];
     for (int pl = 0; pl < planes; ++pl) {
       int rc = mn_k ? make_map_2d(&prm.tb[pl], b_pl[pl], p->b.scalar, p->k, p->n, pitch, 64, BN)
                     : make_map_2d(&prm.tb[pl], b_pl[pl], p->b.scalar, p->n, p->k, pitch, 64, 64);
@@ -475,6 +504,26 @@ int run_tc(const TkGemmPlan* p, const void* a, const void* b, const void* c, voi
                decode_affine(p->t_c, pair, prm.c_mul, prm.c_add, prm.c_relu) &&
                decode_affine(p->t_r2s, pair, prm.r_mul, prm.r_add, prm.r_relu) &&
                decode_affine(p->t_s2g, pair, prm.s_mul, prm.s_add, prm.s_relu);
+  if (op == TK_OP_REAL && !prm.diag_a) {
+    // CTA pair (256x256 tiles) once there are enough pair tiles to cover the SMs
+    const int64_t pair_tiles = ((p->m + 255) / 256) * ((p->n + tk::TC2_BN - 1) / tk::TC2_BN);
+    const int ov = tc_kernel_override();
+    if (ov == 2 || (ov == 0 && pair_tiles >= sm_count() / 2)) {
+      tk::TcParams pp = prm;
+      pp.num_mb = int((p->m + 255) / 256);
+      pp.num_nb = int((p->n + tk::TC2_BN - 1) / tk::TC2_BN);
+      pp.num_tiles = pp.num_mb * pp.num_nb;
+      // per-CTA halves: A box 128 rows (K-major) / B box 128 columns (K-major)
+      int mn;
+      int64_t pitch;
+      int rc;
+      tma_operand(p->a, mn, pitch);
+      if (!mn && (rc = make_map_2d(&pp.ta[0], a_plane0, p->a.scalar, p->k, p->m, pitch, 64, 128))) return rc;
+      tma_operand(p->b, mn, pitch);
+      if (mn && (rc = make_map_2d(&pp.tb[0], b_plane0, p->b.scalar, p->k, p->n, pitch, 64, 128))) return rc;
+      return dense ? launch_tc_pair<true>(pp, s) : launch_tc_pair<false>(pp, s);
+    }
+  }
   switch (op) {
     case TK_OP_REAL: return launch_tc<tk::OP_REAL>(prm, dense, s);
     case TK_OP_COMPLEX: return launch_tc<tk::OP_COMPLEX>(prm, dense, s);

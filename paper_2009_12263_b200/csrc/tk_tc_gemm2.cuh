@@ -1,0 +1,167 @@
+// tk_tc_gemm2.cuh -- the CTA-pair (cta_group::2) tcgen05 GEMM for the real operator.
+//
+// A cluster of two CTAs on one TPC computes a 256 x 256 output tile with 256x256x16
+// tcgen05.mma.cta_group::2 instructions issued by the leader CTA's MMA thread:
+//   * each CTA stages its own 128 rows of A and its own 128 columns of B (half of the pair's N),
+//     so per-SM shared-memory operand traffic is half of the single-CTA 128x256 form;
+//   * both CTAs' TMA loads credit the leader's full barrier (2-SM TMA form);
+//   * MMA completion is multicast to both CTAs' empty / accumulator-full barriers;
+//   * each CTA's TMEM holds its 128 rows x 256 FP32 columns (double-buffered, 512 columns);
+//     both CTAs' epilogue warps release a TMEM stage by arriving on the leader's barrier.
+// The epilogue is the same fused TMEM -> register -> global path as the single-CTA kernel.
+#pragma once
+#include "tk_tc_gemm.cuh"
+
+namespace tk {
+
+constexpr int TC2_BN = 256;                 // pair tile N (instruction N)
+constexpr int TC2_STAGES = 6;
+constexpr int TC2_TILE_BYTES = 128 * 64 * 2;  // A (128 rows) or B (128 cols) per CTA per stage
+constexpr int TC2_STAGE_BYTES = 2 * TC2_TILE_BYTES;
+constexpr int TC2_BAR_OFFSET = TC2_STAGES * TC2_STAGE_BYTES;
+constexpr int TC2_SMEM = TC2_BAR_OFFSET + 256 + 1024;
+
+template <bool DENSE_EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
+    tc_gemm_pair_kernel(const __grid_constant__ TcParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + TC2_BAR_OFFSET);
+  uint64_t* empty = full + TC2_STAGES;
+  uint64_t* tfull = empty + TC2_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x >> 1;
+  const int nclusters = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&p.ta[0]);
+    tma_prefetch(&p.tb[0]);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < TC2_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 2 * TC_EPI_WARPS);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) {
+    tmem_alloc_pair(tmem_slot, 512);
+    tmem_relinquish_pair();
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto a_tile = [&](int s) -> uint8_t* { return smem + s * TC2_STAGE_BYTES; };
+  auto b_tile = [&](int s) -> uint8_t* { return smem + s * TC2_STAGE_BYTES + TC2_TILE_BYTES; };
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer (both CTAs)
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_normal();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cluster; t < p.num_tiles; t += nclusters) {
+        int mb, nb;
+        tile_coords(p, t, mb, nb);
+        const int m0 = mb * 256 + int(rank) * 128;     // this CTA's rows of A
+        const int n0 = nb * TC2_BN + int(rank) * 128;  // this CTA's columns of B
+        for (int kb = 0; kb < p.kb_total; ++kb) {
+          const int k0 = kb * TC_BK;
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * TC2_STAGE_BYTES);
+          const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
+          if (p.a_mn) {
+            tma_load_2d_pair(a_tile(stage), &p.ta[0], fb, m0, k0, pol);
+            tma_load_2d_pair(a_tile(stage) + 8192, &p.ta[0], fb, m0 + 64, k0, pol);
+          } else {
+            tma_load_2d_pair(a_tile(stage), &p.ta[0], fb, k0, m0, pol);
+          }
+          if (p.b_mn) {
+            tma_load_2d_pair(b_tile(stage), &p.tb[0], fb, n0, k0, pol);
+            tma_load_2d_pair(b_tile(stage) + 8192, &p.tb[0], fb, n0 + 64, k0, pol);
+          } else {
+            tma_load_2d_pair(b_tile(stage), &p.tb[0], fb, k0, n0, pol);
+          }
+          if (++stage == TC2_STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader only)
+    if (leader && lane == 0) {
+      const uint32_t idesc = idesc_f16(p.ab_fmt, p.a_mn, p.b_mn, 0, 256, TC2_BN);
+      const uint32_t a_step = p.a_mn ? 2048u : 32u;
+      const uint32_t b_step = p.b_mn ? 2048u : 32u;
+      const uint32_t a_lbo = p.a_mn ? 8192u : 16u;
+      const uint32_t b_lbo = p.b_mn ? 8192u : 16u;
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int t = cluster; t < p.num_tiles; t += nclusters, ++local) {
+        const int as = local & 1;
+        const uint32_t aphase = (local >> 1) & 1;
+        mbar_wait(&tempty[as], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d0 = tmem_base + uint32_t(as * 256);
+        for (int kb = 0; kb < p.kb_total; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < TC_BK / 16; ++kk) {
+            const uint64_t a0 = sdesc_sw128(smem_u32(a_tile(stage)) + kk * a_step, a_lbo, 1024);
+            const uint64_t b0 = sdesc_sw128(smem_u32(b_tile(stage)) + kk * b_step, b_lbo, 1024);
+            tc_mma_f16_pair(d0, a0, b0, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+          }
+          tc_commit_pair(&empty[stage], 0x3);
+          if (++stage == TC2_STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc_commit_pair(&tfull[as], 0x3);
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    const int ew = warp - 4;
+    const int quarter = warp & 3;
+    const int half = ew >> 2;
+    const int row_local = quarter * 32 + lane;
+    int local = 0;
+    for (int t = cluster; t < p.num_tiles; t += nclusters, ++local) {
+      int mb, nb;
+      tile_coords(p, t, mb, nb);
+      const int as = local & 1;
+      const uint32_t aphase = (local >> 1) & 1;
+      const int i = mb * 256 + int(rank) * 128 + row_local;
+      const uint32_t tbase = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(as * 256);
+      const int jbase = nb * TC2_BN + half * 128;
+      if (DENSE_EPI)
+        epilogue_dense<OP_REAL, 128, TC2_BN>(p, tfull + as, aphase, tbase, i, jbase, lane);
+      else
+        epilogue_generic<OP_REAL, 128, TC2_BN>(p, tfull + as, aphase, tbase, i, jbase);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[as]), 0));
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, 512);
+  }
+}
+
+}  // namespace tk

@@ -39,11 +39,18 @@ def _f32(x):
     return np.asarray(x).astype(np.float32)
 
 
+@pytest.fixture(params=["single", "pair"])
+def tc_kernel(request, monkeypatch):
+    """Pin the single-CTA (128x256) or CTA-pair (256x256) tcgen05 kernel."""
+    monkeypatch.setenv("TK_TC_KERNEL", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("dtype", [np.float16, "bf16"])
 @pytest.mark.parametrize("trans", ["nn", "nt", "tn", "tt"])
-def test_dense_integer_exact(cuda, dtype, trans):
+def test_dense_integer_exact(cuda, dtype, trans, tc_kernel):
     dtype = tk.BFLOAT16 if dtype == "bf16" else np.dtype(dtype)
-    m, n, k = 256, 512, 320
+    m, n, k = 384, 640, 320
     ta, tb = trans[0] == "t", trans[1] == "t"
     rng = np.random.default_rng(0)
     a = _half(rng, (m, k), dtype, True)
@@ -63,7 +70,7 @@ def test_dense_integer_exact(cuda, dtype, trans):
 @pytest.mark.parametrize("dtype", [np.float16, "bf16"])
 @pytest.mark.parametrize("mnk", [(128, 256, 64), (1024, 1024, 1024), (384, 768, 2048),
                                  (200, 136, 72), (8, 16, 8), (1000, 520, 4104)])
-def test_dense_random_within_tolerance(cuda, dtype, mnk):
+def test_dense_random_within_tolerance(cuda, dtype, mnk, tc_kernel):
     dtype = tk.BFLOAT16 if dtype == "bf16" else np.dtype(dtype)
     m, n, k = mnk
     rng = np.random.default_rng(1)
