@@ -74,17 +74,16 @@ class ClockSampler:
     def _run(self):
         while not self._stop.is_set():
             try:
-                util = self.nv.nvmlDeviceGetUtilizationRates(self.h).gpu
                 mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
                 mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                if util > 0:
+                if not mask & 0x1:  # not idle
                     self.samples.append(mhz)
                     for bit, name in self.REASONS.items():
                         if mask & bit and name != "gpu_idle":
                             self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.01)
+            time.sleep(0.002)
 
     def __enter__(self):
         if self.ok:

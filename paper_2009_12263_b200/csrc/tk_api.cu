@@ -497,7 +497,8 @@ int run_tc(const TkGemmPlan* p, const void* a, const void* b, const void* c, voi
   prm.num_nb = int((p->n + BN - 1) / BN);
   prm.num_tiles = prm.num_mb * prm.num_nb;
   prm.kb_total = int((p->k + tk::TC_BK - 1) / tk::TC_BK);
-  prm.group_m = 16;
+  prm.group_m = 8;
+  if (const char* g = getenv("TK_GROUP_M")) prm.group_m = std::max(1, atoi(g));
   const bool pair = op != TK_OP_REAL;
   bool dense = colmajor_dense(p->d, prm.ldd) &&
                (p->c.kind == TK_LAYOUT_ZERO || colmajor_dense(p->c, prm.ldc)) &&
