@@ -499,6 +499,9 @@ int run_tc(const TkGemmPlan* p, const void* a, const void* b, const void* c, voi
   prm.kb_total = int((p->k + tk::TC_BK - 1) / tk::TC_BK);
   prm.group_m = 8;
   if (const char* g = getenv("TK_GROUP_M")) prm.group_m = std::max(1, atoi(g));
+  if (const char* g = getenv("TK_DBG_SKIP_EPI")) prm.dbg_skip_epi = atoi(g);
+  prm.pol_ab = 1;  // A/B panels are re-read by neighbouring tiles: keep them in L2
+  if (const char* g = getenv("TK_POLICY_AB")) prm.pol_ab = atoi(g);
   const bool pair = op != TK_OP_REAL;
   bool dense = colmajor_dense(p->d, prm.ldd) &&
                (p->c.kind == TK_LAYOUT_ZERO || colmajor_dense(p->c, prm.ldc)) &&

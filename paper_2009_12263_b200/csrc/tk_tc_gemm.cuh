@@ -77,6 +77,7 @@ struct TcParams {
   int64_t ldc, ldd;
   float c_mul[2], c_add[2], r_mul[2], r_add[2], s_mul[2], s_add[2];
   int32_t c_relu, r_relu, s_relu, pad1;
+  int32_t dbg_skip_epi, pol_ab;  // tuning/diagnostic knobs (TK_DBG_SKIP_EPI, TK_POLICY_AB)
 };
 
 __device__ __forceinline__ void tile_coords(const TcParams& p, int t, int& mb, int& nb) {

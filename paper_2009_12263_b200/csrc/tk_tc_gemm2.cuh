@@ -70,7 +70,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ producer (both CTAs)
     if (lane == 0) {
-      const uint64_t pol = policy_evict_normal();
+      const uint64_t pol = p.pol_ab ? policy_evict_last() : policy_evict_normal();
       int stage = 0;
       uint32_t phase = 0;
       for (int t = cluster; t < p.num_tiles; t += nclusters) {
@@ -146,7 +146,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       const int i = mb * 256 + int(rank) * 128 + row_local;
       const uint32_t tbase = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(as * 256);
       const int jbase = nb * TC2_BN + half * 128;
-      if (DENSE_EPI)
+      if (p.dbg_skip_epi) {
+        mbar_wait(tfull + as, aphase);
+        tc_fence_after();
+      } else if (DENSE_EPI)
         epilogue_dense<OP_REAL, 128, TC2_BN>(p, tfull + as, aphase, tbase, i, jbase, lane);
       else
         epilogue_generic<OP_REAL, 128, TC2_BN>(p, tfull + as, aphase, tbase, i, jbase);
