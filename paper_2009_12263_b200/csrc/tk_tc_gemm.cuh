@@ -337,8 +337,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(const __grid_con
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
-    const uint64_t pol_a = policy_evict_normal();
-    const uint64_t pol_b = policy_evict_normal();
+    const uint64_t pol_a = p.pol_ab ? policy_evict_last() : policy_evict_normal();
+    const uint64_t pol_b = pol_a;
     const uint32_t a_bytes = p.diag_a ? 0u : uint32_t(TC_A_TILE_BYTES * C::PLANES);
     const uint32_t tx_bytes = a_bytes + uint32_t(S::B_TILE_BYTES * C::PLANES);
     int stage = 0;
