@@ -19,6 +19,7 @@
 #include "tk_simt.cuh"
 #include "tk_tc_gemm.cuh"
 #include "tk_tc_gemm2.cuh"
+#include "tk_tc_gemm4.cuh"
 
 namespace {
 
@@ -318,18 +319,74 @@ int launch_tc_pair(const tk::TcParams& prm, cudaStream_t s) {
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, tk::TC2_SMEM));
     attr = true;
   }
-  const int grid = 2 * std::min(prm.num_tiles, sm_count() / 2);
+  static int max_clusters = 0;
+  if (!max_clusters) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * (sm_count() / 2));
+    cfg.blockDim = dim3(tk::TC_THREADS);
+    cfg.dynamicSmemBytes = tk::TC2_SMEM;
+    cudaLaunchAttribute at;
+    at.id = cudaLaunchAttributeClusterDimension;
+    at.val.clusterDim.x = 2;
+    at.val.clusterDim.y = 1;
+    at.val.clusterDim.z = 1;
+    cfg.attrs = &at;
+    cfg.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&max_clusters, tk::tc_gemm_pair_kernel<DENSE>, &cfg) != cudaSuccess ||
+        max_clusters <= 0) {
+      cudaGetLastError();
+      max_clusters = sm_count() / 2;
+    }
+    if (getenv("TK_VERBOSE")) fprintf(stderr, "tk: pair kernel max active clusters %d\n", max_clusters);
+  }
+  const int grid = 2 * std::min(prm.num_tiles, max_clusters);
   tk::tc_gemm_pair_kernel<DENSE><<<grid, tk::TC_THREADS, tk::TC2_SMEM, s>>>(prm);
   TK_CUDA(cudaGetLastError());
   ++g_launches;
   return TK_OK;
 }
 
-// TK_TC_KERNEL=pair|single forces the CTA-pair / single-CTA tcgen05 kernel (tests, tuning)
+template <bool DENSE>
+int launch_tc_quad(const tk::TcParams& prm, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    TK_CUDA(cudaFuncSetAttribute(tk::tc_gemm_quad_kernel<DENSE>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, tk::TC2_SMEM));
+    attr = true;
+  }
+  static int max_clusters = 0;
+  if (!max_clusters) {  // 4-CTA clusters do not tile every GPC: ask how many are co-resident
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(4 * (sm_count() / 4));
+    cfg.blockDim = dim3(tk::TC_THREADS);
+    cfg.dynamicSmemBytes = tk::TC2_SMEM;
+    cudaLaunchAttribute at;
+    at.id = cudaLaunchAttributeClusterDimension;
+    at.val.clusterDim.x = 4;
+    at.val.clusterDim.y = 1;
+    at.val.clusterDim.z = 1;
+    cfg.attrs = &at;
+    cfg.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&max_clusters, tk::tc_gemm_quad_kernel<DENSE>, &cfg) != cudaSuccess ||
+        max_clusters <= 0) {
+      cudaGetLastError();
+      max_clusters = sm_count() / 4;
+    }
+    if (getenv("TK_VERBOSE")) fprintf(stderr, "tk: quad kernel max active clusters %d\n", max_clusters);
+  }
+  const int grid = 4 * std::min(prm.num_tiles, max_clusters);
+  tk::tc_gemm_quad_kernel<DENSE><<<grid, tk::TC_THREADS, tk::TC2_SMEM, s>>>(prm);
+  TK_CUDA(cudaGetLastError());
+  ++g_launches;
+  return TK_OK;
+}
+
+// TK_TC_KERNEL=quad|pair|single forces the CTA-pair / single-CTA tcgen05 kernel (tests, tuning)
 int tc_kernel_override() {
   const char* e = getenv("TK_TC_KERNEL");
   if (!e) return 0;
   if (!strcmp(e, "pair")) return 2;
+  if (!strcmp(e, "quad")) return 4;
   if (!strcmp(e, "single")) return 1;
   return 0;
 }
@@ -512,6 +569,18 @@ int run_tc(const TkGemmPlan* p, const void* a, const void* b, const void* c, voi
     // CTA pair (256x256 tiles) once there are enough pair tiles to cover the SMs
     const int64_t pair_tiles = ((p->m + 255) / 256) * ((p->n + tk::TC2_BN - 1) / tk::TC2_BN);
     const int ov = tc_kernel_override();
+    if (ov == 4) {
+      tk::TcParams pp = prm;
+      pp.num_mb = int((p->m + 511) / 512);
+      pp.num_nb = int((p->n + tk::TC2_BN - 1) / tk::TC2_BN);
+      pp.num_tiles = pp.num_mb * pp.num_nb;
+      int mn;
+      int64_t pitch;
+      int rc;
+      tma_operand(p->b, mn, pitch);  // 64x64 B sub-boxes for both majors
+      if (mn && (rc = make_map_2d(&pp.tb[0], b_plane0, p->b.scalar, p->k, p->n, pitch, 64, 64))) return rc;
+      return dense ? launch_tc_quad<true>(pp, s) : launch_tc_quad<false>(pp, s);
+    }
     if (ov == 2 || (ov == 0 && pair_tiles >= sm_count() / 2)) {
       tk::TcParams pp = prm;
       pp.num_mb = int((p->m + 255) / 256);

@@ -223,3 +223,28 @@ __device__ __forceinline__ void tc_mma_f16_pair(uint32_t d_tmem, uint64_t adesc,
       : "memory");
 }
 }  // namespace tk
+
+namespace tk {
+// 2-SM TMA with cluster multicast: the box lands at the same smem offset in every CTA of
+// `mask`; transaction bytes are credited to the barrier at `bar_local`'s offset in the
+// even (leader) CTA of each destination's pair (peer bit cleared, as the PTX 2-SM form needs).
+__device__ __forceinline__ void tma_load_2d_pair_mc(void* dst, const CUtensorMap* m, uint64_t* bar_local,
+                                                    uint16_t mask, int32_t c0, int32_t c1,
+                                                    uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes."
+      "multicast::cluster.L2::cache_hint [%0], [%1, {%4, %5}], [%2], %3, %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar_local) & 0xFEFFFFFFu), "h"(mask),
+      "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair_local(void* dst, const CUtensorMap* m, uint64_t* bar_local,
+                                                       int32_t c0, int32_t c1, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes."
+      "L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar_local) & 0xFEFFFFFFu), "r"(c0), "r"(c1),
+      "l"(policy)
+      : "memory");
+}
+}  // namespace tk

@@ -39,7 +39,7 @@ def _f32(x):
     return np.asarray(x).astype(np.float32)
 
 
-@pytest.fixture(params=["single", "pair"])
+@pytest.fixture(params=["single", "pair", "quad"])
 def tc_kernel(request, monkeypatch):
     """Pin the single-CTA (128x256) or CTA-pair (256x256) tcgen05 kernel."""
     monkeypatch.setenv("TK_TC_KERNEL", request.param)
