@@ -36,7 +36,7 @@ from .operators import ComplexOperator, DualOperator, FmaOperator, OperatorShape
 
 def matmul(config: KernelConfig, a, b, c, d, **kwargs) -> EventCounters:
     """Resolve, validate and execute a kernel configuration on the B200."""
-    return kernel.gemm_execute(kernel.resolve_config(config), a, b, c, d, **kwargs)
+    return kernel.gemm_execute(config, a, b, c, d, **kwargs)
 
 
 # ---- element types -------------------------------------------------------------------

@@ -507,11 +507,14 @@ int run_tc(const TkGemmPlan* p, const void* a, const void* b, const void* c, voi
       // sums over the other dimension for each index of dim `dim_count`
       const int64_t s_count = L.stride[dim_count][0], s_len = L.stride[1 - dim_count][0];
       if (s_count == 1) {
-        const int blocks = int((count + 255) / 256);
+        TK_CUDA(cudaMemsetAsync(out, 0, count * sizeof(float), s));
+        const int bx = int((count + 255) / 256);
+        const int by = int(std::max<int64_t>(1, std::min<int64_t>(len / 32, (8 * sm_count() + bx - 1) / bx)));
+        const dim3 grid(bx, by);
         if (L.scalar == TK_F16)
-          tk::strided_sum_unit_kernel<__half><<<blocks, 256, 0, s>>>(static_cast<const __half*>(x), out, count, len, s_len);
+          tk::strided_sum_unit_kernel<__half><<<grid, 256, 0, s>>>(static_cast<const __half*>(x), out, count, len, s_len);
         else
-          tk::strided_sum_unit_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x), out, count, len, s_len);
+          tk::strided_sum_unit_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x), out, count, len, s_len);
       } else {
         const int blocks = int((count * 32 + 255) / 256);
         if (L.scalar == TK_F16)

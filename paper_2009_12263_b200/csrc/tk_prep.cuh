@@ -58,15 +58,19 @@ __global__ void strided_sum_kernel(const H* __restrict__ x, float* __restrict__ 
   if (lane == 0) out[warp] = acc;
 }
 
-// out[i] = sum_t X[i + t*s_inner] for unit-stride outputs: one thread per output (coalesced).
+// out[i] += sum_{t in slice} X[i + t*s_inner] for unit-stride outputs: threads along i
+// (coalesced), blockIdx.y splits t so the grid covers the GPU; out must be zeroed first.
 template <typename H>
 __global__ void strided_sum_unit_kernel(const H* __restrict__ x, float* __restrict__ out,
                                         int64_t count, int64_t len, int64_t s_inner) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= count) return;
+  const int64_t per = (len + gridDim.y - 1) / gridDim.y;
+  const int64_t t0 = int64_t(blockIdx.y) * per, t1 = min(len, t0 + per);
   float acc = 0.f;
-  for (int64_t t = 0; t < len; ++t) acc += h2f(x[i + t * s_inner]);
-  out[i] = acc;
+#pragma unroll 8
+  for (int64_t t = t0; t < t1; ++t) acc += h2f(x[i + t * s_inner]);
+  atomicAdd(out + i, acc);
 }
 
 }  // namespace tk
