@@ -29,16 +29,27 @@ def rnd(n, dt):
     return torch.randn(n, generator=g, device=dev).to(dt)
 
 
+from bench import ClockSampler  # noqa: E402
+
+_clock = {}
+
+
 def timeit(fn, reps=10, warm=3):
+    import time
+
+    torch.cuda.synchronize()
+    time.sleep(float(os.environ.get("COOLDOWN", "1.0")))  # let the power/clock state settle
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    for _ in range(reps):
-        fn()
-    e.record()
-    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as cs:
+        s.record()
+        for _ in range(reps):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+    _clock.update(cs.summary())
     return s.elapsed_time(e) / reps * 1e-3
 
 
@@ -48,10 +59,11 @@ results = []
 def report(name, sec, work, unit, lane, extra=None):
     val = work / sec / (1e12 if unit == "TFLOPS" else 1e9)
     row = {"case": name, "ms": sec * 1e3, "value": val, "unit": unit, "lane": lane,
-           "launches": tk.last_run()["launches"], **(extra or {})}
+           "launches": tk.last_run()["launches"], "sm_mhz": _clock.get("sm_mhz"),
+           "reasons": _clock.get("reasons"), **(extra or {})}
     results.append(row)
     print(f"{name:48s} {sec * 1e3:9.3f} ms  {val:9.1f} {unit:6s} lane={lane} "
-          f"launches={row['launches']}", flush=True)
+          f"launches={row['launches']} sm={row['sm_mhz']} {row['reasons']}", flush=True)
 
 
 def run(cfg, a, b, c, d):
