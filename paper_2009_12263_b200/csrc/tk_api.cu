@@ -247,14 +247,18 @@ int make_map_2d(CUtensorMap* map, const void* base, int scalar, uint64_t inner, 
                 uint64_t pitch_elems, uint32_t box_inner, uint32_t box_outer) {
   auto enc = get_encode();
   if (!enc) return fail(TK_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const bool f32 = scalar == TK_F32;
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {pitch_elems * 2};
+  cuuint64_t strides[1] = {pitch_elems * (f32 ? 4 : 2)};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, scalar == TK_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
-                   2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const CUtensorMapDataType dt = f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                     : scalar == TK_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                        : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  CUresult r = enc(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   f32 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(TK_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
   return TK_OK;
 }
@@ -296,16 +300,16 @@ int sm_count() {
   return n;
 }
 
-template <int OP, bool DENSE>
+template <int OP, bool DENSE, bool CSTREAM = false>
 int launch_tc_variant(const tk::TcParams& prm, cudaStream_t s) {
-  using S = tk::TcSmem<OP>;
+  using S = tk::TcSmem<OP, CSTREAM>;
   static bool attr = false;
   if (!attr) {
-    TK_CUDA(cudaFuncSetAttribute(tk::tc_gemm_kernel<OP, DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL));
+    TK_CUDA(cudaFuncSetAttribute(tk::tc_gemm_kernel<OP, DENSE, CSTREAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL));
     attr = true;
   }
   const int grid = std::min(prm.num_tiles, sm_count());
-  tk::tc_gemm_kernel<OP, DENSE><<<grid, tk::TC_THREADS, S::TOTAL, s>>>(prm);
+  tk::tc_gemm_kernel<OP, DENSE, CSTREAM><<<grid, tk::TC_THREADS, S::TOTAL, s>>>(prm);
   TK_CUDA(cudaGetLastError());
   ++g_launches;
   return TK_OK;
@@ -387,6 +391,7 @@ int tc_kernel_override() {
   if (!e) return 0;
   if (!strcmp(e, "pair")) return 2;
   if (!strcmp(e, "quad")) return 4;
+  if (!strcmp(e, "stream")) return 3;
   if (!strcmp(e, "single")) return 1;
   return 0;
 }
@@ -568,10 +573,20 @@ int run_tc(const TkGemmPlan* p, const void* a, const void* b, const void* c, voi
                decode_affine(p->t_c, pair, prm.c_mul, prm.c_add, prm.c_relu) &&
                decode_affine(p->t_r2s, pair, prm.r_mul, prm.r_add, prm.r_relu) &&
                decode_affine(p->t_s2g, pair, prm.s_mul, prm.s_add, prm.s_relu);
+  // HBM-bound shapes (diagonal A, K <= 4 block-K steps): C streamed through TMA by a loader warp
+  const int ov = tc_kernel_override();
+  if (op == TK_OP_REAL && dense && (ov == 3 || (ov == 0 && (prm.diag_a || prm.kb_total <= 4)))) {
+    const bool cs = prm.c_zero || ((prm.ldc * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(c) & 15) == 0);
+    if (cs) {
+      tk::TcParams ps = prm;
+      int rc;
+      if (!prm.c_zero && (rc = make_map_2d(&ps.tcmap, c, TK_F32, p->m, p->n, prm.ldc, 32, 32))) return rc;
+      return launch_tc_variant<tk::OP_REAL, true, true>(ps, s);
+    }
+  }
   if (op == TK_OP_REAL && !prm.diag_a) {
     // CTA pair (256x256 tiles) once there are enough pair tiles to cover the SMs
     const int64_t pair_tiles = ((p->m + 255) / 256) * ((p->n + tk::TC2_BN - 1) / tk::TC2_BN);
-    const int ov = tc_kernel_override();
     if (ov == 4) {
       tk::TcParams pp = prm;
       pp.num_mb = int((p->m + 511) / 512);
@@ -584,7 +599,7 @@ int run_tc(const TkGemmPlan* p, const void* a, const void* b, const void* c, voi
       if (mn && (rc = make_map_2d(&pp.tb[0], b_plane0, p->b.scalar, p->k, p->n, pitch, 64, 64))) return rc;
       return dense ? launch_tc_quad<true>(pp, s) : launch_tc_quad<false>(pp, s);
     }
-    if (ov == 2 || (ov == 0 && pair_tiles >= sm_count() / 2)) {
+    if (ov == 2 || (ov == 0 && pair_tiles >= sm_count() / 2 && prm.kb_total > 4)) {
       tk::TcParams pp = prm;
       pp.num_mb = int((p->m + 255) / 256);
       pp.num_nb = int((p->n + tk::TC2_BN - 1) / tk::TC2_BN);

@@ -42,19 +42,29 @@ struct TcCfg<OP_DUAL> {
   static constexpr int PLANES = 2, BN = 128, STAGES = 3, ACC_COLS = 256, TMEM_COLS = 512;
 };
 
-template <int OP>
+// C-streaming variant (HBM-bound shapes: diagonal A, K <= 256): 2 mainloop stages and a
+// per-epilogue-warp ring of TMA-loaded C boxes (32 rows x 32 columns fp32).
+constexpr int TC_CSLOTS = 3;
+constexpr int TC_CBOX_BYTES = 32 * 32 * 4;
+
+template <int OP, bool CSTREAM = false>
 struct TcSmem {
   using C = TcCfg<OP>;
+  static constexpr int STAGES = CSTREAM ? 2 : C::STAGES;
   static constexpr int B_TILE_BYTES = C::BN * TC_BK * 2;
   static constexpr int STAGE_BYTES = C::PLANES * (TC_A_TILE_BYTES + B_TILE_BYTES);
-  static constexpr int BAR_OFFSET = C::STAGES * STAGE_BYTES;
-  static constexpr int BAR_BYTES = (2 * C::STAGES + 4) * 8 + 16;
+  static constexpr int CRING_OFFSET = STAGES * STAGE_BYTES;
+  static constexpr int CRING_BYTES = CSTREAM ? TC_EPI_WARPS * TC_CSLOTS * TC_CBOX_BYTES : 0;
+  static constexpr int BAR_OFFSET = CRING_OFFSET + CRING_BYTES;
+  static constexpr int NCBAR = CSTREAM ? TC_EPI_WARPS * TC_CSLOTS : 0;
+  static constexpr int BAR_BYTES = (2 * STAGES + 4 + 2 * NCBAR) * 8 + 16;
   static constexpr int TOTAL = BAR_OFFSET + BAR_BYTES + 1024;  // +1024 for manual alignment
 };
 
 struct TcParams {
   CUtensorMap ta[2];
   CUtensorMap tb[2];
+  CUtensorMap tcmap;  // C as {M, N} fp32 boxes of 32x32 (C-streaming epilogue)
   int32_t m, n, k;
   int32_t a_mn, b_mn, ab_fmt;
   int32_t num_mb, num_nb, num_tiles, kb_total;
@@ -233,6 +243,58 @@ __device__ __forceinline__ void epilogue_dense(const TcParams& p, uint64_t* tful
   }
 }
 
+
+// Dense column-major epilogue reading C from the TMA ring filled by the C-loader warp.
+template <int COLS, int BN>
+__device__ __forceinline__ void epilogue_stream(const TcParams& p, uint64_t* tfull, uint32_t aphase,
+                                                uint32_t tbase, int i, int jbase, int lane,
+                                                const float* ring, uint64_t* cfull, uint64_t* cempty,
+                                                uint32_t& cq) {
+  const bool row_ok = i < p.m;
+  const bool has_c = !p.c_zero;
+  float* dp = reinterpret_cast<float*>(p.d_ptr) + (row_ok ? i : 0);
+  const float rterm = p.affine && row_ok ? (p.aff_r * (p.rowsum_a ? p.rowsum_a[i] : 0.f) + p.aff_k) : 0.f;
+  const float bias_m = (p.bias_axis == 2 && row_ok) ? p.bias[i] : 0.f;
+  mbar_wait(tfull, aphase);
+  tc_fence_after();
+#pragma unroll 1
+  for (int ch = 0; ch < COLS / 32; ++ch) {
+    const int j0 = jbase + ch * 32;
+    uint32_t r[32];
+    tmem_ld_32x32b_x32(tbase + uint32_t(j0 - jbase + (jbase % BN)), r);
+    const int jl = j0 + lane;
+    const float bcol = (p.bias_axis == 1 && jl < p.n) ? p.bias[jl] : 0.f;
+    const float qcol = (p.affine && p.colsum_b && jl < p.n) ? p.aff_q * p.colsum_b[jl] : 0.f;
+    float cv[32];
+    if (has_c) {
+      const uint32_t slot = cq % TC_CSLOTS;
+      mbar_wait(&cfull[slot], (cq / TC_CSLOTS) & 1);
+      const float* box = ring + slot * (TC_CBOX_BYTES / 4);
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) cv[jj] = box[jj * 32 + lane];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&cempty[slot]);
+      ++cq;
+    }
+    tmem_ld_wait();
+    float out[32];
+#pragma unroll
+    for (int jj = 0; jj < 32; ++jj) {
+      float v = __uint_as_float(r[jj]);
+      if (p.affine) v = p.aff_s * v + (rterm + __shfl_sync(0xffffffffu, qcol, jj));
+      if (has_c) v = relu_if(cv[jj] * p.c_mul[0] + p.c_add[0], p.c_relu) + v;
+      v = relu_if(v * p.r_mul[0] + p.r_add[0], p.r_relu);
+      v = v + (p.bias_axis == 1 ? __shfl_sync(0xffffffffu, bcol, jj) : bias_m);
+      out[jj] = relu_if(v * p.s_mul[0] + p.s_add[0], p.s_relu);
+    }
+    if (row_ok) {
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj)
+        if (j0 + jj < p.n) __stcs(dp + int64_t(j0 + jj) * p.ldd, out[jj]);
+    }
+  }
+}
+
 // Any digit-mapped C/D layout and any transform program (the rare path).
 template <int OP, int COLS, int BN>
 __device__ __noinline__ void epilogue_generic(const TcParams& p, uint64_t* tfull, uint32_t aphase,
@@ -281,12 +343,12 @@ __device__ __noinline__ void epilogue_generic(const TcParams& p, uint64_t* tfull
   }
 }
 
-template <int OP, bool DENSE_EPI>
+template <int OP, bool DENSE_EPI, bool CSTREAM = false>
 __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(const __grid_constant__ TcParams p) {
   using C = TcCfg<OP>;
-  using S = TcSmem<OP>;
+  using S = TcSmem<OP, CSTREAM>;
   constexpr int BN = C::BN;
-  constexpr int STAGES = C::STAGES;
+  constexpr int STAGES = S::STAGES;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -295,12 +357,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(const __grid_con
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* cfull = tempty + 2;            // [epilogue warp][slot] (C-streaming only)
+  uint64_t* cempty = cfull + S::NCBAR;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + S::NCBAR);
+  const float* cring = reinterpret_cast<const float*>(smem + S::CRING_OFFSET);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
+    if (CSTREAM && !p.c_zero) tma_prefetch(&p.tcmap);
     if (!p.diag_a) {
       tma_prefetch(&p.ta[0]);
       if (C::PLANES > 1) tma_prefetch(&p.ta[1]);
@@ -316,6 +382,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(const __grid_con
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], TC_EPI_WARPS);
+    }
+    for (int s = 0; s < S::NCBAR; ++s) {
+      mbar_init(&cfull[s], 1);
+      mbar_init(&cempty[s], 1);
     }
     fence_mbar_init();
   }
@@ -442,9 +512,32 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(const __grid_con
         tc_commit(&tfull[as]);       // accumulator ready for the epilogue
       }
     }
+  } else if (warp == 3) {
+    // ------------------------------------------------------------ C loader (C-streaming)
+    if (CSTREAM && !p.c_zero && lane == 0) {
+      constexpr int CHUNKS = BN / 2 / 32;
+      uint32_t q = 0;
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        int mb, nb;
+        tile_coords(p, t, mb, nb);
+        for (int ch = 0; ch < CHUNKS; ++ch, ++q) {
+          const uint32_t slot = q % TC_CSLOTS, ph = (q / TC_CSLOTS) & 1;
+          for (int w = 0; w < TC_EPI_WARPS; ++w) {
+            const int bi = w * TC_CSLOTS + int(slot);
+            mbar_wait(&cempty[bi], ph ^ 1);
+            mbar_arrive_expect_tx(&cfull[bi], TC_CBOX_BYTES);
+            const int row0 = mb * TC_BM + (w & 3) * 32;
+            const int col0 = nb * BN + (w >> 2) * (BN / 2) + ch * 32;
+            tma_load_2d(smem + S::CRING_OFFSET + bi * TC_CBOX_BYTES, &p.tcmap, &cfull[bi], row0,
+                        col0, policy_evict_normal());
+          }
+        }
+      }
+    }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
     const int ew = warp - 4;
+    uint32_t cq = 0;
     const int quarter = warp & 3;          // TMEM lane quarter this warp may access
     const int half = ew >> 2;              // which half of the tile's columns
     const int row_local = quarter * 32 + lane;
@@ -458,7 +551,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(const __grid_con
       const int i = mb * TC_BM + row_local;
       const uint32_t tbase = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(as * C::ACC_COLS);
       const int jbase = nb * BN + half * COLS_PER_WARP;
-      if (DENSE_EPI)
+      if (CSTREAM)
+        epilogue_stream<COLS_PER_WARP, BN>(p, tfull + as, aphase, tbase, i, jbase, lane,
+                                           cring + ew * TC_CSLOTS * (TC_CBOX_BYTES / 4),
+                                           cfull + ew * TC_CSLOTS, cempty + ew * TC_CSLOTS, cq);
+      else if (DENSE_EPI)
         epilogue_dense<OP, COLS_PER_WARP, BN>(p, tfull + as, aphase, tbase, i, jbase, lane);
       else
         epilogue_generic<OP, COLS_PER_WARP, BN>(p, tfull + as, aphase, tbase, i, jbase);

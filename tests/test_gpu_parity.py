@@ -39,7 +39,7 @@ def _f32(x):
     return np.asarray(x).astype(np.float32)
 
 
-@pytest.fixture(params=["single", "pair", "quad"])
+@pytest.fixture(params=["single", "pair", "quad", "stream"])
 def tc_kernel(request, monkeypatch):
     """Pin the single-CTA (128x256) or CTA-pair (256x256) tcgen05 kernel."""
     monkeypatch.setenv("TK_TC_KERNEL", request.param)
@@ -69,7 +69,8 @@ def test_dense_integer_exact(cuda, dtype, trans, tc_kernel):
 
 @pytest.mark.parametrize("dtype", [np.float16, "bf16"])
 @pytest.mark.parametrize("mnk", [(128, 256, 64), (1024, 1024, 1024), (384, 768, 2048),
-                                 (200, 136, 72), (8, 16, 8), (1000, 520, 4104)])
+                                 (200, 136, 72), (8, 16, 8), (1000, 520, 4104),
+                                 (1024, 768, 128), (520, 1000, 256)])
 def test_dense_random_within_tolerance(cuda, dtype, mnk, tc_kernel):
     dtype = tk.BFLOAT16 if dtype == "bf16" else np.dtype(dtype)
     m, n, k = mnk
@@ -164,8 +165,11 @@ def _unpack_pair(t, shape, split):
     return p0.reshape(shape, order="F"), p1.reshape(shape, order="F")
 
 
+@pytest.mark.parametrize("kernel", ["auto", "single"])
 @pytest.mark.parametrize("n", [256, 1024, 640])
-def test_diagonal_variant(cuda, n):
+def test_diagonal_variant(cuda, n, kernel, monkeypatch):
+    if kernel != "auto":
+        monkeypatch.setenv("TK_TC_KERNEL", kernel)
     rng = np.random.default_rng(4)
     diag = rng.standard_normal(n).astype(np.float16)
     b = rng.standard_normal((n, n)).astype(np.float16)
