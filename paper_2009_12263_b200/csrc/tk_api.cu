@@ -581,6 +581,9 @@ int run_tc(const TkGemmPlan* p, const void* a, const void* b, const void* c, voi
       tk::TcParams ps = prm;
       int rc;
       if (!prm.c_zero && (rc = make_map_2d(&ps.tcmap, c, TK_F32, p->m, p->n, prm.ldc, 32, 32))) return rc;
+      ps.d_tma = (prm.ldd * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(d) & 15) == 0;
+      if (const char* e = getenv("TK_D_TMA")) ps.d_tma = ps.d_tma && atoi(e);
+      if (ps.d_tma && (rc = make_map_2d(&ps.tdmap, d, TK_F32, p->m, p->n, prm.ldd, 32, 32))) return rc;
       return launch_tc_variant<tk::OP_REAL, true, true>(ps, s);
     }
   }

@@ -65,6 +65,7 @@ struct TcParams {
   CUtensorMap ta[2];
   CUtensorMap tb[2];
   CUtensorMap tcmap;  // C as {M, N} fp32 boxes of 32x32 (C-streaming epilogue)
+  CUtensorMap tdmap;  // D likewise (TMA bulk stores from the same ring slot)
   int32_t m, n, k;
   int32_t a_mn, b_mn, ab_fmt;
   int32_t num_mb, num_nb, num_tiles, kb_total;
@@ -88,6 +89,7 @@ struct TcParams {
   float c_mul[2], c_add[2], r_mul[2], r_add[2], s_mul[2], s_add[2];
   int32_t c_relu, r_relu, s_relu, pad1;
   int32_t dbg_skip_epi, pol_ab;  // tuning/diagnostic knobs (TK_DBG_SKIP_EPI, TK_POLICY_AB)
+  int32_t d_tma, pad2;           // C-streaming epilogue: D through TMA bulk stores
 };
 
 __device__ __forceinline__ void tile_coords(const TcParams& p, int t, int& mb, int& nb) {
@@ -244,12 +246,14 @@ __device__ __forceinline__ void epilogue_dense(const TcParams& p, uint64_t* tful
 }
 
 
-// Dense column-major epilogue reading C from the TMA ring filled by the C-loader warp.
+// Dense column-major epilogue for HBM-bound shapes: C arrives in a per-warp ring of TMA boxes
+// filled by the loader warp; D is written back into the same slot and stored with one TMA
+// bulk store per 32x32 box (the slot is handed back to the loader once that store has read it).
 template <int COLS, int BN>
 __device__ __forceinline__ void epilogue_stream(const TcParams& p, uint64_t* tfull, uint32_t aphase,
                                                 uint32_t tbase, int i, int jbase, int lane,
-                                                const float* ring, uint64_t* cfull, uint64_t* cempty,
-                                                uint32_t& cq) {
+                                                float* ring, uint64_t* cfull, uint64_t* cempty,
+                                                uint32_t& cq, int row0) {
   const bool row_ok = i < p.m;
   const bool has_c = !p.c_zero;
   float* dp = reinterpret_cast<float*>(p.d_ptr) + (row_ok ? i : 0);
@@ -265,16 +269,16 @@ __device__ __forceinline__ void epilogue_stream(const TcParams& p, uint64_t* tfu
     const int jl = j0 + lane;
     const float bcol = (p.bias_axis == 1 && jl < p.n) ? p.bias[jl] : 0.f;
     const float qcol = (p.affine && p.colsum_b && jl < p.n) ? p.aff_q * p.colsum_b[jl] : 0.f;
+    const uint32_t slot = cq % TC_CSLOTS;
+    float* box = ring + slot * (TC_CBOX_BYTES / 4);
     float cv[32];
     if (has_c) {
-      const uint32_t slot = cq % TC_CSLOTS;
       mbar_wait(&cfull[slot], (cq / TC_CSLOTS) & 1);
-      const float* box = ring + slot * (TC_CBOX_BYTES / 4);
 #pragma unroll
       for (int jj = 0; jj < 32; ++jj) cv[jj] = box[jj * 32 + lane];
+    } else if (p.d_tma) {
+      if (lane == 0) bulk_wait_read<TC_CSLOTS - 1>();  // slot's previous store has read it
       __syncwarp();
-      if (lane == 0) mbar_arrive(&cempty[slot]);
-      ++cq;
     }
     tmem_ld_wait();
     float out[32];
@@ -287,11 +291,31 @@ __device__ __forceinline__ void epilogue_stream(const TcParams& p, uint64_t* tfu
       v = v + (p.bias_axis == 1 ? __shfl_sync(0xffffffffu, bcol, jj) : bias_m);
       out[jj] = relu_if(v * p.s_mul[0] + p.s_add[0], p.s_relu);
     }
-    if (row_ok) {
+    if (p.d_tma) {
 #pragma unroll
-      for (int jj = 0; jj < 32; ++jj)
-        if (j0 + jj < p.n) __stcs(dp + int64_t(j0 + jj) * p.ldd, out[jj]);
+      for (int jj = 0; jj < 32; ++jj) box[jj * 32 + lane] = out[jj];
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(&p.tdmap, box, row0, j0);   // the map clips rows >= M / columns >= N
+        bulk_commit();
+        if (has_c) {  // hand the previous chunk's slot back once its store has read it
+          bulk_wait_read<1>();
+          if (cq > 0) mbar_arrive(&cempty[(cq - 1) % TC_CSLOTS]);
+        }
+      }
+    } else {
+      if (has_c) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&cempty[slot]);
+      }
+      if (row_ok) {
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj)
+          if (j0 + jj < p.n) __stcs(dp + int64_t(j0 + jj) * p.ldd, out[jj]);
+      }
     }
+    ++cq;
   }
 }
 
@@ -360,7 +384,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(const __grid_con
   uint64_t* cfull = tempty + 2;            // [epilogue warp][slot] (C-streaming only)
   uint64_t* cempty = cfull + S::NCBAR;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + S::NCBAR);
-  const float* cring = reinterpret_cast<const float*>(smem + S::CRING_OFFSET);
+  float* cring = reinterpret_cast<float*>(smem + S::CRING_OFFSET);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -554,7 +578,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(const __grid_con
       if (CSTREAM)
         epilogue_stream<COLS_PER_WARP, BN>(p, tfull + as, aphase, tbase, i, jbase, lane,
                                            cring + ew * TC_CSLOTS * (TC_CBOX_BYTES / 4),
-                                           cfull + ew * TC_CSLOTS, cempty + ew * TC_CSLOTS, cq);
+                                           cfull + ew * TC_CSLOTS, cempty + ew * TC_CSLOTS, cq,
+                                           mb * TC_BM + quarter * 32);
       else if (DENSE_EPI)
         epilogue_dense<OP, COLS_PER_WARP, BN>(p, tfull + as, aphase, tbase, i, jbase, lane);
       else
@@ -565,6 +590,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(const __grid_con
     }
   }
 
+  if (CSTREAM && warp >= 4 && lane == 0) bulk_wait<0>();  // D stores complete before exit
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
