@@ -167,7 +167,44 @@ bool tma_operand(const TkLayout& L, int& mn_major_dim0, int64_t& pitch) {
   return true;
 }
 
+// GETT-as-GEMM (tensor contraction, reference api.py:259-290): A's M index has two digits
+// (e0, s0), (e1, s1) and D's M digits are the same extents with the order swapped into a
+// dense run (t1 == 1, t0 == e1).  Rewrite to a plain column-major GEMM over m' = m1 + e1*m0:
+// A is permuted once into a dense M' x K workspace (swap_digits_kernel), D (and C) become
+// column-major with the N stride as leading dimension.
+bool permuted_plan(const TkGemmPlan* p, TkGemmPlan* out) {
+  const TkLayout& A = p->a;
+  const TkLayout& D = p->d;
+  if (A.kind != TK_LAYOUT_STRIDED || A.pair || A.ndigits[0] != 2 || A.ndigits[1] != 1) return false;
+  if (D.kind != TK_LAYOUT_STRIDED || D.pair || D.ndigits[0] != 2 || D.ndigits[1] != 1) return false;
+  const int64_t e0 = A.ext[0][0], e1 = A.ext[0][1];
+  if (D.ext[0][0] != e0 || D.ext[0][1] != e1 || D.stride[0][1] != 1 || D.stride[0][0] != e1) return false;
+  if (p->c.kind != TK_LAYOUT_ZERO &&
+      (p->c.kind != TK_LAYOUT_STRIDED || p->c.pair || p->c.ndigits[0] != 2 || p->c.ndigits[1] != 1 ||
+       p->c.ext[0][0] != e0 || p->c.ext[0][1] != e1 || p->c.stride[0][1] != 1 || p->c.stride[0][0] != e1))
+    return false;
+  if (p->bias_axis == 2 || p->predicate != TK_PRED_ALWAYS || !is_half(A.scalar) || p->k > 65535)
+    return false;
+  if (out) {
+    *out = *p;
+    auto dense_cm = [](TkLayout& L, int64_t rows, int64_t cols, int64_t ld) {
+      L.ndigits[0] = L.ndigits[1] = 1;
+      L.ext[0][0] = rows; L.stride[0][0] = 1;
+      L.ext[1][0] = cols; L.stride[1][0] = ld;
+      L.ext[0][1] = L.ext[0][2] = L.ext[1][1] = L.ext[1][2] = 0;
+      L.stride[0][1] = L.stride[0][2] = L.stride[1][1] = L.stride[1][2] = 0;
+    };
+    dense_cm(out->a, p->m, p->k, p->m);
+    out->a.size = p->m * p->k;
+    dense_cm(out->d, p->m, p->n, D.stride[1][0]);
+    if (p->c.kind == TK_LAYOUT_STRIDED) dense_cm(out->c, p->m, p->n, p->c.stride[1][0]);
+  }
+  return true;
+}
+
 bool tc_lane_ok(const TkGemmPlan* p, std::string& why) {
+  TkGemmPlan rewritten;
+  if (permuted_plan(p, &rewritten)) return tc_lane_ok(&rewritten, why);
   auto no = [&](const char* w) { why = w; return false; };
   if (p->compute != TK_F32) return no("tcgen05 lane accumulates in f32 only");
   if (!is_half(p->a.scalar) || p->b.scalar != p->a.scalar) return no("A/B must be f16 or bf16");
@@ -205,14 +242,21 @@ int choose_lane(const TkGemmPlan* p, std::string* why_out = nullptr) {
 
 // ------------------------------------------------------------------ workspace plan
 struct Workspace {
-  int64_t a_planes = -1, b_planes = -1, rowsum = -1, colsum = -1, total = 0;
+  int64_t a_planes = -1, b_planes = -1, rowsum = -1, colsum = -1, a_perm = -1, total = 0;
 };
 
 int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
 
-Workspace plan_workspace(const TkGemmPlan* p, int lane) {
+Workspace plan_workspace(const TkGemmPlan* p0, int lane) {
   Workspace w;
   if (lane != TK_LANE_TCGEN05) return w;
+  TkGemmPlan rewritten;
+  const TkGemmPlan* p = p0;
+  if (permuted_plan(p0, &rewritten)) {
+    w.a_perm = w.total;
+    w.total += align256(p0->m * p0->k * 2);
+    p = &rewritten;
+  }
   if (p->a.kind == TK_LAYOUT_STRIDED && p->a.pair == TK_PAIR_INTERLEAVED) {
     w.a_planes = w.total;
     w.total += align256(p->m * p->k * 2 * 2);
@@ -427,8 +471,22 @@ bool colmajor_dense(const TkLayout& L, int64_t& ld) {
   return true;
 }
 
-int run_tc(const TkGemmPlan* p, const void* a, const void* b, const void* c, void* d, const void* bias,
+int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, void* d, const void* bias,
            uint8_t* ws, const Workspace& w, cudaStream_t s) {
+  TkGemmPlan rewritten;
+  const TkGemmPlan* p = p0;
+  if (w.a_perm >= 0 && permuted_plan(p0, &rewritten)) {
+    const TkLayout& A = p0->a;
+    uint16_t* at = reinterpret_cast<uint16_t*>(ws + w.a_perm);
+    const dim3 grid(unsigned((A.ext[0][0] + 63) / 64), unsigned((A.ext[0][1] + 63) / 64), unsigned(p0->k));
+    tk::swap_digits_kernel<<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(a), at, A.ext[0][0],
+                                                A.stride[0][0], A.ext[0][1], A.stride[0][1], p0->k,
+                                                A.stride[1][0]);
+    TK_CUDA(cudaGetLastError());
+    ++g_launches;
+    a = at;
+    p = &rewritten;
+  }
   tk::TcParams prm;
   memset(&prm, 0, sizeof(prm));
   const int op = p->op;

@@ -253,3 +253,19 @@ def test_simt_complex_dual_bitwise(cuda):
     tk.matmul(cfg, a.ravel(order="F").view(np.float64), b.ravel(order="F").view(np.float64),
               c.ravel(order="F").view(np.float64), d.view(np.float64))
     assert np.array_equal(d.reshape((m, n), order="F"), O.gemm_pair(a, b, c, dual=True))
+
+
+@pytest.mark.parametrize("shape", [(64, 32, 2048, 256), (8, 4, 256, 64), (16, 128, 512, 1024)])
+def test_tensor_contraction_tcgen05(cuda, shape):
+    """D[a,b,c] = sum_d A[b,d,a] B[d,c] on the tensor cores (A's M digits permuted once)."""
+    na, nb, nc, nd = shape
+    rng = np.random.default_rng(9)
+    a = rng.standard_normal((nb, nd, na)).astype(np.float16)
+    b = rng.standard_normal((nd, nc)).astype(np.float16)
+    ta = torch.from_numpy(a).cuda()
+    tb = torch.from_numpy(b).cuda()
+    d, counters = tk.contract(ta, tb)
+    assert tk.last_run()["lane"] == "tcgen05"
+    want = O.tc_reference(a.astype(np.float32), b.astype(np.float32))
+    assert O.rel_err(d.cpu().numpy(), want) <= O.tolerance(nd)
+    assert counters.global_stores == na * nb * nc

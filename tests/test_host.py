@@ -430,7 +430,7 @@ def test_lane_selection_variants():
         lanes[name] = kernel.plan_lane(kernel.lower(kernel.resolve_config(cfg))[0])
     assert lanes == {"complex16": "tcgen05", "complex16_split": "tcgen05", "dual16": "tcgen05",
                      "diag16": "tcgen05", "fused16": "tcgen05", "complex64": "simt",
-                     "tc16": "simt"}
+                     "tc16": "tcgen05"}
     # a relu on the A stream is not affine: the exact lane runs it
     cfg = dataclasses.replace(tk.build_dense_config(256, 256, 64, np.float16),
                               transform_g2s_a=components.relu)
