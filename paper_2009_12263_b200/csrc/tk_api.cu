@@ -13,6 +13,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/tk_sm100.h"
 #include "tk_prep.cuh"
@@ -939,6 +940,98 @@ extern "C" int tk_gemm_ex_raw_async(int tag, int ta, int tb, long long m, long l
   return rc;
 }
 
+namespace {
+
+struct ExStreams {
+  cudaStream_t in = nullptr, comp = nullptr, out = nullptr;
+  bool ok = false;
+};
+
+ExStreams& ex_streams() {
+  static ExStreams st;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    st.ok = cudaStreamCreateWithFlags(&st.in, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&st.comp, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&st.out, cudaStreamNonBlocking) == cudaSuccess;
+    // keep freed staging memory in the stream-ordered pool between calls
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
+  return st;
+}
+
+// Host-buffer gemm_ex: H2D of column slabs of B and C, the slab GEMMs and the D2H of finished
+// slabs run on three streams, so both PCIe directions and the tensor cores overlap.  Column
+// slabs of column-major B (not transposed) and C are contiguous sub-buffers.
+int ex_pipelined(int tag, int ta, long long m, long long n, long long k, double are, double aim,
+                 const void* a, const void* b, double bre, double bim, void* c, int64_t esz_ab,
+                 int64_t esz_c, int pairf) {
+  ExStreams& st = ex_streams();
+  if (!st.ok) return fail(TK_ERR_CUDA, "stream creation failed");
+  const int64_t sa = m * k * esz_ab * pairf, sb = k * n * esz_ab * pairf, sc = m * n * esz_c * pairf;
+  void *da = nullptr, *db = nullptr, *dc = nullptr;
+  TK_CUDA(cudaMallocAsync(&da, sa, st.in));
+  TK_CUDA(cudaMallocAsync(&db, sb, st.in));
+  TK_CUDA(cudaMallocAsync(&dc, sc, st.in));
+  TK_CUDA(cudaMemcpyAsync(da, a, sa, cudaMemcpyHostToDevice, st.in));
+  int slabs = int(std::max<long long>(1, std::min<long long>(8, n / 1024)));
+  const long long w = ((n / slabs + 255) / 256) * 256;
+  slabs = int((n + w - 1) / w);
+  int rc = TK_OK;
+  int launches = 0;
+  std::vector<cudaEvent_t> ev_in(slabs), ev_done(slabs);
+  for (int i = 0; i < slabs; ++i) {
+    cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_done[i], cudaEventDisableTiming);
+  }
+  for (int i = 0; i < slabs && rc == TK_OK; ++i) {
+    const long long j0 = i * w, cols = std::min<long long>(w, n - j0);
+    const int64_t ob = j0 * k * esz_ab * pairf, oc = j0 * m * esz_c * pairf;
+    const int64_t nb = cols * k * esz_ab * pairf, nc = cols * m * esz_c * pairf;
+    if (cudaMemcpyAsync(static_cast<char*>(db) + ob, static_cast<const char*>(b) + ob, nb,
+                        cudaMemcpyHostToDevice, st.in) != cudaSuccess ||
+        cudaMemcpyAsync(static_cast<char*>(dc) + oc, static_cast<char*>(c) + oc, nc,
+                        cudaMemcpyHostToDevice, st.in) != cudaSuccess) {
+      rc = fail(TK_ERR_CUDA, "host-to-device copy failed");
+      break;
+    }
+    cudaEventRecord(ev_in[i], st.in);
+    cudaStreamWaitEvent(st.comp, ev_in[i], 0);
+    rc = tk_gemm_ex_raw_async(tag, ta, 0, m, cols, k, are, aim, da, static_cast<char*>(db) + ob,
+                              bre, bim, static_cast<char*>(dc) + oc, st.comp);
+    launches += g_launches;
+    cudaEventRecord(ev_done[i], st.comp);
+    cudaStreamWaitEvent(st.out, ev_done[i], 0);
+    if (rc == TK_OK && cudaMemcpyAsync(static_cast<char*>(c) + oc, static_cast<char*>(dc) + oc, nc,
+                                       cudaMemcpyDeviceToHost, st.out) != cudaSuccess)
+      rc = fail(TK_ERR_CUDA, "device-to-host copy failed");
+  }
+  cudaStreamSynchronize(st.in);
+  cudaStreamSynchronize(st.comp);
+  cudaStreamSynchronize(st.out);
+  cudaFreeAsync(da, st.out);
+  cudaFreeAsync(db, st.out);
+  cudaFreeAsync(dc, st.out);
+  cudaStreamSynchronize(st.out);
+  for (int i = 0; i < slabs; ++i) {
+    cudaEventDestroy(ev_in[i]);
+    cudaEventDestroy(ev_done[i]);
+  }
+  g_launches = launches;
+  if (rc == TK_OK) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(TK_ERR_CUDA, "pipelined gemm_ex: %s", cudaGetErrorString(e));
+  }
+  return rc;
+}
+
+}  // namespace
+
 extern "C" int tk_gemm_ex_raw(int tag, int ta, int tb, long long m, long long n, long long k,
                               double are, double aim, void* a, void* b, double bre, double bim, void* c) {
   g_err.clear();
@@ -963,6 +1056,13 @@ extern "C" int tk_gemm_ex_raw(int tag, int ta, int tb, long long m, long long n,
     if (rc) return rc;
     TK_CUDA(cudaDeviceSynchronize());
     return TK_OK;
+  }
+  // large problems: overlap the host<->device traffic with the slab GEMMs
+  if (!tb && p.a.kind != TK_LAYOUT_ZERO && m * n * k >= (1ll << 30)) {
+    TagInfo ti;
+    tag_info(tag, ti);
+    return ex_pipelined(tag, ta, m, n, k, are, aim, a, b, bre, bim, c, scalar_bytes(ti.ab_scalar),
+                        scalar_bytes(ti.c_scalar), ti.op == TK_OP_REAL ? 1 : 2);
   }
   void *da = nullptr, *db = nullptr, *dc = nullptr;
   auto cleanup = [&] {

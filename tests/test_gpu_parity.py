@@ -269,3 +269,19 @@ def test_tensor_contraction_tcgen05(cuda, shape):
     want = O.tc_reference(a.astype(np.float32), b.astype(np.float32))
     assert O.rel_err(d.cpu().numpy(), want) <= O.tolerance(nd)
     assert counters.global_stores == na * nb * nc
+
+
+@pytest.mark.parametrize("trans_a", [0, 1])
+def test_gemm_ex_raw_host_pipelined(cuda, trans_a):
+    """Host-buffer tk_gemm_ex_raw above 2^30 MACs takes the 3-stream slab pipeline."""
+    m, n, k = 512, 4096 + 256, 512
+    rng = np.random.default_rng(10)
+    a = np.asfortranarray(rng.standard_normal((k, m) if trans_a else (m, k)).astype(np.float16))
+    b = np.asfortranarray(rng.standard_normal((k, n)).astype(np.float16))
+    c = np.asfortranarray(rng.standard_normal((m, n)).astype(np.float32))
+    op_a = _f32(a).T if trans_a else _f32(a)
+    want = O.exact_gemm(op_a, _f32(b), c, alpha=1.25, beta=-0.5)
+    st = tk.gemm_ex_raw(tk.TAG_F16F32, trans_a, 0, m, n, k, 1.25, 0.0, a.ctypes.data,
+                        b.ctypes.data, -0.5, 0.0, c.ctypes.data)
+    assert st == 0, tk._lib.last_error()
+    assert O.rel_err(c, want) <= O.tolerance(k)
