@@ -241,8 +241,18 @@ def run_ours(args):
     burst, sustained, hbm, src = _peaks()
     kernel_ms = ms / launches_per_step
     achieved = flops_rank / (kernel_ms * 1e-3) / 1e12
+    traffic = args.traffic
+    if traffic is None:  # dram bytes per launch from the committed ncu --set full capture
+        try:
+            with open(os.path.join(ROOT, "profiles", "roofline_traffic.json")) as f:
+                traffic = json.load(f).get(f"{args.dtype}_{m}")
+        except (OSError, ValueError):
+            traffic = None
     roofline = {"bound": "tensor", "achieved": achieved, "peak": burst, "unit": "TFLOP/s",
-                "frac": achieved / burst, "traffic": args.traffic,
+                "frac": achieved / burst, "traffic": traffic,
+                "traffic_unit": "bytes/launch (dram read+write, ncu --set full)",
+                "algorithmic_flops_per_launch": flops_rank,
+                "algorithmic_bytes_per_launch": 2 * (m * k + k * n) + 8 * m * n,
                 "peak_source": f"{src} bf16 burst (MEASURED_PEAKS.json)",
                 "frac_of_sustained": achieved / sustained if sustained else None,
                 "frac_of_spec_2250": achieved / 2250.0}
