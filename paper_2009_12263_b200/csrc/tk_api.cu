@@ -308,6 +308,24 @@ int make_map_2d(CUtensorMap* map, const void* base, int scalar, uint64_t inner, 
   return TK_OK;
 }
 
+// MN-major operand as {64 (MN inner), K, MN/64}: one TMA box {64, 64, atoms} fills `atoms`
+// consecutive 128B-swizzled 64x64 atoms (8 KB apart) -- the same smem image as `atoms` 2-D boxes.
+int make_map_mn3d(CUtensorMap* map, const void* base, int scalar, uint64_t mn, uint64_t k,
+                  uint64_t pitch_elems, uint32_t atoms) {
+  auto enc = get_encode();
+  if (!enc) return fail(TK_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {64, k, (mn + 63) / 64};
+  cuuint64_t strides[2] = {pitch_elems * 2, 128};
+  cuuint32_t box[3] = {64, 64, atoms};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, scalar == TK_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                   3, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(TK_ERR_CUDA, "cuTensorMapEncodeTiled (3-D) failed (%d)", int(r));
+  return TK_OK;
+}
+
 tk::DigitMap to_map(const TkLayout& L) {
   tk::DigitMap m{};
   for (int d = 0; d < 2; ++d) {
@@ -671,9 +689,21 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
       int64_t pitch;
       int rc;
       tma_operand(p->a, mn, pitch);
+      pp.mn3d = 0;
+      const char* e3 = getenv("TK_MN3D");
+      const bool use3d = !e3 || atoi(e3);
+      // MN-major A (M % 64 == 0 so atoms never straddle the M edge): one 3-D box per stage
+      if (mn && use3d && p->m % 64 == 0) {
+        if ((rc = make_map_mn3d(&pp.ta[0], a_plane0, p->a.scalar, p->m, p->k, pitch, 2))) return rc;
+        pp.mn3d |= 1;
+      }
       if (!mn && (rc = make_map_2d(&pp.ta[0], a_plane0, p->a.scalar, p->k, p->m, pitch, 64, 128))) return rc;
       tma_operand(p->b, mn, pitch);
       if (mn && (rc = make_map_2d(&pp.tb[0], b_plane0, p->b.scalar, p->k, p->n, pitch, 64, 128))) return rc;
+      if (!mn && use3d && p->n % 64 == 0) {
+        if ((rc = make_map_mn3d(&pp.tb[0], b_plane0, p->b.scalar, p->n, p->k, pitch, 2))) return rc;
+        pp.mn3d |= 2;
+      }
       return dense ? launch_tc_pair<true>(pp, s) : launch_tc_pair<false>(pp, s);
     }
   }

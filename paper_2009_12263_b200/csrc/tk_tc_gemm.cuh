@@ -89,7 +89,7 @@ struct TcParams {
   float c_mul[2], c_add[2], r_mul[2], r_add[2], s_mul[2], s_add[2];
   int32_t c_relu, r_relu, s_relu, pad1;
   int32_t dbg_skip_epi, pol_ab;  // tuning/diagnostic knobs (TK_DBG_SKIP_EPI, TK_POLICY_AB)
-  int32_t d_tma, pad2;           // C-streaming epilogue: D through TMA bulk stores
+  int32_t d_tma, mn3d;           // C-streaming epilogue: D via TMA; MN-major operands via 3-D maps (bit0 A, bit1 B)
 };
 
 __device__ __forceinline__ void tile_coords(const TcParams& p, int t, int& mb, int& nb) {

@@ -83,13 +83,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * TC2_STAGE_BYTES);
           const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
-          if (p.a_mn) {
+          if (p.a_mn && (p.mn3d & 1)) {
+            tma_load_3d_pair(a_tile(stage), &p.ta[0], fb, 0, k0, m0 >> 6, pol);
+          } else if (p.a_mn) {
             tma_load_2d_pair(a_tile(stage), &p.ta[0], fb, m0, k0, pol);
             tma_load_2d_pair(a_tile(stage) + 8192, &p.ta[0], fb, m0 + 64, k0, pol);
           } else {
             tma_load_2d_pair(a_tile(stage), &p.ta[0], fb, k0, m0, pol);
           }
-          if (p.b_mn) {
+          if (p.b_mn && (p.mn3d & 2)) {
+            tma_load_3d_pair(b_tile(stage), &p.tb[0], fb, 0, k0, n0 >> 6, pol);
+          } else if (p.b_mn) {
             tma_load_2d_pair(b_tile(stage), &p.tb[0], fb, n0, k0, pol);
             tma_load_2d_pair(b_tile(stage) + 8192, &p.tb[0], fb, n0 + 64, k0, pol);
           } else {
