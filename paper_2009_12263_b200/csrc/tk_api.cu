@@ -378,12 +378,13 @@ int launch_tc_variant(const tk::TcParams& prm, cudaStream_t s) {
   return TK_OK;
 }
 
-template <bool DENSE>
+template <bool DENSE, bool CSTREAM = false>
 int launch_tc_pair(const tk::TcParams& prm, cudaStream_t s) {
+  constexpr int SMEM = CSTREAM ? tk::TC2S_SMEM : tk::TC2_SMEM;
   static bool attr = false;
   if (!attr) {
-    TK_CUDA(cudaFuncSetAttribute(tk::tc_gemm_pair_kernel<DENSE>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, tk::TC2_SMEM));
+    TK_CUDA(cudaFuncSetAttribute(tk::tc_gemm_pair_kernel<DENSE, CSTREAM>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
     attr = true;
   }
   static int max_clusters = 0;
@@ -391,7 +392,7 @@ int launch_tc_pair(const tk::TcParams& prm, cudaStream_t s) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * (sm_count() / 2));
     cfg.blockDim = dim3(tk::TC_THREADS);
-    cfg.dynamicSmemBytes = tk::TC2_SMEM;
+    cfg.dynamicSmemBytes = SMEM;
     cudaLaunchAttribute at;
     at.id = cudaLaunchAttributeClusterDimension;
     at.val.clusterDim.x = 2;
@@ -399,7 +400,7 @@ int launch_tc_pair(const tk::TcParams& prm, cudaStream_t s) {
     at.val.clusterDim.z = 1;
     cfg.attrs = &at;
     cfg.numAttrs = 1;
-    if (cudaOccupancyMaxActiveClusters(&max_clusters, tk::tc_gemm_pair_kernel<DENSE>, &cfg) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveClusters(&max_clusters, tk::tc_gemm_pair_kernel<DENSE, CSTREAM>, &cfg) != cudaSuccess ||
         max_clusters <= 0) {
       cudaGetLastError();
       max_clusters = sm_count() / 2;
@@ -407,7 +408,7 @@ int launch_tc_pair(const tk::TcParams& prm, cudaStream_t s) {
     if (getenv("TK_VERBOSE")) fprintf(stderr, "tk: pair kernel max active clusters %d\n", max_clusters);
   }
   const int grid = 2 * std::min(prm.num_tiles, max_clusters);
-  tk::tc_gemm_pair_kernel<DENSE><<<grid, tk::TC_THREADS, tk::TC2_SMEM, s>>>(prm);
+  tk::tc_gemm_pair_kernel<DENSE, CSTREAM><<<grid, tk::TC_THREADS, SMEM, s>>>(prm);
   TK_CUDA(cudaGetLastError());
   ++g_launches;
   return TK_OK;
@@ -703,6 +704,16 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
       if (!mn && use3d && p->n % 64 == 0) {
         if ((rc = make_map_mn3d(&pp.tb[0], b_plane0, p->b.scalar, p->n, p->k, pitch, 2))) return rc;
         pp.mn3d |= 2;
+      }
+      // streamed C/D epilogue (TMA ring + bulk stores) when C/D are TMA-compatible
+      bool cs = dense && (prm.c_zero || ((prm.ldc * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(c) & 15) == 0)) &&
+                (prm.ldd * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(d) & 15) == 0;
+      if (const char* e = getenv("TK_PAIR_CSTREAM")) cs = cs && atoi(e);
+      if (cs) {
+        if (!prm.c_zero && (rc = make_map_2d(&pp.tcmap, c, TK_F32, p->m, p->n, prm.ldc, 32, 32))) return rc;
+        if ((rc = make_map_2d(&pp.tdmap, d, TK_F32, p->m, p->n, prm.ldd, 32, 32))) return rc;
+        pp.d_tma = 1;
+        return launch_tc_pair<true, true>(pp, s);
       }
       return dense ? launch_tc_pair<true>(pp, s) : launch_tc_pair<false>(pp, s);
     }

@@ -249,7 +249,7 @@ __device__ __forceinline__ void epilogue_dense(const TcParams& p, uint64_t* tful
 // Dense column-major epilogue for HBM-bound shapes: C arrives in a per-warp ring of TMA boxes
 // filled by the loader warp; D is written back into the same slot and stored with one TMA
 // bulk store per 32x32 box (the slot is handed back to the loader once that store has read it).
-template <int COLS, int BN>
+template <int COLS, int BN, int CSLOTS = TC_CSLOTS>
 __device__ __forceinline__ void epilogue_stream(const TcParams& p, uint64_t* tfull, uint32_t aphase,
                                                 uint32_t tbase, int i, int jbase, int lane,
                                                 float* ring, uint64_t* cfull, uint64_t* cempty,
@@ -269,15 +269,15 @@ __device__ __forceinline__ void epilogue_stream(const TcParams& p, uint64_t* tfu
     const int jl = j0 + lane;
     const float bcol = (p.bias_axis == 1 && jl < p.n) ? p.bias[jl] : 0.f;
     const float qcol = (p.affine && p.colsum_b && jl < p.n) ? p.aff_q * p.colsum_b[jl] : 0.f;
-    const uint32_t slot = cq % TC_CSLOTS;
+    const uint32_t slot = cq % CSLOTS;
     float* box = ring + slot * (TC_CBOX_BYTES / 4);
     float cv[32];
     if (has_c) {
-      mbar_wait(&cfull[slot], (cq / TC_CSLOTS) & 1);
+      mbar_wait(&cfull[slot], (cq / CSLOTS) & 1);
 #pragma unroll
       for (int jj = 0; jj < 32; ++jj) cv[jj] = box[jj * 32 + lane];
     } else if (p.d_tma) {
-      if (lane == 0) bulk_wait_read<TC_CSLOTS - 1>();  // slot's previous store has read it
+      if (lane == 0) bulk_wait_read<CSLOTS - 1>();  // slot's previous store has read it
       __syncwarp();
     }
     tmem_ld_wait();
@@ -301,7 +301,7 @@ __device__ __forceinline__ void epilogue_stream(const TcParams& p, uint64_t* tfu
         bulk_commit();
         if (has_c) {  // hand the previous chunk's slot back once its store has read it
           bulk_wait_read<1>();
-          if (cq > 0) mbar_arrive(&cempty[(cq - 1) % TC_CSLOTS]);
+          if (cq > 0) mbar_arrive(&cempty[(cq - 1) % CSLOTS]);
         }
       }
     } else {

@@ -15,23 +15,37 @@
 namespace tk {
 
 constexpr int TC2_BN = 256;                 // pair tile N (instruction N)
-constexpr int TC2_STAGES = 6;
+#ifndef TK_TC2_STAGES
+#define TK_TC2_STAGES 6
+#endif
+constexpr int TC2_STAGES = TK_TC2_STAGES;
 constexpr int TC2_TILE_BYTES = 128 * 64 * 2;  // A (128 rows) or B (128 cols) per CTA per stage
 constexpr int TC2_STAGE_BYTES = 2 * TC2_TILE_BYTES;
 constexpr int TC2_BAR_OFFSET = TC2_STAGES * TC2_STAGE_BYTES;
 constexpr int TC2_SMEM = TC2_BAR_OFFSET + 256 + 1024;
+// C-streaming variant: 5 stages + a 2-slot C/D ring per epilogue warp
+constexpr int TC2S_STAGES = 5;
+constexpr int TC2S_CSLOTS = 2;
+constexpr int TC2S_CRING = TC2S_STAGES * TC2_STAGE_BYTES;
+constexpr int TC2S_BAR_OFFSET = TC2S_CRING + TC_EPI_WARPS * TC2S_CSLOTS * TC_CBOX_BYTES;
+constexpr int TC2S_SMEM = TC2S_BAR_OFFSET + 512 + 1024;
 
-template <bool DENSE_EPI>
+template <bool DENSE_EPI, bool CSTREAM = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     tc_gemm_pair_kernel(const __grid_constant__ TcParams p) {
+  constexpr int STAGES = CSTREAM ? TC2S_STAGES : TC2_STAGES;
+  constexpr int NCBAR = CSTREAM ? TC_EPI_WARPS * TC2S_CSLOTS : 0;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + TC2_BAR_OFFSET);
-  uint64_t* empty = full + TC2_STAGES;
-  uint64_t* tfull = empty + TC2_STAGES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (CSTREAM ? TC2S_BAR_OFFSET : TC2_BAR_OFFSET));
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* cfull = tempty + 2;
+  uint64_t* cempty = cfull + NCBAR;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + NCBAR);
+  float* cring = reinterpret_cast<float*>(smem + TC2S_CRING);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -43,15 +57,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&p.ta[0]);
     tma_prefetch(&p.tb[0]);
+    if (CSTREAM && !p.c_zero) tma_prefetch(&p.tcmap);
+    if (CSTREAM) tma_prefetch(&p.tdmap);
   }
   if (warp == 1 && lane == 0) {
-    for (int s = 0; s < TC2_STAGES; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 2 * TC_EPI_WARPS);
+    }
+    for (int s = 0; s < NCBAR; ++s) {
+      mbar_init(&cfull[s], 1);
+      mbar_init(&cempty[s], 1);
     }
     fence_mbar_init();
   }
@@ -67,7 +87,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
   auto a_tile = [&](int s) -> uint8_t* { return smem + s * TC2_STAGE_BYTES; };
   auto b_tile = [&](int s) -> uint8_t* { return smem + s * TC2_STAGE_BYTES + TC2_TILE_BYTES; };
 
-  if (warp == 0) {
+  if (CSTREAM && warp == 3) {
+    // ------------------------------------------------------------ C loader (both CTAs)
+    if (!p.c_zero && lane == 0) {
+      uint32_t q = 0;
+      for (int t = cluster; t < p.num_tiles; t += nclusters) {
+        int mb, nb;
+        tile_coords(p, t, mb, nb);
+        for (int ch = 0; ch < 4; ++ch, ++q) {
+          const uint32_t slot = q % TC2S_CSLOTS, ph = (q / TC2S_CSLOTS) & 1;
+          for (int w = 0; w < TC_EPI_WARPS; ++w) {
+            const int bi = w * TC2S_CSLOTS + int(slot);
+            mbar_wait(&cempty[bi], ph ^ 1);
+            mbar_arrive_expect_tx(&cfull[bi], TC_CBOX_BYTES);
+            tma_load_2d(smem + TC2S_CRING + bi * TC_CBOX_BYTES, &p.tcmap, &cfull[bi],
+                        mb * 256 + int(rank) * 128 + (w & 3) * 32,
+                        nb * TC2_BN + (w >> 2) * 128 + ch * 32, policy_evict_normal());
+          }
+        }
+      }
+    }
+  } else if (warp == 0) {
     // ------------------------------------------------------------ producer (both CTAs)
     if (lane == 0) {
       const uint64_t pol = p.pol_ab ? policy_evict_last() : policy_evict_normal();
@@ -99,7 +139,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           } else {
             tma_load_2d_pair(b_tile(stage), &p.tb[0], fb, k0, n0, pol);
           }
-          if (++stage == TC2_STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
@@ -130,7 +170,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
             tc_mma_f16_pair(d0, a0, b0, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
           }
           tc_commit_pair(&empty[stage], 0x3);
-          if (++stage == TC2_STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
         tc_commit_pair(&tfull[as], 0x3);
       }
@@ -142,6 +182,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     const int half = ew >> 2;
     const int row_local = quarter * 32 + lane;
     int local = 0;
+    uint32_t cq = 0;
     for (int t = cluster; t < p.num_tiles; t += nclusters, ++local) {
       int mb, nb;
       tile_coords(p, t, mb, nb);
@@ -150,7 +191,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       const int i = mb * 256 + int(rank) * 128 + row_local;
       const uint32_t tbase = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(as * 256);
       const int jbase = nb * TC2_BN + half * 128;
-      if (p.dbg_skip_epi) {
+      if (CSTREAM) {
+        epilogue_stream<128, TC2_BN, TC2S_CSLOTS>(
+            p, tfull + as, aphase, tbase, i, jbase, lane, cring + ew * TC2S_CSLOTS * (TC_CBOX_BYTES / 4),
+            cfull + ew * TC2S_CSLOTS, cempty + ew * TC2S_CSLOTS, cq, mb * 256 + int(rank) * 128 + quarter * 32);
+      } else if (p.dbg_skip_epi) {
         mbar_wait(tfull + as, aphase);
         tc_fence_after();
       } else if (DENSE_EPI)
@@ -163,6 +208,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     }
   }
 
+  if (CSTREAM && warp >= 4 && lane == 0) bulk_wait<0>();
   tc_fence_before();
   cluster_sync();
   if (warp == 2) {
