@@ -21,6 +21,7 @@
 #include "tk_tc_gemm.cuh"
 #include "tk_tc_gemm2.cuh"
 #include "tk_tc_gemm4.cuh"
+#include "tk_tc_gemm2c.cuh"
 
 namespace {
 
@@ -522,6 +523,8 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
   const void* a_pl[2] = {a, nullptr};
   const void* a_plane0 = a;
   const void* b_plane0 = b;
+  const void* planes_a[2] = {a, nullptr};
+  const void* planes_b[2] = {b, nullptr};
   if (p->a.kind == TK_LAYOUT_DIAGONAL) {
     prm.diag_a = 1;
     prm.diag = a;
@@ -543,6 +546,8 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
       a_pl[1] = p0 + vol;
     }
     a_plane0 = a_pl[0];
+    planes_a[0] = a_pl[0];
+    planes_a[1] = a_pl[1];
     for (int pl = 0; pl < planes; ++pl) {
       int rc = mn ? make_map_2d(&prm.ta[pl], a_pl[pl], p->a.scalar, p->m, p->k, pitch, 64, 64)
                   : make_map_2d(&prm.ta[pl], a_pl[pl], p->a.scalar, p->k, p->m, pitch, 64, 128);
@@ -569,6 +574,8 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
       b_pl[1] = p0 + vol;
     }
     b_plane0 = b_pl[0];
+    planes_b[0] = b_pl[0];
+    planes_b[1] = b_pl[1];
     for (int pl = 0; pl < planes; ++pl) {
       int rc = mn_k ? make_map_2d(&prm.tb[pl], b_pl[pl], p->b.scalar, p->k, p->n, pitch, 64, BN)
                     : make_map_2d(&prm.tb[pl], b_pl[pl], p->b.scalar, p->n, p->k, pitch, 64, 64);
@@ -716,6 +723,50 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
         return launch_tc_pair<true, true>(pp, s);
       }
       return dense ? launch_tc_pair<true>(pp, s) : launch_tc_pair<false>(pp, s);
+    }
+  }
+  if (op != TK_OP_REAL) {
+    // complex / dual on a CTA pair once there are enough 256x128 pair tiles
+    const int64_t pair_tiles = ((p->m + 255) / 256) * ((p->n + tk::TC2C_BN - 1) / tk::TC2C_BN);
+    if (ov == 2 || (ov == 0 && pair_tiles >= sm_count() / 2 && prm.kb_total > 4)) {
+      tk::TcParams pp = prm;
+      pp.num_mb = int((p->m + 255) / 256);
+      pp.num_nb = int((p->n + tk::TC2C_BN - 1) / tk::TC2C_BN);
+      pp.num_tiles = pp.num_mb * pp.num_nb;
+      int mn;
+      int64_t pitch;
+      int rc;
+      tma_operand(p->a, mn, pitch);
+      pp.mn3d = 0;
+      if (p->a.pair == TK_PAIR_INTERLEAVED) pitch = mn ? p->m : p->k;  // de-interleaved planes
+      if (mn && p->m % 64 == 0) {
+        for (int pl = 0; pl < 2; ++pl)
+          if ((rc = make_map_mn3d(&pp.ta[pl], planes_a[pl], p->a.scalar, p->m, p->k, pitch, 2))) return rc;
+        pp.mn3d |= 1;
+      }
+      tma_operand(p->b, mn, pitch);
+      if (p->b.pair == TK_PAIR_INTERLEAVED) pitch = mn ? p->k : p->n;
+      if (mn)  // K-major B: this CTA's 64-column half per box
+        for (int pl = 0; pl < 2; ++pl)
+          if ((rc = make_map_2d(&pp.tb[pl], planes_b[pl], p->b.scalar, p->k, p->n, pitch, 64, 64))) return rc;
+      static bool attr[2][2] = {{false, false}, {false, false}};
+      const int oi = op == TK_OP_COMPLEX ? 0 : 1;
+      auto launch = [&](auto kern) -> int {
+        if (!attr[oi][dense]) {
+          TK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tk::TC2C_SMEM));
+          attr[oi][dense] = true;
+        }
+        const int grid = 2 * std::min(pp.num_tiles, sm_count() / 2);
+        kern<<<grid, tk::TC_THREADS, tk::TC2C_SMEM, s>>>(pp);
+        TK_CUDA(cudaGetLastError());
+        ++g_launches;
+        return TK_OK;
+      };
+      if (op == TK_OP_COMPLEX)
+        return dense ? launch(tk::tc_gemm_pair_ops_kernel<tk::OP_COMPLEX, true>)
+                     : launch(tk::tc_gemm_pair_ops_kernel<tk::OP_COMPLEX, false>);
+      return dense ? launch(tk::tc_gemm_pair_ops_kernel<tk::OP_DUAL, true>)
+                   : launch(tk::tc_gemm_pair_ops_kernel<tk::OP_DUAL, false>);
     }
   }
   switch (op) {

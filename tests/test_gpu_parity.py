@@ -106,10 +106,13 @@ def test_fused_affine_bias_relu(cuda):
     assert counters.global_stores == m * n
 
 
+@pytest.mark.parametrize("kernel", ["auto", "single", "pair"])
 @pytest.mark.parametrize("split", [False, True])
 @pytest.mark.parametrize("kind", ["complex", "dual"])
-def test_pair_operators(cuda, split, kind):
-    m, n, k = 256, 384, 192
+def test_pair_operators(cuda, split, kind, kernel, monkeypatch):
+    if kernel != "auto":
+        monkeypatch.setenv("TK_TC_KERNEL", kernel)
+    m, n, k = 512, 384, 320
     rng = np.random.default_rng(3)
     h16 = lambda s: rng.standard_normal(s).astype(np.float16)
     if kind == "complex":
