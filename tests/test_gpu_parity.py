@@ -288,3 +288,25 @@ def test_gemm_ex_raw_host_pipelined(cuda, trans_a):
                         b.ctypes.data, -0.5, 0.0, c.ctypes.data)
     assert st == 0, tk._lib.last_error()
     assert O.rel_err(c, want) <= O.tolerance(k)
+
+
+def test_cuda_graph_capture(cuda):
+    """gemm_execute launches are stream-ordered and capture into a CUDA graph."""
+    m = n = k = 512
+    rng = np.random.default_rng(11)
+    a = _dev(rng.integers(-4, 5, (m, k)).astype(np.float16))
+    b = _dev(rng.integers(-4, 5, (k, n)).astype(np.float16))
+    c = _dev(rng.integers(-4, 5, (m, n)).astype(np.float32))
+    d = torch.zeros(m * n, device=cuda)
+    cfg = tk.build_dense_config(m, n, k, np.float16)
+    tk.matmul(cfg, a, b, c, d)                      # warm: plan cached, attributes set
+    want = d.clone()
+    d.zero_()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            tk.matmul(cfg, a, b, c, d, synchronize=False)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(d, want)
