@@ -660,7 +660,13 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
                decode_affine(p->t_s2g, pair, prm.s_mul, prm.s_add, prm.s_relu);
   // HBM-bound shapes (diagonal A, K <= 4 block-K steps): C streamed through TMA by a loader warp
   const int ov = tc_kernel_override();
-  if (op == TK_OP_REAL && dense && (ov == 3 || (ov == 0 && (prm.diag_a || prm.kb_total <= 4)))) {
+  const int64_t pair_tiles_real = ((p->m + 255) / 256) * ((p->n + tk::TC2_BN - 1) / tk::TC2_BN);
+  const bool pair_ok = !prm.diag_a && prm.kb_total > 4 && pair_tiles_real >= 32;
+  // streamed-C single-CTA kernel: HBM-bound shapes, and single-wave dense shapes too small
+  // for the CTA pair (C prefetched by the loader warp while the mainloop runs)
+  const bool single_wave = prm.num_tiles <= sm_count();
+  if (op == TK_OP_REAL && dense &&
+      (ov == 3 || (ov == 0 && (prm.diag_a || prm.kb_total <= 4 || (single_wave && !pair_ok))))) {
     const bool cs = prm.c_zero || ((prm.ldc * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(c) & 15) == 0);
     if (cs) {
       tk::TcParams ps = prm;
@@ -687,7 +693,7 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
       if (mn && (rc = make_map_2d(&pp.tb[0], b_plane0, p->b.scalar, p->k, p->n, pitch, 64, 64))) return rc;
       return dense ? launch_tc_quad<true>(pp, s) : launch_tc_quad<false>(pp, s);
     }
-    if (ov == 2 || (ov == 0 && pair_tiles >= sm_count() / 2 && prm.kb_total > 4)) {
+    if (ov == 2 || (ov == 0 && pair_ok)) {
       tk::TcParams pp = prm;
       pp.num_mb = int((p->m + 255) / 256);
       pp.num_nb = int((p->n + tk::TC2_BN - 1) / tk::TC2_BN);

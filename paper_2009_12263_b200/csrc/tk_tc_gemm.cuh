@@ -44,13 +44,13 @@ struct TcCfg<OP_DUAL> {
 
 // C-streaming variant (HBM-bound shapes: diagonal A, K <= 256): 2 mainloop stages and a
 // per-epilogue-warp ring of TMA-loaded C boxes (32 rows x 32 columns fp32).
-constexpr int TC_CSLOTS = 3;
+constexpr int TC_CSLOTS = 2;
 constexpr int TC_CBOX_BYTES = 32 * 32 * 4;
 
 template <int OP, bool CSTREAM = false>
 struct TcSmem {
   using C = TcCfg<OP>;
-  static constexpr int STAGES = CSTREAM ? 2 : C::STAGES;
+  static constexpr int STAGES = CSTREAM ? 3 : C::STAGES;
   static constexpr int B_TILE_BYTES = C::BN * TC_BK * 2;
   static constexpr int STAGE_BYTES = C::PLANES * (TC_A_TILE_BYTES + B_TILE_BYTES);
   static constexpr int CRING_OFFSET = STAGES * STAGE_BYTES;
