@@ -364,7 +364,7 @@ int sm_count() {
   return n;
 }
 
-template <int OP, bool DENSE, bool CSTREAM = false>
+template <int OP, bool DENSE, int CSTREAM = 0>
 int launch_tc_variant(const tk::TcParams& prm, cudaStream_t s) {
   using S = tk::TcSmem<OP, CSTREAM>;
   static bool attr = false;
@@ -675,7 +675,8 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
       ps.d_tma = (prm.ldd * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(d) & 15) == 0;
       if (const char* e = getenv("TK_D_TMA")) ps.d_tma = ps.d_tma && atoi(e);
       if (ps.d_tma && (rc = make_map_2d(&ps.tdmap, d, TK_F32, p->m, p->n, prm.ldd, 32, 32))) return rc;
-      return launch_tc_variant<tk::OP_REAL, true, true>(ps, s);
+      const bool hbm = prm.diag_a || prm.kb_total <= 4;
+      return hbm ? launch_tc_variant<tk::OP_REAL, true, 1>(ps, s) : launch_tc_variant<tk::OP_REAL, true, 2>(ps, s);
     }
   }
   if (op == TK_OP_REAL && !prm.diag_a) {

@@ -42,21 +42,24 @@ struct TcCfg<OP_DUAL> {
   static constexpr int PLANES = 2, BN = 128, STAGES = 3, ACC_COLS = 256, TMEM_COLS = 512;
 };
 
-// C-streaming variant (HBM-bound shapes: diagonal A, K <= 256): 2 mainloop stages and a
-// per-epilogue-warp ring of TMA-loaded C boxes (32 rows x 32 columns fp32).
-constexpr int TC_CSLOTS = 2;
+// C-streaming variants: a per-epilogue-warp ring of TMA-loaded C boxes (32 rows x 32 columns
+// fp32), refilled by the loader warp.  CS = 1 (HBM-bound shapes: diagonal A, K <= 256):
+// 2 mainloop stages, 3 ring slots.  CS = 2 (single-wave dense shapes): 3 stages, 2 slots.
 constexpr int TC_CBOX_BYTES = 32 * 32 * 4;
+__host__ __device__ constexpr int tc_cslots(int cs) { return cs == 1 ? 3 : 2; }
+constexpr int TC_CSLOTS = 3;
 
-template <int OP, bool CSTREAM = false>
+template <int OP, int CSTREAM = 0>
 struct TcSmem {
   using C = TcCfg<OP>;
-  static constexpr int STAGES = CSTREAM ? 3 : C::STAGES;
+  static constexpr int CSLOTS = tc_cslots(CSTREAM);
+  static constexpr int STAGES = CSTREAM == 1 ? 2 : CSTREAM == 2 ? 3 : C::STAGES;
   static constexpr int B_TILE_BYTES = C::BN * TC_BK * 2;
   static constexpr int STAGE_BYTES = C::PLANES * (TC_A_TILE_BYTES + B_TILE_BYTES);
   static constexpr int CRING_OFFSET = STAGES * STAGE_BYTES;
-  static constexpr int CRING_BYTES = CSTREAM ? TC_EPI_WARPS * TC_CSLOTS * TC_CBOX_BYTES : 0;
+  static constexpr int CRING_BYTES = CSTREAM ? TC_EPI_WARPS * CSLOTS * TC_CBOX_BYTES : 0;
   static constexpr int BAR_OFFSET = CRING_OFFSET + CRING_BYTES;
-  static constexpr int NCBAR = CSTREAM ? TC_EPI_WARPS * TC_CSLOTS : 0;
+  static constexpr int NCBAR = CSTREAM ? TC_EPI_WARPS * CSLOTS : 0;
   static constexpr int BAR_BYTES = (2 * STAGES + 4 + 2 * NCBAR) * 8 + 16;
   static constexpr int TOTAL = BAR_OFFSET + BAR_BYTES + 1024;  // +1024 for manual alignment
 };
@@ -367,7 +370,7 @@ __device__ __noinline__ void epilogue_generic(const TcParams& p, uint64_t* tfull
   }
 }
 
-template <int OP, bool DENSE_EPI, bool CSTREAM = false>
+template <int OP, bool DENSE_EPI, int CSTREAM = 0>
 __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(const __grid_constant__ TcParams p) {
   using C = TcCfg<OP>;
   using S = TcSmem<OP, CSTREAM>;
@@ -545,9 +548,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(const __grid_con
         int mb, nb;
         tile_coords(p, t, mb, nb);
         for (int ch = 0; ch < CHUNKS; ++ch, ++q) {
-          const uint32_t slot = q % TC_CSLOTS, ph = (q / TC_CSLOTS) & 1;
+          const uint32_t slot = q % S::CSLOTS, ph = (q / S::CSLOTS) & 1;
           for (int w = 0; w < TC_EPI_WARPS; ++w) {
-            const int bi = w * TC_CSLOTS + int(slot);
+            const int bi = w * S::CSLOTS + int(slot);
             mbar_wait(&cempty[bi], ph ^ 1);
             mbar_arrive_expect_tx(&cfull[bi], TC_CBOX_BYTES);
             const int row0 = mb * TC_BM + (w & 3) * 32;
@@ -576,9 +579,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(const __grid_con
       const uint32_t tbase = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(as * C::ACC_COLS);
       const int jbase = nb * BN + half * COLS_PER_WARP;
       if (CSTREAM)
-        epilogue_stream<COLS_PER_WARP, BN>(p, tfull + as, aphase, tbase, i, jbase, lane,
-                                           cring + ew * TC_CSLOTS * (TC_CBOX_BYTES / 4),
-                                           cfull + ew * TC_CSLOTS, cempty + ew * TC_CSLOTS, cq,
+        epilogue_stream<COLS_PER_WARP, BN, S::CSLOTS>(p, tfull + as, aphase, tbase, i, jbase, lane,
+                                           cring + ew * S::CSLOTS * (TC_CBOX_BYTES / 4),
+                                           cfull + ew * S::CSLOTS, cempty + ew * S::CSLOTS, cq,
                                            mb * TC_BM + quarter * 32);
       else if (DENSE_EPI)
         epilogue_dense<OP, COLS_PER_WARP, BN>(p, tfull + as, aphase, tbase, i, jbase, lane);
