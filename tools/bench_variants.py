@@ -29,7 +29,7 @@ def rnd(n, dt):
     return torch.randn(n, generator=g, device=dev).to(dt)
 
 
-from bench import ClockSampler  # noqa: E402
+from paper_2009_12263_b200.clocks import ClockSampler  # noqa: E402
 
 _clock = {}
 
