@@ -88,7 +88,7 @@ def cpu_sample(m, k, threads):
     SURVEY 8c protocol).  The slab width s bounds the run to a few seconds on the host cores.
     """
     tilekit, kind = _reference_module()
-    s = 512 * max(1, min(8, threads // 8))
+    s = 1024 * max(1, min(8, -(-threads // 8)))  # one 1024-column block per 8 host threads
     a, b, c = _cpu_inputs(m, k, s)
     flops = 2.0 * m * s * k
     if tilekit is not None:
