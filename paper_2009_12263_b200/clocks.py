@@ -16,6 +16,7 @@ class ClockSampler:
 
     def __init__(self, index):
         self.samples, self.reasons, self.ok = [], set(), False
+        self.power = []
         self.max_mhz = None
         try:
             import pynvml
@@ -36,6 +37,10 @@ class ClockSampler:
                 mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 if not mask & 0x1:  # not idle
                     self.samples.append(mhz)
+                    try:
+                        self.power.append(self.nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
+                    except Exception:
+                        pass
                     for bit, name in self.REASONS.items():
                         if mask & bit and name != "gpu_idle":
                             self.reasons.add(name)
@@ -58,5 +63,8 @@ class ClockSampler:
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
                     "samples": 0}
-        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        out = {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+               "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        if self.power:
+            out["power_w"] = float(np.max(self.power))
+        return out

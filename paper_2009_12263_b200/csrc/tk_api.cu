@@ -276,6 +276,15 @@ Workspace plan_workspace(const TkGemmPlan* p0, int lane) {
 }
 
 // ------------------------------------------------------------------ TMA
+// TK_L2_PROMO=0|64|128|256 (tuning knob; default 256B L2 sector promotion for TMA loads)
+CUtensorMapL2promotion l2_promo() {
+  const char* e = getenv("TK_L2_PROMO");
+  const int v = e ? atoi(e) : 256;
+  return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+       : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+       : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -304,7 +313,7 @@ int make_map_2d(CUtensorMap* map, const void* base, int scalar, uint64_t inner, 
   CUresult r = enc(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE,
                    f32 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   l2_promo(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(TK_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
   return TK_OK;
 }
@@ -321,7 +330,7 @@ int make_map_mn3d(CUtensorMap* map, const void* base, int scalar, uint64_t mn, u
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(map, scalar == TK_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
                    3, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_SWIZZLE_128B, l2_promo(),
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(TK_ERR_CUDA, "cuTensorMapEncodeTiled (3-D) failed (%d)", int(r));
   return TK_OK;
@@ -379,13 +388,13 @@ int launch_tc_variant(const tk::TcParams& prm, cudaStream_t s) {
   return TK_OK;
 }
 
-template <bool DENSE, bool CSTREAM = false>
+template <bool DENSE, bool CSTREAM = false, int NSUB = 1>
 int launch_tc_pair(const tk::TcParams& prm, cudaStream_t s) {
-  constexpr int SMEM = CSTREAM ? tk::TC2S_SMEM : tk::TC2_SMEM;
+  constexpr int SMEM = tk::Tc2Plan<NSUB, CSTREAM>::SMEM;
+  auto kern = tk::tc_gemm_pair_kernel<DENSE, CSTREAM, NSUB>;
   static bool attr = false;
   if (!attr) {
-    TK_CUDA(cudaFuncSetAttribute(tk::tc_gemm_pair_kernel<DENSE, CSTREAM>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+    TK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
     attr = true;
   }
   static int max_clusters = 0;
@@ -401,15 +410,14 @@ int launch_tc_pair(const tk::TcParams& prm, cudaStream_t s) {
     at.val.clusterDim.z = 1;
     cfg.attrs = &at;
     cfg.numAttrs = 1;
-    if (cudaOccupancyMaxActiveClusters(&max_clusters, tk::tc_gemm_pair_kernel<DENSE, CSTREAM>, &cfg) != cudaSuccess ||
-        max_clusters <= 0) {
+    if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters <= 0) {
       cudaGetLastError();
       max_clusters = sm_count() / 2;
     }
     if (getenv("TK_VERBOSE")) fprintf(stderr, "tk: pair kernel max active clusters %d\n", max_clusters);
   }
   const int grid = 2 * std::min(prm.num_tiles, max_clusters);
-  tk::tc_gemm_pair_kernel<DENSE, CSTREAM><<<grid, tk::TC_THREADS, SMEM, s>>>(prm);
+  kern<<<grid, tk::TC_THREADS, SMEM, s>>>(prm);
   TK_CUDA(cudaGetLastError());
   ++g_launches;
   return TK_OK;
@@ -629,6 +637,7 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
   }
   // ---- epilogue
   prm.c_zero = p->c.kind == TK_LAYOUT_ZERO;
+  if (const char* g = getenv("TK_DBG_C_ZERO")) prm.c_zero |= atoi(g);  // diagnostic: skip C
   prm.c_pair = p->c.pair;
   prm.d_pair = p->d.pair;
   prm.c_ptr = c;
@@ -650,6 +659,8 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
   prm.group_m = 8;
   if (const char* g = getenv("TK_GROUP_M")) prm.group_m = std::max(1, atoi(g));
   if (const char* g = getenv("TK_DBG_SKIP_EPI")) prm.dbg_skip_epi = atoi(g);
+  if (const char* g = getenv("TK_DBG_NO_LOAD")) prm.dbg_skip_epi |= atoi(g) ? 2 : 0;
+  if (const char* g = getenv("TK_DBG_NO_MMA")) prm.dbg_skip_epi |= atoi(g) ? 4 : 0;
   prm.pol_ab = 1;  // A/B panels are re-read by neighbouring tiles: keep them in L2
   if (const char* g = getenv("TK_POLICY_AB")) prm.pol_ab = atoi(g);
   const bool pair = op != TK_OP_REAL;
@@ -696,8 +707,10 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
     }
     if (ov == 2 || (ov == 0 && pair_ok)) {
       tk::TcParams pp = prm;
+      int nsub = 1;
+      if (const char* e = getenv("TK_PAIR_NSUB")) nsub = atoi(e) == 2 ? 2 : 1;
       pp.num_mb = int((p->m + 255) / 256);
-      pp.num_nb = int((p->n + tk::TC2_BN - 1) / tk::TC2_BN);
+      pp.num_nb = int((p->n + tk::TC2_BN * nsub - 1) / (tk::TC2_BN * nsub));
       pp.num_tiles = pp.num_mb * pp.num_nb;
       // per-CTA halves: A box 128 rows (K-major) / B box 128 columns (K-major)
       int mn;
@@ -727,8 +740,9 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
         if (!prm.c_zero && (rc = make_map_2d(&pp.tcmap, c, TK_F32, p->m, p->n, prm.ldc, 32, 32))) return rc;
         if ((rc = make_map_2d(&pp.tdmap, d, TK_F32, p->m, p->n, prm.ldd, 32, 32))) return rc;
         pp.d_tma = 1;
-        return launch_tc_pair<true, true>(pp, s);
+        return nsub == 2 ? launch_tc_pair<true, true, 2>(pp, s) : launch_tc_pair<true, true>(pp, s);
       }
+      if (nsub == 2) return dense ? launch_tc_pair<true, false, 2>(pp, s) : launch_tc_pair<false, false, 2>(pp, s);
       return dense ? launch_tc_pair<true>(pp, s) : launch_tc_pair<false>(pp, s);
     }
   }
@@ -856,6 +870,44 @@ int tk_abi_version(void) { return TK_ABI_VERSION; }
 const char* tk_last_error(void) { return g_err.c_str(); }
 
 int tk_last_launch_count(void) { return g_launches; }
+
+namespace {
+__global__ void clock_probe_kernel(unsigned long long ns, unsigned long long* out) {
+  unsigned long long t0, t1, c0 = clock64();
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(1000);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+  } while (t1 - t0 < ns);
+  out[0] = clock64() - c0;
+  out[1] = t1 - t0;
+}
+unsigned long long* g_probe_buf = nullptr;
+}  // namespace
+
+// tuning aids (not part of the ABI header).  tk_debug_clock_probe launches one 32-thread CTA
+// that sleeps for `us` microseconds on `stream` and records SM clock ticks vs globaltimer;
+// tk_debug_clock_probe_mhz() reads the result (after a synchronize): the SM clock seen while
+// other work (e.g. a library GEMM) ran concurrently.
+int tk_debug_clock_probe(double us, void* stream) {
+  if (!g_probe_buf && cudaMalloc(&g_probe_buf, 16) != cudaSuccess) return 2;
+  clock_probe_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>((unsigned long long)(us * 1e3), g_probe_buf);
+  return cudaGetLastError() == cudaSuccess ? 0 : 2;
+}
+double tk_debug_clock_probe_mhz(void) {
+  unsigned long long v[2] = {0, 0};
+  if (!g_probe_buf || cudaMemcpy(v, g_probe_buf, sizeof(v), cudaMemcpyDeviceToHost) != cudaSuccess || !v[1])
+    return 0.0;
+  return double(v[0]) * 1e3 / double(v[1]);
+}
+
+// tuning aid (not part of the ABI header): effective SM MHz of CTA 0 over the last
+// pair-kernel launch (clock64 ticks / globaltimer ns), after a device synchronize.
+double tk_debug_pair_mhz(void) {
+  unsigned long long v[2] = {0, 0};
+  if (cudaMemcpyFromSymbol(v, tk::g_dbg_clk, sizeof(v)) != cudaSuccess || !v[1]) return 0.0;
+  return double(v[0]) * 1e3 / double(v[1]);
+}
 
 int tk_plan_lane(const TkGemmPlan* plan) {
   if (check_plan(plan)) return -1;

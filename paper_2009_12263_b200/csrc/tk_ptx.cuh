@@ -29,6 +29,29 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Long waits (epilogue warps waiting a whole mainloop for their accumulator): back off with
+// nanosleep between polls so 8 spinning warps do not burn issue slots and power.
+#ifndef TK_EPI_SLEEP
+#define TK_EPI_SLEEP 0
+#endif
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  if (TK_EPI_SLEEP == 0) {
+    mbar_wait(bar, parity);
+    return;
+  }
+  uint32_t done = 0;
+  while (true) {
+    asm volatile(
+        "{\n.reg .pred P1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+    __nanosleep(TK_EPI_SLEEP);
+  }
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }

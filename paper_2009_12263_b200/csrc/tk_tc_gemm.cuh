@@ -166,7 +166,7 @@ __device__ __forceinline__ void epilogue_dense(const TcParams& p, uint64_t* tful
       }
     };
     load_c(jbase);
-    mbar_wait(tfull, aphase);
+    mbar_wait_sleep(tfull, aphase);
     tc_fence_after();
 #pragma unroll 1
     for (int ch = 0; ch < COLS / 32; ++ch) {
@@ -200,7 +200,7 @@ __device__ __forceinline__ void epilogue_dense(const TcParams& p, uint64_t* tful
     const float* cp = reinterpret_cast<const float*>(p.c_ptr);
     float* dp = reinterpret_cast<float*>(p.d_ptr);
     const int64_t ci = row_ok ? i : 0;
-    mbar_wait(tfull, aphase);
+    mbar_wait_sleep(tfull, aphase);
     tc_fence_after();
 #pragma unroll 1
     for (int ch = 0; ch < COLS / 32; ++ch) {
@@ -262,7 +262,7 @@ __device__ __forceinline__ void epilogue_stream(const TcParams& p, uint64_t* tfu
   float* dp = reinterpret_cast<float*>(p.d_ptr) + (row_ok ? i : 0);
   const float rterm = p.affine && row_ok ? (p.aff_r * (p.rowsum_a ? p.rowsum_a[i] : 0.f) + p.aff_k) : 0.f;
   const float bias_m = (p.bias_axis == 2 && row_ok) ? p.bias[i] : 0.f;
-  mbar_wait(tfull, aphase);
+  mbar_wait_sleep(tfull, aphase);
   tc_fence_after();
 #pragma unroll 1
   for (int ch = 0; ch < COLS / 32; ++ch) {
@@ -331,7 +331,7 @@ __device__ __noinline__ void epilogue_generic(const TcParams& p, uint64_t* tfull
   const int64_t d_row = row_ok ? map_dim(p.d_map, 0, i) : 0;
   const float rsum = (p.affine && row_ok && p.rowsum_a) ? p.rowsum_a[i] : 0.f;
   const float bias_m = (p.bias_axis == 2 && row_ok) ? p.bias[i] : 0.f;
-  mbar_wait(tfull, aphase);
+  mbar_wait_sleep(tfull, aphase);
   tc_fence_after();
 #pragma unroll 1
   for (int ch = 0; ch < COLS / 32; ++ch) {

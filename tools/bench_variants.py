@@ -50,6 +50,14 @@ def timeit(fn, reps=10, warm=3):
         e.record()
         torch.cuda.synchronize()
     _clock.update(cs.summary())
+    try:  # effective SM clock of the last pair-kernel launch, measured in-kernel
+        import ctypes as _ct
+        from paper_2009_12263_b200 import _lib as _l
+        f = _l.load().tk_debug_pair_mhz
+        f.restype = _ct.c_double
+        _clock["kernel_mhz"] = round(f(), 1)
+    except Exception:
+        pass
     return s.elapsed_time(e) / reps * 1e-3 / getattr(fn, "per_call", 1)
 
 
@@ -63,7 +71,7 @@ def report(name, sec, work, unit, lane, extra=None):
            "reasons": _clock.get("reasons"), **(extra or {})}
     results.append(row)
     print(f"{name:48s} {sec * 1e3:9.3f} ms  {val:9.1f} {unit:6s} lane={lane} "
-          f"launches={row['launches']} sm={row['sm_mhz']} {row['reasons']}", flush=True)
+          f"launches={row['launches']} sm={row['sm_mhz']} kmhz={_clock.get('kernel_mhz')} W={_clock.get('power_w')} {row['reasons']}", flush=True)
 
 
 def run(cfg, a, b, c, d):
