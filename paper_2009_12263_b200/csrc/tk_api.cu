@@ -388,10 +388,10 @@ int launch_tc_variant(const tk::TcParams& prm, cudaStream_t s) {
   return TK_OK;
 }
 
-template <bool DENSE, bool CSTREAM = false, int NSUB = 1>
+template <bool DENSE, bool CSTREAM = false, int NSUB = 1, int BNI = 256>
 int launch_tc_pair(const tk::TcParams& prm, cudaStream_t s) {
-  constexpr int SMEM = tk::Tc2Plan<NSUB, CSTREAM>::SMEM;
-  auto kern = tk::tc_gemm_pair_kernel<DENSE, CSTREAM, NSUB>;
+  constexpr int SMEM = tk::Tc2Plan<NSUB, CSTREAM, BNI>::SMEM;
+  auto kern = tk::tc_gemm_pair_kernel<DENSE, CSTREAM, NSUB, BNI>;
   static bool attr = false;
   if (!attr) {
     TK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
@@ -421,6 +421,44 @@ int launch_tc_pair(const tk::TcParams& prm, cudaStream_t s) {
   TK_CUDA(cudaGetLastError());
   ++g_launches;
   return TK_OK;
+}
+
+// instantiate the pair kernel for the chosen instruction N
+template <bool DENSE, bool CSTREAM>
+int launch_tc_pair_bni(const tk::TcParams& prm, int bni, cudaStream_t s) {
+  if (bni == 64) return launch_tc_pair<DENSE, CSTREAM, 1, 64>(prm, s);
+  if (bni == 128) return launch_tc_pair<DENSE, CSTREAM, 1, 128>(prm, s);
+  return launch_tc_pair<DENSE, CSTREAM, 1, 256>(prm, s);
+}
+
+// Pair-tile width for the real operator: the instruction N (256 / 128 / 64) minimising
+// waves x per-tile time (per k-block, per SM: MMA 2*BNI clocks vs operand ingest of
+// (16 KB + 64*BNI B) at ~60 B/clock); 64 needs K-major B (64-column MN-major atoms).
+int choose_pair_bni(int64_t m, int64_t n, bool b_mn_major, int clusters) {
+  if (const char* e = getenv("TK_PAIR_BNI")) {
+    const int v = atoi(e);
+    if (v == 64 || v == 128 || v == 256) return (v == 64 && b_mn_major) ? 128 : v;
+  }
+  int best = 256;
+  double best_t = 1e300;
+  for (int bni : {256, 128, 64}) {
+    if (bni == 64 && b_mn_major) continue;
+    const int64_t tiles = ((m + 255) / 256) * ((n + bni - 1) / bni);
+    const int64_t waves = (tiles + clusters - 1) / clusters;
+    const double per_kb = std::max(2.0 * bni, (16384.0 + 64.0 * bni) / 60.0);
+    const double t = double(waves) * per_kb;
+    if (t < best_t * 0.97) { best_t = t; best = bni; }
+  }
+  return best;
+}
+
+int pair_clusters() {
+  static int c = 0;
+  if (!c) {
+    c = sm_count() / 2;
+    if (const char* e = getenv("TK_PAIR_CLUSTERS")) c = std::max(1, atoi(e));
+  }
+  return c;
 }
 
 template <bool DENSE>
@@ -671,8 +709,9 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
                decode_affine(p->t_s2g, pair, prm.s_mul, prm.s_add, prm.s_relu);
   // HBM-bound shapes (diagonal A, K <= 4 block-K steps): C streamed through TMA by a loader warp
   const int ov = tc_kernel_override();
-  const int64_t pair_tiles_real = ((p->m + 255) / 256) * ((p->n + tk::TC2_BN - 1) / tk::TC2_BN);
-  const bool pair_ok = !prm.diag_a && prm.kb_total > 4 && pair_tiles_real >= 32;
+  // the CTA pair takes every real-operator shape with more than 4 block-K steps and at least
+  // 256 rows (narrower pair tiles keep small problems spread over the SMs)
+  const bool pair_ok = !prm.diag_a && prm.kb_total > 4 && p->m > 128;
   // streamed-C single-CTA kernel: HBM-bound shapes, and single-wave dense shapes too small
   // for the CTA pair (C prefetched by the loader warp while the mainloop runs)
   const bool single_wave = prm.num_tiles <= sm_count();
@@ -692,7 +731,6 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
   }
   if (op == TK_OP_REAL && !prm.diag_a) {
     // CTA pair (256x256 tiles) once there are enough pair tiles to cover the SMs
-    const int64_t pair_tiles = ((p->m + 255) / 256) * ((p->n + tk::TC2_BN - 1) / tk::TC2_BN);
     if (ov == 4) {
       tk::TcParams pp = prm;
       pp.num_mb = int((p->m + 511) / 512);
@@ -709,13 +747,15 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
       tk::TcParams pp = prm;
       int nsub = 1;
       if (const char* e = getenv("TK_PAIR_NSUB")) nsub = atoi(e) == 2 ? 2 : 1;
-      pp.num_mb = int((p->m + 255) / 256);
-      pp.num_nb = int((p->n + tk::TC2_BN * nsub - 1) / (tk::TC2_BN * nsub));
-      pp.num_tiles = pp.num_mb * pp.num_nb;
-      // per-CTA halves: A box 128 rows (K-major) / B box 128 columns (K-major)
       int mn;
       int64_t pitch;
       int rc;
+      tma_operand(p->b, mn, pitch);
+      const int bni = nsub == 2 ? 256 : choose_pair_bni(p->m, p->n, /*b_mn_major=*/!mn, pair_clusters());
+      pp.num_mb = int((p->m + 255) / 256);
+      pp.num_nb = int((p->n + bni * nsub - 1) / (bni * nsub));
+      pp.num_tiles = pp.num_mb * pp.num_nb;
+      // per-CTA halves: A box 128 rows / B box bni/2 columns
       tma_operand(p->a, mn, pitch);
       pp.mn3d = 0;
       const char* e3 = getenv("TK_MN3D");
@@ -727,11 +767,12 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
       }
       if (!mn && (rc = make_map_2d(&pp.ta[0], a_plane0, p->a.scalar, p->k, p->m, pitch, 64, 128))) return rc;
       tma_operand(p->b, mn, pitch);
-      if (mn && (rc = make_map_2d(&pp.tb[0], b_plane0, p->b.scalar, p->k, p->n, pitch, 64, 128))) return rc;
+      if (mn && (rc = make_map_2d(&pp.tb[0], b_plane0, p->b.scalar, p->k, p->n, pitch, 64, bni / 2))) return rc;
       if (!mn && use3d && p->n % 64 == 0) {
-        if ((rc = make_map_mn3d(&pp.tb[0], b_plane0, p->b.scalar, p->n, p->k, pitch, 2))) return rc;
+        if ((rc = make_map_mn3d(&pp.tb[0], b_plane0, p->b.scalar, p->n, p->k, pitch, bni / 128))) return rc;
         pp.mn3d |= 2;
       }
+      if (getenv("TK_VERBOSE")) fprintf(stderr, "tk: pair kernel bni %d nsub %d tiles %d\n", bni, nsub, pp.num_tiles);
       // streamed C/D epilogue (TMA ring + bulk stores) when C/D are TMA-compatible
       bool cs = dense && (prm.c_zero || ((prm.ldc * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(c) & 15) == 0)) &&
                 (prm.ldd * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(d) & 15) == 0;
@@ -740,10 +781,13 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
         if (!prm.c_zero && (rc = make_map_2d(&pp.tcmap, c, TK_F32, p->m, p->n, prm.ldc, 32, 32))) return rc;
         if ((rc = make_map_2d(&pp.tdmap, d, TK_F32, p->m, p->n, prm.ldd, 32, 32))) return rc;
         pp.d_tma = 1;
-        return nsub == 2 ? launch_tc_pair<true, true, 2>(pp, s) : launch_tc_pair<true, true>(pp, s);
+        pp.c_pf_kb = nsub == 2 ? 16 : 0;
+        if (const char* e = getenv("TK_C_PF")) pp.c_pf_kb = atoi(e);
+        pp.c_pf_kb = std::min(pp.c_pf_kb, pp.kb_total);
+        return nsub == 2 ? launch_tc_pair<true, true, 2>(pp, s) : launch_tc_pair_bni<true, true>(pp, bni, s);
       }
       if (nsub == 2) return dense ? launch_tc_pair<true, false, 2>(pp, s) : launch_tc_pair<false, false, 2>(pp, s);
-      return dense ? launch_tc_pair<true>(pp, s) : launch_tc_pair<false>(pp, s);
+      return dense ? launch_tc_pair_bni<true, false>(pp, bni, s) : launch_tc_pair_bni<false, false>(pp, bni, s);
     }
   }
   if (op != TK_OP_REAL) {
@@ -899,6 +943,14 @@ double tk_debug_clock_probe_mhz(void) {
   if (!g_probe_buf || cudaMemcpy(v, g_probe_buf, sizeof(v), cudaMemcpyDeviceToHost) != cudaSuccess || !v[1])
     return 0.0;
   return double(v[0]) * 1e3 / double(v[1]);
+}
+
+// tuning aid: the 8 globaltimer stamps of CTA 0 of the last pair-kernel launch, relative to entry (us)
+int tk_debug_pair_ts(double* out) {
+  unsigned long long v[8];
+  if (cudaMemcpyFromSymbol(v, tk::g_dbg_ts, sizeof(v)) != cudaSuccess) return 2;
+  for (int i = 0; i < 8; ++i) out[i] = v[i] >= v[0] ? double(v[i] - v[0]) * 1e-3 : -1.0;
+  return 0;
 }
 
 // tuning aid (not part of the ABI header): effective SM MHz of CTA 0 over the last

@@ -93,6 +93,7 @@ struct TcParams {
   int32_t c_relu, r_relu, s_relu, pad1;
   int32_t dbg_skip_epi, pol_ab;  // tuning/diagnostic knobs (TK_DBG_SKIP_EPI, TK_POLICY_AB)
   int32_t d_tma, mn3d;           // C-streaming epilogue: D via TMA; MN-major operands via 3-D maps (bit0 A, bit1 B)
+  int32_t c_pf_kb, pad2;         // pair kernel: prefetch the tile's C into L2 this many k-blocks before its end
 };
 
 __device__ __forceinline__ void tile_coords(const TcParams& p, int t, int& mb, int& nb) {

@@ -1,12 +1,14 @@
 // tk_tc_gemm2.cuh -- the CTA-pair (cta_group::2) tcgen05 GEMM for the real operator.
 //
-// A cluster of two CTAs on one TPC computes a 256 x 256 output tile with 256x256x16
-// tcgen05.mma.cta_group::2 instructions issued by the leader CTA's MMA thread:
-//   * each CTA stages its own 128 rows of A and its own 128 columns of B (half of the pair's N),
-//     so per-SM shared-memory operand traffic is half of the single-CTA 128x256 form;
+// A cluster of two CTAs on one TPC computes a 256 x (NSUB*BNI) output tile with
+// 256 x BNI x 16 tcgen05.mma.cta_group::2 instructions issued by the leader CTA's MMA thread
+// (BNI = 256 for large problems; 128 / 64 give more tiles for single-wave shapes):
+//   * each CTA stages its own 128 rows of A and its own BNI/2 columns of B (half of the pair's N),
+//     so per-SM shared-memory operand traffic is half of the single-CTA form;
 //   * both CTAs' TMA loads credit the leader's full barrier (2-SM TMA form);
 //   * MMA completion is multicast to both CTAs' empty / accumulator-full barriers;
-//   * each CTA's TMEM holds its 128 rows x 256 FP32 columns (double-buffered, 512 columns);
+//   * each CTA's TMEM holds its 128 rows x BNI FP32 columns (double-buffered) or, for NSUB 2,
+//     one 128 x 512 accumulator;
 //     both CTAs' epilogue warps release a TMEM stage by arriving on the leader's barrier.
 // The epilogue is the same fused TMEM -> register -> global path as the single-CTA kernel.
 #pragma once
@@ -16,6 +18,15 @@ namespace tk {
 
 // diagnostic: SM clock ticks and globaltimer ns of CTA 0 over the last pair-kernel launch
 __device__ unsigned long long g_dbg_clk[2];
+// diagnostic: globaltimer stamps of CTA 0 (entry, prologue done, first stage full, last MMA
+// issued, last accumulator full, epilogue done, stores drained, exit)
+__device__ unsigned long long g_dbg_ts[8];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TK_TS(i) do { if (blockIdx.x == 0) g_dbg_ts[i] = gtimer(); } while (0)
 
 constexpr int TC2_BN = 256;                 // pair tile N per MMA (instruction N)
 #ifndef TK_TC2_STAGES
@@ -36,28 +47,35 @@ constexpr int TC2S_CRING = TC2S_STAGES * TC2_STAGE_BYTES;
 constexpr int TC2S_BAR_OFFSET = TC2S_CRING + TC_EPI_WARPS * TC2S_CSLOTS * TC_CBOX_BYTES;
 constexpr int TC2S_SMEM = TC2S_BAR_OFFSET + 512 + 1024;
 
-// Shared-memory plan of the pair kernel.  NSUB = number of N=256 pair MMAs per K step:
-// 1 -> 256 x 256 pair tiles, two TMEM accumulators (epilogue overlaps the next tile);
-// 2 -> 256 x 512 pair tiles (A re-used across 512 columns: 1/3 fewer operand bytes per
-// flop), one 512-column accumulator.
-template <int NSUB, bool CSTREAM>
+// Shared-memory plan of the pair kernel.  BNI = instruction N (pair columns per MMA);
+// NSUB = number of BNI-wide pair MMAs per K step sharing one A tile:
+// NSUB 1 -> 256 x BNI pair tiles, two TMEM accumulators (epilogue overlaps the next tile);
+// NSUB 2 -> 256 x 512 pair tiles (BNI 256; A re-used across 512 columns: 1/3 fewer operand
+// bytes per flop), one 512-column accumulator drained in two halves.
+template <int NSUB, bool CSTREAM, int BNI = 256>
 struct Tc2Plan {
-  static constexpr int STAGE_BYTES = TC2_TILE_BYTES * (1 + NSUB);
-  static constexpr int STAGES = NSUB == 1 ? (CSTREAM ? TC2S_STAGES : TC2_STAGES) : (CSTREAM ? 3 : 4);
+  static constexpr int B_BYTES = BNI * 64;  // BNI/2 columns x 64 K x 2 bytes per CTA per MMA
+  static constexpr int STAGE_BYTES = TC2_TILE_BYTES + NSUB * B_BYTES;
+  static constexpr int CRING_BYTES = CSTREAM ? TC_EPI_WARPS * TC2S_CSLOTS * TC_CBOX_BYTES : 0;
+  static constexpr int MAX_STAGES = (200 * 1024 - CRING_BYTES) / STAGE_BYTES;
+  static constexpr int STAGES = NSUB == 2 ? (CSTREAM ? 3 : 4)
+                              : BNI == 256 ? (CSTREAM ? TC2S_STAGES : TC2_STAGES)
+                              : (MAX_STAGES > 8 ? 8 : MAX_STAGES);
   static constexpr int CRING = STAGES * STAGE_BYTES;
-  static constexpr int BAR_OFFSET = CRING + (CSTREAM ? TC_EPI_WARPS * TC2S_CSLOTS * TC_CBOX_BYTES : 0);
+  static constexpr int BAR_OFFSET = CRING + CRING_BYTES;
   static constexpr int SMEM = BAR_OFFSET + 512 + 1024;
-  static constexpr int BNP = TC2_BN * NSUB;  // pair tile N
-  static constexpr int NACC = 2 / NSUB;      // TMEM accumulators (512 columns total)
+  static constexpr int BNP = BNI * NSUB;                       // pair tile N
+  static constexpr int TMEM_COLS = NSUB == 2 ? 512 : 2 * BNI;  // double-buffered for NSUB 1
+  static constexpr int WCOLS = BNI / 2;                        // columns per epilogue warp per pass
 };
 
-template <bool DENSE_EPI, bool CSTREAM = false, int NSUB = 1>
+template <bool DENSE_EPI, bool CSTREAM = false, int NSUB = 1, int BNI = 256>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     tc_gemm_pair_kernel(const __grid_constant__ TcParams p) {
-  using PL = Tc2Plan<NSUB, CSTREAM>;
+  using PL = Tc2Plan<NSUB, CSTREAM, BNI>;
+  static_assert(NSUB == 1 || BNI == 256, "NSUB 2 uses 256-wide MMAs");
   constexpr int STAGES = PL::STAGES;
   constexpr int BNP = PL::BNP;
-  constexpr int NACC = PL::NACC;
   constexpr int NCBAR = CSTREAM ? TC_EPI_WARPS * TC2S_CSLOTS : 0;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -73,6 +91,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) TK_TS(0);
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   const int cluster = blockIdx.x >> 1;
@@ -100,13 +119,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     fence_mbar_init();
   }
   if (warp == 2) {
-    tmem_alloc_pair(tmem_slot, 512);
+    tmem_alloc_pair(tmem_slot, PL::TMEM_COLS);
     tmem_relinquish_pair();
   }
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) TK_TS(1);
   unsigned long long clk0 = 0, ns0 = 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     clk0 = clock64();
@@ -115,6 +135,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
 
   auto a_tile = [&](int s) -> uint8_t* { return smem + s * PL::STAGE_BYTES; };
   auto b_tile = [&](int s) -> uint8_t* { return smem + s * PL::STAGE_BYTES + TC2_TILE_BYTES; };
+  constexpr int CH = PL::WCOLS / 32;  // 32-column chunks per epilogue warp per pass
 
   if (CSTREAM && warp == 3) {
     // ------------------------------------------------------------ C loader (both CTAs)
@@ -123,7 +144,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       for (int t = cluster; t < p.num_tiles; t += nclusters) {
         int mb, nb;
         tile_coords(p, t, mb, nb);
-        for (int ch = 0; ch < BNP / 64; ++ch, ++q) {
+        for (int ch = 0; ch < NSUB * CH; ++ch, ++q) {
           const uint32_t slot = q % TC2S_CSLOTS, ph = (q / TC2S_CSLOTS) & 1;
           for (int w = 0; w < TC_EPI_WARPS; ++w) {
             const int bi = w * TC2S_CSLOTS + int(slot);
@@ -131,7 +152,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
             mbar_arrive_expect_tx(&cfull[bi], TC_CBOX_BYTES);
             tma_load_2d(smem + PL::CRING + bi * TC_CBOX_BYTES, &p.tcmap, &cfull[bi],
                         mb * 256 + int(rank) * 128 + (w & 3) * 32,
-                        nb * BNP + (w >> 2) * (BNP / 2) + ch * 32, policy_evict_normal());
+                        nb * BNP + (ch / CH) * BNI + (w >> 2) * PL::WCOLS + (ch % CH) * 32,
+                        policy_evict_normal());
           }
         }
       }
@@ -146,7 +168,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         int mb, nb;
         tile_coords(p, t, mb, nb);
         const int m0 = mb * 256 + int(rank) * 128;     // this CTA's rows of A
-        const int n0 = nb * BNP + int(rank) * 128;  // this CTA's columns of B (per N=256 MMA)
+        const int n0 = nb * BNP + int(rank) * (BNI / 2);  // this CTA's columns of B (per MMA)
         for (int kb = 0; kb < p.kb_total; ++kb) {
           const int k0 = kb * TC_BK;
           mbar_wait(&empty[stage], phase ^ 1);
@@ -154,6 +176,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
             if (leader) mbar_arrive(&full[stage]);
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
             continue;
+          }
+          if (CSTREAM && kb == p.kb_total - p.c_pf_kb && p.c_pf_kb > 0 && !p.c_zero) {
+            // warm L2 with this CTA's C block so the (non-overlapped part of the) drain hits L2
+            for (int r = 0; r < 4; ++r)
+              for (int c = 0; c < BNP / 32; ++c)
+                tma_prefetch_l2_2d(&p.tcmap, mb * 256 + int(rank) * 128 + r * 32, nb * BNP + c * 32);
           }
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * PL::STAGE_BYTES);
           const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
@@ -167,13 +195,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           }
 #pragma unroll
           for (int sub = 0; sub < NSUB; ++sub) {
-            uint8_t* bt = b_tile(stage) + sub * TC2_TILE_BYTES;
-            const int nn = n0 + sub * TC2_BN;
+            uint8_t* bt = b_tile(stage) + sub * PL::B_BYTES;
+            const int nn = n0 + sub * BNI;
             if (p.b_mn && (p.mn3d & 2)) {
               tma_load_3d_pair(bt, &p.tb[0], fb, 0, k0, nn >> 6, pol);
-            } else if (p.b_mn) {
-              tma_load_2d_pair(bt, &p.tb[0], fb, nn, k0, pol);
-              tma_load_2d_pair(bt + 8192, &p.tb[0], fb, nn + 64, k0, pol);
+            } else if (p.b_mn) {  // 64-column atoms (BNI >= 128)
+              for (int h = 0; h < BNI / 128; ++h)
+                tma_load_2d_pair(bt + h * 8192, &p.tb[0], fb, nn + 64 * h, k0, pol);
             } else {
               tma_load_2d_pair(bt, &p.tb[0], fb, k0, nn, pol);
             }
@@ -185,7 +213,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader only)
     if (leader && lane == 0) {
-      const uint32_t idesc = idesc_f16(p.ab_fmt, p.a_mn, p.b_mn, 0, 256, TC2_BN);
+      const uint32_t idesc = idesc_f16(p.ab_fmt, p.a_mn, p.b_mn, 0, 256, BNI);
       const uint32_t a_step = p.a_mn ? 2048u : 32u;
       const uint32_t b_step = p.b_mn ? 2048u : 32u;
       const uint32_t a_lbo = p.a_mn ? 8192u : 16u;
@@ -193,30 +221,70 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int t = cluster; t < p.num_tiles; t += nclusters, ++local) {
-        const int as = local % NACC;
-        const uint32_t aphase = (local / NACC) & 1;
-        mbar_wait(&tempty[as], aphase ^ 1);
-        tc_fence_after();
-        const uint32_t d0 = tmem_base + uint32_t(as * 256);
-        for (int kb = 0; kb < p.kb_total; ++kb) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
+      auto issue = [&](int st, int sub, uint32_t d, bool first) {
 #pragma unroll
-          for (int kk = 0; kk < TC_BK / 16; ++kk) {
-            if (p.dbg_skip_epi & 4) break;  // diagnostic: operand traffic without MMAs
-            const uint64_t a0 = sdesc_sw128(smem_u32(a_tile(stage)) + kk * a_step, a_lbo, 1024);
-#pragma unroll
-            for (int sub = 0; sub < NSUB; ++sub) {
-              const uint64_t b0 =
-                  sdesc_sw128(smem_u32(b_tile(stage) + sub * TC2_TILE_BYTES) + kk * b_step, b_lbo, 1024);
-              tc_mma_f16_pair(d0 + uint32_t(sub * 256), a0, b0, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
-            }
-          }
-          tc_commit_pair(&empty[stage], 0x3);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        for (int kk = 0; kk < TC_BK / 16; ++kk) {
+          if (p.dbg_skip_epi & 4) break;  // diagnostic: operand traffic without MMAs
+          const uint64_t a0 = sdesc_sw128(smem_u32(a_tile(st)) + kk * a_step, a_lbo, 1024);
+          const uint64_t b0 =
+              sdesc_sw128(smem_u32(b_tile(st) + sub * PL::B_BYTES) + kk * b_step, b_lbo, 1024);
+          tc_mma_f16_pair(d, a0, b0, idesc, (!first || kk > 0) ? 1u : 0u);
         }
-        tc_commit_pair(&tfull[as], 0x3);
+      };
+      for (int t = cluster; t < p.num_tiles; t += nclusters, ++local) {
+        if (NSUB == 1) {
+          const int as = local & 1;
+          const uint32_t aphase = (local >> 1) & 1;
+          mbar_wait(&tempty[as], aphase ^ 1);
+          tc_fence_after();
+          const uint32_t d0 = tmem_base + uint32_t(as * BNI);
+          for (int kb = 0; kb < p.kb_total; ++kb) {
+            mbar_wait(&full[stage], phase);
+            if (local == 0 && kb == 0) TK_TS(2);
+            tc_fence_after();
+            issue(stage, 0, d0, kb == 0);
+            tc_commit_pair(&empty[stage], 0x3);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          }
+          tc_commit_pair(&tfull[as], 0x3);
+          TK_TS(3);
+        } else {
+          // 256 x 512 tile, one accumulator: columns [0,256) (lo) and [256,512) (hi) are drained
+          // in that order (tempty[0], tempty[1]).  The lo MMAs of the next tile start as soon as lo
+          // is drained; hi MMAs trail, holding up to STAGES operand stages, until hi is drained.
+          const uint32_t tph = (local & 1) ^ 1;
+          mbar_wait(&tempty[0], tph);
+          tc_fence_after();
+          bool hi_ok = false;
+          int held = 0, st0 = stage;
+          for (int kb = 0; kb < p.kb_total; ++kb) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            issue(stage, 0, tmem_base, kb == 0);
+            if (hi_ok) {
+              issue(stage, 1, tmem_base + 256u, false);
+              tc_commit_pair(&empty[stage], 0x3);
+            } else {
+              ++held;
+              if (mbar_test(&tempty[1], tph)) {
+                hi_ok = true;
+              } else if (held == STAGES || kb == p.kb_total - 1) {
+                mbar_wait(&tempty[1], tph);
+                hi_ok = true;
+              }
+              if (hi_ok) {
+                tc_fence_after();
+                for (int h = 0; h < held; ++h) {
+                  const int st = (st0 + h) % STAGES;
+                  issue(st, 1, tmem_base + 256u, h == 0 && kb + 1 == held);
+                  tc_commit_pair(&empty[st], 0x3);
+                }
+              }
+            }
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          }
+          tc_commit_pair(&tfull[0], 0x3);
+        }
       }
     }
   } else if (warp >= 4) {
@@ -230,29 +298,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     for (int t = cluster; t < p.num_tiles; t += nclusters, ++local) {
       int mb, nb;
       tile_coords(p, t, mb, nb);
-      const int as = local % NACC;
-      const uint32_t aphase = (local / NACC) & 1;
       const int i = mb * 256 + int(rank) * 128 + row_local;
-      const uint32_t tbase = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(as * 256);
-      const int jbase = nb * BNP + half * (BNP / 2);
-      if (CSTREAM) {
-        epilogue_stream<BNP / 2, BNP, TC2S_CSLOTS>(
-            p, tfull + as, aphase, tbase, i, jbase, lane, cring + ew * TC2S_CSLOTS * (TC_CBOX_BYTES / 4),
-            cfull + ew * TC2S_CSLOTS, cempty + ew * TC2S_CSLOTS, cq, mb * 256 + int(rank) * 128 + quarter * 32);
-      } else if (p.dbg_skip_epi) {
-        mbar_wait_sleep(tfull + as, aphase);
-        tc_fence_after();
-      } else if (DENSE_EPI)
-        epilogue_dense<OP_REAL, BNP / 2, BNP>(p, tfull + as, aphase, tbase, i, jbase, lane);
-      else
-        epilogue_generic<OP_REAL, BNP / 2, BNP>(p, tfull + as, aphase, tbase, i, jbase);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[as]), 0));
+      const int row0 = mb * 256 + int(rank) * 128 + quarter * 32;
+      float* my_ring = cring + ew * TC2S_CSLOTS * (TC_CBOX_BYTES / 4);
+      // NSUB 1: accumulator `local & 1`, one pass over this warp's 128 columns.
+      // NSUB 2: one accumulator, pass 0 drains columns [0,256), pass 1 [256,512) (128 per warp).
+#pragma unroll 1
+      for (int pass = 0; pass < NSUB; ++pass) {
+        const int as = NSUB == 1 ? (local & 1) : 0;
+        const uint32_t aphase = NSUB == 1 ? ((local >> 1) & 1) : (local & 1);
+        const uint32_t tbase = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(as * BNI);
+        const int jbase = nb * BNP + pass * BNI + half * PL::WCOLS;
+        if (blockIdx.x == 0 && warp == 4 && lane == 0 && t + nclusters >= p.num_tiles) {
+          mbar_wait(tfull + as, aphase);
+          TK_TS(4);
+        }
+        if (CSTREAM) {
+          epilogue_stream<PL::WCOLS, BNP, TC2S_CSLOTS>(p, tfull + as, aphase, tbase, i, jbase, lane, my_ring,
+                                                 cfull + ew * TC2S_CSLOTS, cempty + ew * TC2S_CSLOTS, cq, row0);
+        } else if (p.dbg_skip_epi) {
+          mbar_wait_sleep(tfull + as, aphase);
+          tc_fence_after();
+        } else if (DENSE_EPI)
+          epilogue_dense<OP_REAL, PL::WCOLS, BNP>(p, tfull + as, aphase, tbase, i, jbase, lane);
+        else
+          epilogue_generic<OP_REAL, PL::WCOLS, BNP>(p, tfull + as, aphase, tbase, i, jbase);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[NSUB == 1 ? as : pass]), 0));
+        if (warp == 4 && lane == 0) TK_TS(5);
+      }
     }
   }
 
   if (CSTREAM && warp >= 4 && lane == 0) bulk_wait<0>();
+  if (warp == 4 && lane == 0) TK_TS(6);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long ns1;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns1));
@@ -263,7 +343,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
   cluster_sync();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc_pair(tmem_base, 512);
+    tmem_dealloc_pair(tmem_base, PL::TMEM_COLS);
+    if (lane == 0) TK_TS(7);
   }
 }
 

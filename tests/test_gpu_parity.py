@@ -39,11 +39,20 @@ def _f32(x):
     return np.asarray(x).astype(np.float32)
 
 
-@pytest.fixture(params=["single", "pair", "quad", "stream"])
+@pytest.fixture(params=["single", "pair", "pair128", "pair64", "pair512", "quad", "stream"])
 def tc_kernel(request, monkeypatch):
-    """Pin the single-CTA (128x256) or CTA-pair (256x256) tcgen05 kernel."""
-    monkeypatch.setenv("TK_TC_KERNEL", request.param)
-    return request.param
+    """Pin the single-CTA (128x256), CTA-pair (256 x 256/128/64 tiles, or 256 x 512 with two
+    MMAs per K step), 4-CTA multicast or C-streaming tcgen05 kernel."""
+    name = request.param
+    if name.startswith("pair") and name != "pair":
+        monkeypatch.setenv("TK_TC_KERNEL", "pair")
+        if name == "pair512":
+            monkeypatch.setenv("TK_PAIR_NSUB", "2")
+        else:
+            monkeypatch.setenv("TK_PAIR_BNI", name[4:])
+    else:
+        monkeypatch.setenv("TK_TC_KERNEL", name)
+    return name
 
 
 @pytest.mark.parametrize("dtype", [np.float16, "bf16"])

@@ -113,6 +113,31 @@ def dense(n, m=None, k=None, dtype="fp16", trans="nn", name=None):
     return sec
 
 
+def cublas_ref(n, dtype=torch.float16):
+    """cuBLAS on the same operation (fp16/bf16 A,B; fp32 C,D; D = A*B + C) via torch.addmm with
+    out_dtype=float32 -- the library baseline for the sweep (graph-replayed when GRAPH=1)."""
+    a = torch.randn(n, n, generator=g, device=dev).to(dtype)
+    b = torch.randn(n, n, generator=g, device=dev).to(dtype)
+    c = torch.randn(n, n, generator=g, device=dev)
+    f = lambda: torch.addmm(c, a, b, out_dtype=torch.float32)
+    if os.environ.get("GRAPH") == "1":
+        f()
+        torch.cuda.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            for _ in range(10):
+                f()
+
+        def replay():
+            gr.replay()
+        replay.per_call = 10
+        fn = replay
+    else:
+        fn = f
+    sec = timeit(fn)
+    report(f"cuBLAS addmm {dtype} {n}^3 (same op)", sec, 2.0 * n ** 3, "TFLOPS", "cublas")
+
+
 def skinny(n, k):
     m = n
     cfg = tk.build_dense_config(m, n, k, tk.FLOAT16)
@@ -196,6 +221,9 @@ if __name__ == "__main__":
     if "sweep" in which:
         for n in (1024, 2048, 4096, 16384):
             dense(n)
+    if "cublas" in which:
+        for n in (1024, 2048, 4096, 8192, 16384):
+            cublas_ref(n)
     if "fused" in which:
         fused_c3(8192)
         fused_builder(8192)

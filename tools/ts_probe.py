@@ -1,0 +1,26 @@
+"""Where does a small pair-kernel launch spend its time: CTA-0 globaltimer stamps (us)."""
+import ctypes
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2009_12263_b200 as tk  # noqa: E402
+from paper_2009_12263_b200 import _lib, kernel  # noqa: E402
+
+lib = _lib.load()
+names = ["entry", "prologue", "1st full", "last MMA issued", "last acc full", "epilogue done", "stores drained",
+         "exit"]
+for (m, n, k) in [(1024, 1024, 320), (1024, 1024, 1024), (1024, 1024, 4096), (2048, 2048, 2048)]:
+    cfg = kernel.resolve_config(tk.build_dense_config(m, n, k, tk.FLOAT16))
+    a = torch.randn(m * k, device="cuda").half()
+    b = torch.randn(k * n, device="cuda").half()
+    c = torch.randn(m * n, device="cuda")
+    d = torch.empty(m * n, device="cuda")
+    for _ in range(5):
+        tk.gemm_execute(cfg, a, b, c, d)
+    torch.cuda.synchronize()
+    out = (ctypes.c_double * 8)()
+    lib.tk_debug_pair_ts(out)
+    print(f"{m}x{n}x{k}: " + "  ".join(f"{nm}={v:.2f}" for nm, v in zip(names, out) if nm != "-"))
