@@ -416,7 +416,9 @@ int launch_tc_pair(const tk::TcParams& prm, cudaStream_t s) {
     }
     if (getenv("TK_VERBOSE")) fprintf(stderr, "tk: pair kernel max active clusters %d\n", max_clusters);
   }
-  const int grid = 2 * std::min(prm.num_tiles, max_clusters);
+  int clusters = std::min(prm.num_tiles, max_clusters);
+  if (const char* e = getenv("TK_PAIR_GRID")) clusters = std::max(1, std::min(clusters, atoi(e)));
+  const int grid = 2 * clusters;
   kern<<<grid, tk::TC_THREADS, SMEM, s>>>(prm);
   TK_CUDA(cudaGetLastError());
   ++g_launches;

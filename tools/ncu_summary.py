@@ -20,6 +20,8 @@ KEYS = [
     "sm__throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread",
     "launch__grid_size", "launch__block_size", "launch__shared_mem_per_block_dynamic",
     "smsp__inst_executed.sum", "launch__cluster_dim_x",
+    "l1tex__m_xbar2l1tex_read_bytes.sum", "lts__t_sectors_srcunit_tex.sum",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
 ]
 SCALE = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0, "Tbyte": 1e12}
 
