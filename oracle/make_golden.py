@@ -206,6 +206,48 @@ def variant_cases():
          a=a, b=b, c=c0, d=c)
 
 
+GETT_CASES = (("abcd-aebf-dfce", dict(a=8, b=4, c=4, d=6, e=4, f=6)),
+              ("abc-acd-db", dict(a=8, b=16, c=4, d=8)),
+              ("ab-cad-dcb", dict(a=16, b=24, c=2, d=4)))
+
+
+def gett_cases():
+    """General contractions through the reference's own StridedPermutation layouts
+    (layouts.py:435-506), wired like its build_tc_config (api.py:259-290) but for any
+    TCCG spec 'D-A-B': M = A-free indices in D order, N = B-free in D order, K = contracted
+    indices in A order."""
+    rng = np.random.default_rng(9)
+    L = tk.layouts
+    for spec, ext in GETT_CASES:
+        d_idx, a_idx, b_idx = spec.split("-")
+        m_idx = [i for i in d_idx if i in a_idx]
+        n_idx = [i for i in d_idx if i in b_idx]
+        k_idx = [i for i in a_idx if i in b_idx]
+        vol = lambda idx: int(np.prod([ext[i] for i in idx]))
+        m, n, k = vol(m_idx), vol(n_idx), vol(k_idx)
+        grp = lambda idx: tuple((i, ext[i]) for i in idx)
+        dt = np.dtype(np.float32)
+        base = tk.build_dense_config(m, n, k, dt, operator_shape=(8, 8, 8))
+        cfg = dataclasses.replace(
+            base,
+            global_a_layout=L.StridedPermutation(dt, ("M", "K"), (m, k), dim_map={"M": grp(m_idx), "K": grp(k_idx)},
+                                                 storage_order=tuple(a_idx)),
+            global_b_layout=L.StridedPermutation(dt, ("K", "N"), (k, n), dim_map={"K": grp(k_idx), "N": grp(n_idx)},
+                                                 storage_order=tuple(b_idx)),
+            global_c_layout=L.Zero(dt, ("M", "N"), (m, n)),
+            global_d_layout=L.StridedPermutation(dt, ("M", "N"), (m, n), dim_map={"M": grp(m_idx), "N": grp(n_idx)},
+                                                 storage_order=tuple(d_idx)))
+        a = np.asfortranarray(rng.standard_normal([ext[i] for i in a_idx]).astype(np.float32))
+        b = np.asfortranarray(rng.standard_normal([ext[i] for i in b_idx]).astype(np.float32))
+        d = np.zeros(m * n, np.float32)
+        cnt = tk.matmul(cfg, a.ravel(order="F"), b.ravel(order="F"), np.zeros(0, np.float32), d)
+        res = tk.kernel.resolve_config(cfg)
+        save("gett_" + spec.replace("-", "_"), {"spec": spec, "sizes": ext,
+                                                "block_tile": list(res.params.block_tile),
+                                                "counters": counters_dict(cnt)},
+             a=a, b=b, d=d.reshape([ext[i] for i in d_idx], order="F"))
+
+
 def host_logic_cases():
     """Resolved tilings and counters (no element data) for the planner/counter tests."""
     cases = []
@@ -233,9 +275,7 @@ def host_logic_cases():
 
 if __name__ == "__main__":
     print("reference lane:", tk.active_lane())
-    dense_cases()
-    fused_cases()
-    pair_cases()
-    variant_cases()
-    host_logic_cases()
+    which = sys.argv[1:] or ["dense", "fused", "pair", "variant", "gett", "host_logic"]
+    for name in which:
+        globals()[f"{name}_cases"]()
     print("wrote", sorted(os.listdir(OUT)))

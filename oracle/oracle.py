@@ -169,6 +169,37 @@ def tc_reference(a, b, threads=None):
     return dmn.reshape(nb, na, nc, order="F").transpose(1, 0, 2)
 
 
+def gett_indices(spec):
+    """M / N / K index groups of a TCCG spec 'D-A-B' (the wiring of oracle/make_golden.py
+    gett_cases and paper_2009_12263_b200.build_gett_config)."""
+    d_idx, a_idx, b_idx = spec.split("-")
+    return (d_idx, a_idx, b_idx, [i for i in d_idx if i in a_idx], [i for i in d_idx if i in b_idx],
+            [i for i in a_idx if i in b_idx])
+
+
+def gett_matrices(spec, a, b):
+    """The GEMM view (A as M x K, B as K x N, column-major digits) of a contraction."""
+    d_idx, a_idx, b_idx, m_idx, n_idx, k_idx = gett_indices(spec)
+    ext = dict(zip(a_idx, a.shape))
+    ext.update(zip(b_idx, b.shape))
+    vol = lambda idx: int(np.prod([ext[i] for i in idx]))
+    amk = np.asarray(a).transpose([a_idx.index(i) for i in m_idx + k_idx]) \
+        .reshape(vol(m_idx), vol(k_idx), order="F")
+    bkn = np.asarray(b).transpose([b_idx.index(i) for i in k_idx + n_idx]) \
+        .reshape(vol(k_idx), vol(n_idx), order="F")
+    return np.asfortranarray(amk), np.asfortranarray(bkn), ext
+
+
+def gett_reference(spec, a, b, threads=None):
+    """D = A . B for a TCCG spec via the real oracle over the GEMM view (k ascending in the
+    K-digit order, f32 multiply-then-add: the reference's generic path, layouts.py:435-506)."""
+    d_idx, a_idx, b_idx, m_idx, n_idx, k_idx = gett_indices(spec)
+    amk, bkn, ext = gett_matrices(spec, np.asarray(a, np.float32), np.asarray(b, np.float32))
+    dmn = gemm_real(amk, bkn, None, threads=threads)
+    d = dmn.reshape([ext[i] for i in m_idx + n_idx], order="F")
+    return d.transpose([(m_idx + n_idx).index(i) for i in d_idx])
+
+
 # ---- exact references and tolerance -----------------------------------------------------
 
 def exact_gemm(a, b, c=None, alpha=1.0, beta=0.0):

@@ -387,6 +387,108 @@ def contract(a, b, *, worker_threads=1, block_tile=None, **run_kwargs):
     return d.reshape((na, nb, nc), order="F"), counters
 
 
+# ---- general tensor contractions (GETT) ----------------------------------------------------
+
+def _parse_gett(spec):
+    try:
+        d_idx, a_idx, b_idx = spec.replace(" ", "").split("-")
+    except ValueError:
+        raise ConfigError(f"GETT spec {spec!r} must read 'D-A-B', e.g. 'abc-bda-dc'") from None
+    for name, idx in (("D", d_idx), ("A", a_idx), ("B", b_idx)):
+        if len(set(idx)) != len(idx):
+            raise ConfigError(f"GETT spec {spec!r}: repeated index in {name}")
+    m_idx = tuple(i for i in d_idx if i in a_idx and i not in b_idx)
+    n_idx = tuple(i for i in d_idx if i in b_idx and i not in a_idx)
+    k_idx = tuple(i for i in a_idx if i in b_idx and i not in d_idx)
+    if set(d_idx) != set(m_idx) | set(n_idx) or set(a_idx) != set(m_idx) | set(k_idx) or \
+            set(b_idx) != set(n_idx) | set(k_idx):
+        raise ConfigError(f"GETT spec {spec!r}: every index must be free in exactly one operand "
+                          "and D, or contracted between A and B (no batch / trace indices)")
+    if not (m_idx and n_idx and k_idx):
+        raise ConfigError(f"GETT spec {spec!r}: needs free indices in A and B and a contraction")
+    if max(len(m_idx), len(n_idx), len(k_idx)) > _lib.MAX_DIGITS:
+        raise ConfigError(f"GETT spec {spec!r}: at most {_lib.MAX_DIGITS} indices per GEMM dimension")
+    return d_idx, a_idx, b_idx, m_idx, n_idx, k_idx
+
+
+def build_gett_config(spec, sizes, dtype=np.float32, *, operator_shape=None,
+                      worker_threads=1) -> KernelConfig:
+    """A general tensor contraction D = A . B as a GEMM with fused transpositions (GETT).
+
+    ``spec`` is TCCG notation ``"D-A-B"`` over single-letter indices, each tensor listed in
+    storage order (first index fastest, column-major like every layout here), e.g.
+    ``"abc-bda-dc"`` (the case ``build_tc_config`` wires) or ``"abcd-aebf-dfce"``.  Free
+    indices of A form M (ordered as in D), free indices of B form N (as in D), contracted
+    indices form K (as in A); each operand is a ``StridedPermutation`` over its own storage
+    order, C is Zero.  This generalises the reference's single contraction
+    (``api.py:259-312``) to the StridedPermutation layouts it defines (``layouts.py:435-506``);
+    on the tcgen05 lane non-TMA operands are gathered once into dense workspaces and D is
+    scattered by the epilogue's digit maps.
+    """
+    d_idx, a_idx, b_idx, m_idx, n_idx, k_idx = _parse_gett(spec)
+    missing = [i for i in set(d_idx + a_idx + b_idx) if i not in sizes]
+    if missing:
+        raise ConfigError(f"GETT sizes missing {sorted(missing)}")
+    ext = {i: int(sizes[i]) for i in set(d_idx + a_idx + b_idx)}
+    dtype = np.dtype(dtype)
+    acc = accumulator_dtype(dtype)
+    vol = lambda idx: int(np.prod([ext[i] for i in idx]))
+    m, n, k = vol(m_idx), vol(n_idx), vol(k_idx)
+    group = lambda idx: tuple((i, ext[i]) for i in idx)
+    layout_a = StridedPermutation(dtype, ("M", "K"), (m, k),
+                                  dim_map={"M": group(m_idx), "K": group(k_idx)},
+                                  storage_order=tuple(a_idx))
+    layout_b = StridedPermutation(dtype, ("K", "N"), (k, n),
+                                  dim_map={"K": group(k_idx), "N": group(n_idx)},
+                                  storage_order=tuple(b_idx))
+    layout_d = StridedPermutation(acc, ("M", "N"), (m, n),
+                                  dim_map={"M": group(m_idx), "N": group(n_idx)},
+                                  storage_order=tuple(d_idx))
+    shape = OperatorShape(*(operator_shape or _tc_operator_shape(m, n, k)))
+    return KernelConfig(
+        params=Params(gemm_shape=(m, n, k), operator_shape=(shape.m, shape.n, shape.k),
+                      worker_threads=worker_threads),
+        operator=_operator_for(dtype, shape, False),
+        global_a_layout=layout_a, global_b_layout=layout_b,
+        global_c_layout=Zero(acc, ("M", "N"), (m, n)), global_d_layout=layout_d,
+        shared_a_layout=col_major(dtype), shared_b_layout=col_major(dtype),
+        shared_c_layout=col_major(acc), shared_d_layout=col_major(acc),
+    )
+
+
+def gett(spec, a, b, **run_kwargs):
+    """Contract ``a`` and ``b`` per ``spec`` (see ``build_gett_config``); arrays are indexed in
+    the order their spec letters are written.  numpy in -> numpy D; torch CUDA tensors stay on
+    the device.  Returns (D, counters)."""
+    d_idx, a_idx, b_idx, *_ = _parse_gett(spec)
+    sizes = dict(zip(a_idx, a.shape))
+    sizes.update(zip(b_idx, b.shape))
+    for i, e in list(zip(a_idx, a.shape)) + list(zip(b_idx, b.shape)):
+        if sizes[i] != e:
+            raise ConfigError(f"index {i!r} has inconsistent extents")
+    d_shape = tuple(sizes[i] for i in d_idx)
+    if _is_torch(a):
+        import torch
+
+        dt = dtypes.from_torch(a.dtype)
+        cfg = build_gett_config(spec, sizes, dt)
+        accd = dtypes.torch_scalar(accumulator_dtype(dt))
+        d = torch.zeros(int(np.prod(d_shape)), dtype=accd, device=a.device)
+        fa = a.permute(*reversed(range(a.dim()))).reshape(-1)  # column-major flattening
+        fb = b.permute(*reversed(range(b.dim()))).reshape(-1)
+        counters = matmul(cfg, fa, fb, torch.empty(0, dtype=accd, device=a.device), d,
+                          **run_kwargs)
+        return d.reshape(tuple(reversed(d_shape))).permute(*reversed(range(len(d_shape)))), counters
+    a = np.asfortranarray(a)
+    b = np.asfortranarray(b)
+    cfg = build_gett_config(spec, sizes, a.dtype)
+    accd = accumulator_dtype(a.dtype)
+    d = np.zeros(int(np.prod(d_shape)), dtype=accd)
+    counters = matmul(cfg, a.ravel(order="F"), b.ravel(order="F"), np.zeros(0, accd), d,
+                      **run_kwargs)
+    return d.reshape(d_shape, order="F"), counters
+
+
 # ---- C-compatible export ------------------------------------------------------------------
 
 TAG_F32, TAG_F64, TAG_C64, TAG_C128, TAG_DUAL32, TAG_DUAL64 = range(6)

@@ -169,6 +169,32 @@ bool tma_operand(const TkLayout& L, int& mn_major_dim0, int64_t& pitch) {
   return true;
 }
 
+// A half-precision strided operand the TMA cannot read directly (multi-digit permutations,
+// non-unit innermost strides, non-bijective interleaved pairs) is gathered once into a dense
+// column-major workspace by pack_half_kernel and then takes the normal tensor-core path.
+bool pack_needed(const TkLayout& L) {
+  int mn;
+  int64_t pitch;
+  return L.kind == TK_LAYOUT_STRIDED && is_half(L.scalar) && !tma_operand(L, mn, pitch);
+}
+
+// rewrite a layout as the dense column-major rows x cols operand pack_half_kernel produces
+void dense_operand(TkLayout& L, int64_t rows, int64_t cols) {
+  const int pair = L.pair ? TK_PAIR_SPLIT : 0;
+  const int scalar = L.scalar;
+  memset(&L, 0, sizeof(L));
+  L.kind = TK_LAYOUT_STRIDED;
+  L.pair = pair;
+  L.scalar = scalar;
+  L.ndigits[0] = L.ndigits[1] = 1;
+  L.ext[0][0] = rows;
+  L.ext[1][0] = cols;
+  L.stride[0][0] = 1;
+  L.stride[1][0] = rows;
+  L.plane_stride = pair ? rows * cols : 0;
+  L.size = rows * cols * (pair ? 2 : 1);
+}
+
 // GETT-as-GEMM (tensor contraction, reference api.py:259-290): A's M index has two digits
 // (e0, s0), (e1, s1) and D's M digits are the same extents with the order swapped into a
 // dense run (t1 == 1, t0 == e1).  Rewrite to a plain column-major GEMM over m' = m1 + e1*m0:
@@ -215,10 +241,11 @@ bool tc_lane_ok(const TkGemmPlan* p, std::string& why) {
   int64_t pitch;
   if (p->a.kind == TK_LAYOUT_DIAGONAL) {
     if (p->op != TK_OP_REAL || p->t_a.n) return no("Diagonal A only with real op, identity g2s_a");
-  } else if (!tma_operand(p->a, mn, pitch)) {
-    return no("A layout is not TMA-compatible");
+  } else if (p->a.kind != TK_LAYOUT_STRIDED) {
+    return no("A layout is neither strided nor diagonal");
+  } else if (!tma_operand(p->a, mn, pitch) && (p->m * p->k * 2 * 2 > (int64_t(1) << 40))) {
+    return no("A too large to pack");
   }
-  if (!tma_operand(p->b, mn, pitch)) return no("B layout is not TMA-compatible");
   if (p->c.kind != TK_LAYOUT_ZERO && p->c.scalar != TK_F32) return no("C must be f32");
   if (p->d.scalar != TK_F32) return no("D must be f32");
   if (p->c.kind == TK_LAYOUT_DIAGONAL) return no("Diagonal C unsupported on tcgen05 lane");
@@ -244,7 +271,8 @@ int choose_lane(const TkGemmPlan* p, std::string* why_out = nullptr) {
 
 // ------------------------------------------------------------------ workspace plan
 struct Workspace {
-  int64_t a_planes = -1, b_planes = -1, rowsum = -1, colsum = -1, a_perm = -1, total = 0;
+  int64_t a_planes = -1, b_planes = -1, rowsum = -1, colsum = -1, a_perm = -1, a_pack = -1, b_pack = -1,
+          total = 0;
 };
 
 int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
@@ -259,6 +287,18 @@ Workspace plan_workspace(const TkGemmPlan* p0, int lane) {
     w.total += align256(p0->m * p0->k * 2);
     p = &rewritten;
   }
+  TkGemmPlan packed = *p;
+  if (pack_needed(p->a)) {
+    w.a_pack = w.total;
+    w.total += align256(p->m * p->k * 2 * (p->a.pair ? 2 : 1));
+    dense_operand(packed.a, p->m, p->k);
+  }
+  if (pack_needed(p->b)) {
+    w.b_pack = w.total;
+    w.total += align256(p->k * p->n * 2 * (p->b.pair ? 2 : 1));
+    dense_operand(packed.b, p->k, p->n);
+  }
+  p = &packed;
   if (p->a.kind == TK_LAYOUT_STRIDED && p->a.pair == TK_PAIR_INTERLEAVED) {
     w.a_planes = w.total;
     w.total += align256(p->m * p->k * 2 * 2);
@@ -556,6 +596,80 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
     a = at;
     p = &rewritten;
   }
+  TkGemmPlan packed;
+  if (w.a_pack >= 0 || w.b_pack >= 0) {
+    packed = *p;
+    auto pack = [&](const TkLayout& L, const void* src, uint16_t* dst, int64_t rows, int64_t cols) -> int {
+      tk::PackDesc pd;
+      memset(&pd, 0, sizeof(pd));
+      int64_t q = 1;
+      for (int d = 0; d < 2; ++d) {
+        if (d == 1) q = rows;
+        for (int t = 0; t < L.ndigits[d]; ++t) {
+          pd.ext[pd.n] = L.ext[d][t];
+          pd.ss[pd.n] = L.stride[d][t];
+          pd.ds[pd.n] = q;
+          q *= L.ext[d][t];
+          ++pd.n;
+        }
+      }
+      for (int t = 0; t < pd.n; ++t)
+        if (pd.ss[t] < pd.ss[pd.fs] || (pd.ss[t] == pd.ss[pd.fs] && pd.ext[t] > pd.ext[pd.fs])) pd.fs = t;
+      pd.fd = 0;  // first row digit: destination stride 1
+      if (pd.fd == pd.fs) {
+        pd.fd = -1;
+        for (int t = 0; t < pd.n; ++t)
+          if (t != pd.fs && (pd.fd < 0 || pd.ds[t] < pd.ds[pd.fd])) pd.fd = t;
+        if (pd.fd < 0) {  // single digit: pad with a unit digit
+          pd.ext[pd.n] = 1;
+          pd.ss[pd.n] = pd.ds[pd.n] = 0;
+          pd.fd = pd.n++;
+        }
+      }
+      // 16-byte vectors: unit stride along the vector digit, extents and every other stride
+      // multiples of 8 elements, 16-byte aligned base (interleaved pairs read scalar-wise)
+      auto all8 = [&](const int64_t* st, int skip) {
+        for (int t = 0; t < pd.n; ++t)
+          if (t != skip && (st[t] % 8) != 0) return false;
+        return true;
+      };
+      const int64_t pl_off = L.pair == TK_PAIR_SPLIT ? L.plane_stride : 0;
+      pd.vec_rd = L.pair != TK_PAIR_INTERLEAVED && pd.ss[pd.fs] == 1 && pd.ext[pd.fs] % 8 == 0 &&
+                  all8(pd.ss, pd.fs) && pl_off % 8 == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+      pd.wr_x = pd.ds[pd.fs] < pd.ds[pd.fd];
+      const int wd = pd.wr_x ? pd.fs : pd.fd;
+      pd.vec_wr = pd.ds[wd] == 1 && pd.ext[wd] % 8 == 0 && all8(pd.ds, wd) &&
+                  (rows * cols) % 8 == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+      pd.tiles_s = (pd.ext[pd.fs] + 63) / 64;
+      pd.tiles_d = (pd.ext[pd.fd] + 63) / 64;
+      pd.outer = 1;
+      for (int t = 0; t < pd.n; ++t)
+        if (t != pd.fs && t != pd.fd) pd.outer *= pd.ext[t];
+      const int64_t blocks = pd.tiles_s * pd.tiles_d * pd.outer;
+      const unsigned grid = unsigned(std::min<int64_t>(blocks, 64 * sm_count()));
+      for (int pl = 0; pl < (L.pair ? 2 : 1); ++pl) {
+        tk::pack_half_kernel<<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(src), dst + pl * rows * cols, pd,
+                                                  L.pair, L.plane_stride, pl);
+        TK_CUDA(cudaGetLastError());
+        ++g_launches;
+      }
+      return TK_OK;
+    };
+    int rc;
+    if (w.a_pack >= 0) {
+      uint16_t* dst = reinterpret_cast<uint16_t*>(ws + w.a_pack);
+      if ((rc = pack(p->a, a, dst, p->m, p->k))) return rc;
+      dense_operand(packed.a, p->m, p->k);
+      a = dst;
+    }
+    if (w.b_pack >= 0) {
+      uint16_t* dst = reinterpret_cast<uint16_t*>(ws + w.b_pack);
+      if ((rc = pack(p->b, b, dst, p->k, p->n))) return rc;
+      dense_operand(packed.b, p->k, p->n);
+      b = dst;
+    }
+    p = &packed;
+  }
   tk::TcParams prm;
   memset(&prm, 0, sizeof(prm));
   const int op = p->op;
@@ -704,8 +818,18 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
   prm.pol_ab = 1;  // A/B panels are re-read by neighbouring tiles: keep them in L2
   if (const char* g = getenv("TK_POLICY_AB")) prm.pol_ab = atoi(g);
   const bool pair = op != TK_OP_REAL;
-  bool dense = colmajor_dense(p->d, prm.ldd) &&
-               (p->c.kind == TK_LAYOUT_ZERO || colmajor_dense(p->c, prm.ldc)) &&
+  // real operator: C/D rows may follow any digit map (GETT outputs whose M indices are not
+  // one contiguous run) as long as columns are one strided digit -- the register epilogue
+  // then adds a per-thread row offset instead of i (rows stay coalesced inside a run)
+  auto rowmapped = [&](const TkLayout& L, int64_t& ld, int32_t& flag) {
+    if (colmajor_dense(L, ld)) return true;
+    if (op != TK_OP_REAL || L.kind != TK_LAYOUT_STRIDED || L.ndigits[1] != 1) return false;
+    ld = L.stride[1][0];
+    flag = 1;
+    return true;
+  };
+  bool dense = rowmapped(p->d, prm.ldd, prm.d_rmap) &&
+               (p->c.kind == TK_LAYOUT_ZERO || rowmapped(p->c, prm.ldc, prm.c_rmap)) &&
                decode_affine(p->t_c, pair, prm.c_mul, prm.c_add, prm.c_relu) &&
                decode_affine(p->t_r2s, pair, prm.r_mul, prm.r_add, prm.r_relu) &&
                decode_affine(p->t_s2g, pair, prm.s_mul, prm.s_add, prm.s_relu);
@@ -717,7 +841,8 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
   // streamed-C single-CTA kernel: HBM-bound shapes, and single-wave dense shapes too small
   // for the CTA pair (C prefetched by the loader warp while the mainloop runs)
   const bool single_wave = prm.num_tiles <= sm_count();
-  if (op == TK_OP_REAL && dense &&
+  const bool rmapped = prm.c_rmap || prm.d_rmap;
+  if (op == TK_OP_REAL && dense && !rmapped &&
       (ov == 3 || (ov == 0 && (prm.diag_a || prm.kb_total <= 4 || (single_wave && !pair_ok))))) {
     const bool cs = prm.c_zero || ((prm.ldc * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(c) & 15) == 0);
     if (cs) {
@@ -776,7 +901,7 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
       }
       if (getenv("TK_VERBOSE")) fprintf(stderr, "tk: pair kernel bni %d nsub %d tiles %d\n", bni, nsub, pp.num_tiles);
       // streamed C/D epilogue (TMA ring + bulk stores) when C/D are TMA-compatible
-      bool cs = dense && (prm.c_zero || ((prm.ldc * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(c) & 15) == 0)) &&
+      bool cs = dense && !rmapped && (prm.c_zero || ((prm.ldc * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(c) & 15) == 0)) &&
                 (prm.ldd * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(d) & 15) == 0;
       if (const char* e = getenv("TK_PAIR_CSTREAM")) cs = cs && atoi(e);
       if (cs) {
@@ -909,6 +1034,45 @@ bool aligned16(const void* x) { return (reinterpret_cast<uintptr_t>(x) & 15) == 
 }  // namespace
 
 // ====================================================================== C ABI
+namespace {
+// Canonical digit maps: unit digits dropped, and adjacent digits whose strides chain
+// (stride[t+1] == stride[t] * ext[t]) merged into one -- the same element map
+// (d0*s0 + d1*s0*e0 == (d0 + e0*d1)*s0), but many GETT operands become plain strided
+// matrices the TMA reads directly instead of needing a gather pass.
+void normalize_layout(TkLayout& L) {
+  if (L.kind != TK_LAYOUT_STRIDED) return;
+  for (int d = 0; d < 2; ++d) {
+    int64_t e[3], st[3];
+    int n = 0;
+    for (int t = 0; t < L.ndigits[d]; ++t) {
+      if (L.ext[d][t] == 1 && L.ndigits[d] > 1) continue;
+      if (n > 0 && L.stride[d][t] == st[n - 1] * e[n - 1]) {
+        e[n - 1] *= L.ext[d][t];
+        continue;
+      }
+      e[n] = L.ext[d][t];
+      st[n] = L.stride[d][t];
+      ++n;
+    }
+    if (n == 0) { e[0] = 1; st[0] = 1; n = 1; }
+    for (int t = 0; t < 3; ++t) {
+      L.ext[d][t] = t < n ? e[t] : 0;
+      L.stride[d][t] = t < n ? st[t] : 0;
+    }
+    L.ndigits[d] = n;
+  }
+}
+
+const TkGemmPlan* normalized(const TkGemmPlan* p, TkGemmPlan& out) {
+  out = *p;
+  normalize_layout(out.a);
+  normalize_layout(out.b);
+  normalize_layout(out.c);
+  normalize_layout(out.d);
+  return &out;
+}
+}  // namespace
+
 extern "C" {
 
 int tk_abi_version(void) { return TK_ABI_VERSION; }
@@ -963,8 +1127,10 @@ double tk_debug_pair_mhz(void) {
   return double(v[0]) * 1e3 / double(v[1]);
 }
 
-int tk_plan_lane(const TkGemmPlan* plan) {
-  if (check_plan(plan)) return -1;
+int tk_plan_lane(const TkGemmPlan* plan0) {
+  if (check_plan(plan0)) return -1;
+  TkGemmPlan norm;
+  const TkGemmPlan* plan = normalized(plan0, norm);
   std::string why;
   int lane = choose_lane(plan, &why);
   if (lane < 0) {
@@ -974,19 +1140,23 @@ int tk_plan_lane(const TkGemmPlan* plan) {
   return lane;
 }
 
-int64_t tk_workspace_bytes(const TkGemmPlan* plan) {
-  if (check_plan(plan)) return -1;
+int64_t tk_workspace_bytes(const TkGemmPlan* plan0) {
+  if (check_plan(plan0)) return -1;
+  TkGemmPlan norm;
+  const TkGemmPlan* plan = normalized(plan0, norm);
   int lane = choose_lane(plan);
   if (lane < 0) return -1;
   return plan_workspace(plan, lane).total;
 }
 
-int tk_gemm(const TkGemmPlan* plan, const void* a, const void* b, const void* c, void* d, const void* bias,
+int tk_gemm(const TkGemmPlan* plan0, const void* a, const void* b, const void* c, void* d, const void* bias,
             const uint8_t* kmask, void* workspace, int64_t workspace_bytes, void* stream) {
   g_err.clear();
   g_launches = 0;
-  int rc = check_plan(plan);
+  int rc = check_plan(plan0);
   if (rc) return rc;
+  TkGemmPlan norm;
+  const TkGemmPlan* plan = normalized(plan0, norm);
   std::string why;
   int lane = choose_lane(plan, &why);
   if (lane < 0) return fail(TK_ERR_CONFIG, "tcgen05 lane requested but not applicable: %s", why.c_str());

@@ -101,3 +101,103 @@ __global__ void swap_digits_kernel(const uint16_t* __restrict__ a, uint16_t* __r
   }
 }
 }  // namespace tk
+
+namespace tk {
+
+// Gather one plane of a half-precision operand stored under an arbitrary digit map (the
+// StridedPermutation / GETT layouts, reference layouts.py:435-506) into a dense column-major
+// rows x cols buffer, so any fused-transposition operand reaches the tensor cores through a
+// plain 2-D TMA map.  The operand is viewed as an n-digit tensor (<= 6 digits: each digit has
+// an extent, a source stride and a destination stride).  A block moves 64 x 64 tiles spanning
+// digit X (the source's fastest) and digit Y (the destination's fastest, or its next digit
+// when that is X) through shared memory: the read phase runs along X, the write phase along
+// whichever tile digit is fastest in the destination, each with 16-byte vectors when that
+// digit has unit stride and 8-element alignment; the remaining digits index tiles by block.
+// Element offsets count pair elements: interleaved pairs sit at 2*off + plane, split planes
+// at off + plane * plane_stride (scalars).
+struct PackDesc {
+  int32_t n, fs, fd, vec_rd;   // X = fs, Y = fd; vec_rd: 16-byte reads along X
+  int32_t wr_x, vec_wr, pad0, pad1;  // wr_x: destination-fastest tile digit is X; vec_wr: 16-byte writes
+  int64_t ext[6], ss[6], ds[6];
+  int64_t tiles_s, tiles_d, outer;  // tiles along X, along Y, outer digit combinations
+};
+
+__global__ void __launch_bounds__(256) pack_half_kernel(const uint16_t* __restrict__ src, uint16_t* __restrict__ dst,
+                                                        const __grid_constant__ PackDesc pd, int pair,
+                                                        int64_t plane_stride, int plane) {
+  __shared__ __align__(16) uint16_t tile[64][72];  // [y][x]; 144-byte rows keep 16-byte alignment
+  const int64_t nblocks = pd.tiles_s * pd.tiles_d * pd.outer;
+  const int64_t sx = pd.ss[pd.fs], sy = pd.ss[pd.fd], dx = pd.ds[pd.fs], dy = pd.ds[pd.fd];
+  for (int64_t blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
+    int64_t q = blk;
+    const int64_t ts = q % pd.tiles_s;
+    q /= pd.tiles_s;
+    const int64_t td = q % pd.tiles_d;
+    q /= pd.tiles_d;
+    int64_t so = 0, dof = 0;
+    for (int t = 0; t < pd.n; ++t) {  // outer digits
+      if (t == pd.fs || t == pd.fd) continue;
+      const int64_t v = q % pd.ext[t];
+      q /= pd.ext[t];
+      so += v * pd.ss[t];
+      dof += v * pd.ds[t];
+    }
+    const int64_t x0 = ts * 64, y0 = td * 64;
+    const int64_t rx = pd.ext[pd.fs] - x0, ry = pd.ext[pd.fd] - y0;
+    const int nx = rx < 64 ? int(rx) : 64, ny = ry < 64 ? int(ry) : 64;
+    so += x0 * sx + y0 * sy;
+    dof += x0 * dx + y0 * dy;
+    __syncthreads();
+    if (pd.vec_rd) {  // 8 threads per 64-element row of X, 32 rows per pass
+      for (int idx = threadIdx.x; idx < 64 * 8; idx += blockDim.x) {
+        const int x = (idx & 7) * 8, y = idx >> 3;
+        if (y < ny && x < nx)
+          *reinterpret_cast<uint4*>(&tile[y][x]) =
+              *reinterpret_cast<const uint4*>(src + so + y * sy + x + int64_t(plane) * plane_stride);
+      }
+    } else {
+      for (int idx = threadIdx.x; idx < 64 * 64; idx += blockDim.x) {
+        const int x = idx & 63, y = idx >> 6;
+        if (x < nx && y < ny) {
+          const int64_t off = so + x * sx + y * sy;
+          tile[y][x] = src[pair == P_INTERLEAVED ? 2 * off + plane : off + int64_t(plane) * plane_stride];
+        }
+      }
+    }
+    __syncthreads();
+    if (pd.wr_x) {  // destination runs along X: rows of the tile are contiguous
+      if (pd.vec_wr) {
+        for (int idx = threadIdx.x; idx < 64 * 8; idx += blockDim.x) {
+          const int x = (idx & 7) * 8, y = idx >> 3;
+          if (y < ny && x < nx)
+            *reinterpret_cast<uint4*>(dst + dof + y * dy + x) = *reinterpret_cast<const uint4*>(&tile[y][x]);
+        }
+      } else {
+        for (int idx = threadIdx.x; idx < 64 * 64; idx += blockDim.x) {
+          const int x = idx & 63, y = idx >> 6;
+          if (x < nx && y < ny) dst[dof + x * dx + y * dy] = tile[y][x];
+        }
+      }
+    } else {  // destination runs along Y: transpose through shared memory
+      if (pd.vec_wr) {
+        for (int idx = threadIdx.x; idx < 64 * 8; idx += blockDim.x) {
+          const int y = (idx & 7) * 8, x = idx >> 3;
+          if (x < nx && y < ny) {
+            uint4 v;
+            uint16_t* h = reinterpret_cast<uint16_t*>(&v);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) h[e] = tile[y + e][x];
+            *reinterpret_cast<uint4*>(dst + dof + x * dx + y) = v;
+          }
+        }
+      } else {
+        for (int idx = threadIdx.x; idx < 64 * 64; idx += blockDim.x) {
+          const int y = idx & 63, x = idx >> 6;
+          if (x < nx && y < ny) dst[dof + x * dx + y * dy] = tile[y][x];
+        }
+      }
+    }
+  }
+}
+
+}  // namespace tk

@@ -94,6 +94,7 @@ struct TcParams {
   int32_t dbg_skip_epi, pol_ab;  // tuning/diagnostic knobs (TK_DBG_SKIP_EPI, TK_POLICY_AB)
   int32_t d_tma, mn3d;           // C-streaming epilogue: D via TMA; MN-major operands via 3-D maps (bit0 A, bit1 B)
   int32_t c_pf_kb, pad2;         // pair kernel: prefetch the tile's C into L2 this many k-blocks before its end
+  int32_t c_rmap, d_rmap;        // dense epilogue: C / D row offsets through c_map / d_map (GETT outputs)
 };
 
 __device__ __forceinline__ void tile_coords(const TcParams& p, int t, int& mb, int& nb) {
@@ -154,8 +155,10 @@ __device__ __forceinline__ void epilogue_dense(const TcParams& p, uint64_t* tful
   const bool row_ok = i < p.m;
   const bool has_c = !p.c_zero;
   if (OP == OP_REAL) {
-    const float* cp = reinterpret_cast<const float*>(p.c_ptr) + (row_ok ? i : 0);
-    float* dp = reinterpret_cast<float*>(p.d_ptr) + (row_ok ? i : 0);
+    const int64_t crow = !row_ok ? 0 : p.c_rmap ? map_dim(p.c_map, 0, i) : i;
+    const int64_t drow = !row_ok ? 0 : p.d_rmap ? map_dim(p.d_map, 0, i) : i;
+    const float* cp = reinterpret_cast<const float*>(p.c_ptr) + crow;
+    float* dp = reinterpret_cast<float*>(p.d_ptr) + drow;
     const float rterm = p.affine && row_ok ? (p.aff_r * (p.rowsum_a ? p.rowsum_a[i] : 0.f) + p.aff_k) : 0.f;
     const float bias_m = (p.bias_axis == 2 && row_ok) ? p.bias[i] : 0.f;
     float cv[32];

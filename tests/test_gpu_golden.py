@@ -137,6 +137,17 @@ def test_contract_bitwise(cuda, shape):
     assert dataclasses.asdict(cnt) == meta["counters"]
 
 
+@pytest.mark.parametrize("spec", ["abcd_aebf_dfce", "abc_acd_db", "ab_cad_dcb"])
+def test_gett_bitwise(cuda, spec):
+    """General contractions (f32: exact lane) against the reference's own outputs, with the
+    reference's counters and resolved tiling."""
+    meta, z = load(f"gett_{spec}")
+    d, cnt = \
+        tk.gett(meta["spec"], z["a"], z["b"])
+    assert np.array_equal(d, z["d"])
+    assert dataclasses.asdict(cnt) == meta["counters"]
+
+
 def test_alpha_zero_bitwise(cuda):
     meta, z = load("alpha_zero")
     m, n, k = meta["m"], meta["n"], meta["k"]

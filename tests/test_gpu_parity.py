@@ -283,6 +283,33 @@ def test_tensor_contraction_tcgen05(cuda, shape):
     assert counters.global_stores == na * nb * nc
 
 
+@pytest.mark.parametrize("spec,sizes", [
+    ("abcd-aebf-dfce", dict(a=32, b=8, c=16, d=24, e=16, f=24)),   # A, B gathered; D dense
+    ("abc-acd-db", dict(a=64, b=96, c=8, d=136)),                 # A gathered, B TMA, D dense
+    ("ab-cad-dcb", dict(a=160, b=200, c=4, d=36)),                # 2-digit K in both operands
+    ("bac-abd-dc", dict(a=24, b=16, c=72, d=200)),                # D scattered (generic epilogue)
+])
+@pytest.mark.parametrize("integer", [True, False])
+def test_gett_tcgen05(cuda, spec, sizes, integer):
+    """General GETT on the tensor cores: non-TMA operands are packed once into dense
+    workspaces (pack_half_kernel), D leaves through the epilogue's digit maps."""
+    rng = np.random.default_rng(13)
+    d_idx, a_idx, b_idx = spec.split("-")
+    a = _half(rng, [sizes[i] for i in a_idx], np.float16, integer)
+    b = _half(rng, [sizes[i] for i in b_idx], np.float16, integer)
+    d, counters = tk.gett(spec, torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda())
+    assert tk.last_run()["lane"] == "tcgen05", tk.last_run()
+    want = O.gett_reference(spec, _f32(a), _f32(b))
+    got = d.cpu().numpy()
+    assert got.shape == want.shape
+    k = int(np.prod([sizes[i] for i in a_idx if i in b_idx]))
+    if integer:
+        assert np.array_equal(got, want), float(np.abs(got - want).max())
+    else:
+        assert O.rel_err(got, want) <= O.tolerance(k), O.rel_err(got, want)
+    assert counters.global_stores == got.size
+
+
 @pytest.mark.parametrize("trans_a", [0, 1])
 def test_gemm_ex_raw_host_pipelined(cuda, trans_a):
     """Host-buffer tk_gemm_ex_raw above 2^30 MACs takes the 3-stream slab pipeline."""

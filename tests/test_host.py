@@ -456,3 +456,20 @@ def test_gemm_ex_cfunc_is_a_c_function_pointer():
     assert isinstance(fn, tk.GEMM_EX_CFUNC)
     assert ctypes.cast(fn, ctypes.c_void_p).value == \
         ctypes.cast(_lib.load().tk_gemm_ex_raw, ctypes.c_void_p).value
+
+
+def test_gett_config_wiring():
+    """build_gett_config: M = A-free indices in D order, N = B-free in D order, K = contracted
+    in A order; the reference's build_tc_config is the special case 'abc-bda-dc'."""
+    import paper_2009_12263_b200 as tk
+
+    cfg = tk.build_gett_config("abcd-aebf-dfce", dict(a=8, b=4, c=6, d=2, e=3, f=5), np.float16)
+    assert cfg.params.gemm_shape == (32, 12, 15)
+    assert cfg.global_a_layout.digits() == [[(8, 1), (4, 24)], [(3, 8), (5, 96)]]
+    tc = tk.build_gett_config("abc-bda-dc", dict(a=8, b=4, c=6, d=2), np.float32)
+    ref = tk.build_tc_config(8, 4, 6, 2, np.float32)
+    assert tc.params.gemm_shape == ref.params.gemm_shape
+    assert tc.global_a_layout.physical_size() == ref.global_a_layout.physical_size()
+    for bad in ("abc-bd", "abc-bda-dcc", "ab-abc-bc", "abe-bda-dc"):
+        with pytest.raises(tk.ConfigError):
+            tk.build_gett_config(bad, dict(a=2, b=2, c=2, d=2, e=2), np.float32)

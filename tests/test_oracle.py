@@ -88,6 +88,16 @@ def test_tensor_contraction_bitwise(shape):
     assert np.array_equal(O.tc_reference(z["a"], z["b"]), z["d"])
 
 
+GETT = ["abcd_aebf_dfce", "abc_acd_db", "ab_cad_dcb"]
+
+
+@pytest.mark.parametrize("spec", GETT)
+def test_general_contraction_bitwise(spec):
+    """General GETT (reference StridedPermutation layouts over any index permutation)."""
+    meta, z = load(f"gett_{spec}")
+    assert np.array_equal(O.gett_reference(meta["spec"], z["a"], z["b"]), z["d"])
+
+
 def test_alpha_zero_bitwise():
     meta, z = load("alpha_zero")
     m, n, k = meta["m"], meta["n"], meta["k"]

@@ -211,8 +211,20 @@ def contraction(na, nb, nc, nd):
            tk.last_run()["lane"])
 
 
+def gett_case(spec, sizes):
+    d_idx, a_idx, b_idx = spec.split("-")
+    cfg = tk.build_gett_config(spec, sizes, tk.FLOAT16)
+    m, n, k = cfg.params.gemm_shape
+    a = rnd(int(np.prod([sizes[i] for i in a_idx])), torch.float16)
+    b = rnd(int(np.prod([sizes[i] for i in b_idx])), torch.float16)
+    d = torch.empty(m * n, device=dev)
+    c = torch.empty(0, device=dev)
+    sec = timeit(run(cfg, a, b, c, d), reps=5, warm=2)
+    report(f"GETT {spec} M={m} N={n} K={k}", sec, 2.0 * m * n * k, "TFLOPS", tk.last_run()["lane"])
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["dense", "sweep", "fused", "pair", "diag", "skinny", "tc"]
+    which = sys.argv[1:] or ["dense", "sweep", "fused", "pair", "diag", "skinny", "tc", "gett"]
     if "dense" in which:
         dense(8192)
         dense(8192, dtype="bf16")
@@ -238,6 +250,11 @@ if __name__ == "__main__":
     if "skinny" in which:
         skinny(8192, 128)
         skinny(8192, 256)
+    if "gett" in which:
+        gett_case("abcd-aebf-dfce", dict(a=128, b=64, c=128, d=64, e=128, f=64))
+        gett_case("abcd-aebf-fdec", dict(a=128, b=64, c=128, d=64, e=128, f=64))
+        gett_case("abc-acd-db", dict(a=128, b=8192, c=64, d=8192))
+        gett_case("abc-bda-dc", dict(a=64, b=128, c=8192, d=8192))
     if "tc" in which:
         contraction(64, 32, 2048, 2048)
         contraction(64, 128, 8192, 8192)
