@@ -272,10 +272,16 @@ int choose_lane(const TkGemmPlan* p, std::string* why_out = nullptr) {
 // ------------------------------------------------------------------ workspace plan
 struct Workspace {
   int64_t a_planes = -1, b_planes = -1, rowsum = -1, colsum = -1, a_perm = -1, a_pack = -1, b_pack = -1,
-          total = 0;
+          splitk = -1, total = 0;
 };
 
 int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
+
+struct SplitPlan;
+SplitPlan split_plan(int64_t tiles, int clusters, int kb_total, int bnp);
+int choose_pair_bni(int64_t m, int64_t n, bool b_mn_major, int clusters);
+int pair_clusters();
+int64_t split_ws_bytes(int64_t m, int64_t n, int64_t k, const TkLayout& b);
 
 Workspace plan_workspace(const TkGemmPlan* p0, int lane) {
   Workspace w;
@@ -310,6 +316,10 @@ Workspace plan_workspace(const TkGemmPlan* p0, int lane) {
   double aa, ba, ab, bb;
   affine_of(p->t_a, aa, ba);
   affine_of(p->t_b, ab, bb);
+  if (p->op == TK_OP_REAL && p->a.kind != TK_LAYOUT_DIAGONAL) {  // split-K partials (pair kernel)
+    const int64_t sb = split_ws_bytes(p->m, p->n, p->k, p->b);
+    if (sb > 0) { w.splitk = w.total; w.total += align256(sb); }
+  }
   if (p->op == TK_OP_REAL && bb != 0.0) { w.rowsum = w.total; w.total += align256(p->m * 4); }
   if (p->op == TK_OP_REAL && ba != 0.0) { w.colsum = w.total; w.total += align256(p->n * 4); }
   return w;
@@ -456,10 +466,15 @@ int launch_tc_pair(const tk::TcParams& prm, cudaStream_t s) {
     }
     if (getenv("TK_VERBOSE")) fprintf(stderr, "tk: pair kernel max active clusters %d\n", max_clusters);
   }
-  int clusters = std::min(prm.num_tiles, max_clusters);
+  tk::TcParams run = prm;
+  if (run.sk_parts > 1 && max_clusters != pair_clusters()) {  // split parts must all be co-resident
+    run.num_units = run.sk_first = run.num_tiles;
+    run.sk_parts = 1;
+  }
+  int clusters = std::min(run.num_units, max_clusters);
   if (const char* e = getenv("TK_PAIR_GRID")) clusters = std::max(1, std::min(clusters, atoi(e)));
   const int grid = 2 * clusters;
-  kern<<<grid, tk::TC_THREADS, SMEM, s>>>(prm);
+  kern<<<grid, tk::TC_THREADS, SMEM, s>>>(run);
   TK_CUDA(cudaGetLastError());
   ++g_launches;
   return TK_OK;
@@ -471,6 +486,41 @@ int launch_tc_pair_bni(const tk::TcParams& prm, int bni, cudaStream_t s) {
   if (bni == 64) return launch_tc_pair<DENSE, CSTREAM, 1, 64>(prm, s);
   if (bni == 128) return launch_tc_pair<DENSE, CSTREAM, 1, 128>(prm, s);
   return launch_tc_pair<DENSE, CSTREAM, 1, 256>(prm, s);
+}
+
+// Split-K of a poorly filled last wave: with T tiles over P clusters, W = T / P full waves and
+// R = T % P left over, the R tiles are cut into S K-parts (S <= 4, R*S <= P, >= 64 k-blocks per
+// part) when the last wave would otherwise leave at least half of the clusters idle.
+struct SplitPlan {
+  int first = 0, parts = 1, tiles = 0;
+  int64_t ws_bytes = 0;
+};
+SplitPlan split_plan(int64_t tiles, int clusters, int kb_total, int bnp) {
+  SplitPlan sp;
+  sp.first = int(tiles);
+  if (const char* e = getenv("TK_SPLITK"))
+    if (!atoi(e)) return sp;
+  const int64_t r = tiles % clusters;
+  if (r == 0 || r > clusters / 2) return sp;
+  // >= 64 block-K steps per part: below that the partial hand-off costs what the wave gains
+  // (measured: 4096^3 -2 %, 4096x4096x16384 +6.5 %, 1536x4096x16384 +13 %)
+  int parts = int(std::min<int64_t>(std::min<int64_t>(4, clusters / r), kb_total / 64));
+  if (const char* e = getenv("TK_SPLITK_S")) parts = std::max(1, std::min(parts, atoi(e)));
+  if (parts < 2) return sp;
+  sp.first = int(tiles - r);
+  sp.parts = parts;
+  sp.tiles = int(r);
+  sp.ws_bytes = r * (parts - 1) * 2 * 128 * int64_t(bnp) * 4 + 256 + align256(r * 4);
+  return sp;
+}
+
+int64_t split_ws_bytes(int64_t m, int64_t n, int64_t k, const TkLayout& b) {
+  int mn;
+  int64_t pitch;
+  const bool b_mn = tma_operand(b, mn, pitch) ? !mn : false;
+  const int bni = choose_pair_bni(m, n, b_mn, pair_clusters());
+  const int64_t tiles = ((m + 255) / 256) * ((n + bni - 1) / bni);
+  return split_plan(tiles, pair_clusters(), int((k + 63) / 64), bni).ws_bytes;
 }
 
 // Pair-tile width for the real operator: the instruction N (256 / 128 / 64) minimising
@@ -810,13 +860,20 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
   prm.num_nb = int((p->n + BN - 1) / BN);
   prm.num_tiles = prm.num_mb * prm.num_nb;
   prm.kb_total = int((p->k + tk::TC_BK - 1) / tk::TC_BK);
+  prm.num_units = prm.num_tiles;  // pair kernel schedule: whole tiles unless split below
+  prm.sk_first = prm.num_tiles;
+  prm.sk_parts = 1;
   prm.group_m = 8;
   if (const char* g = getenv("TK_GROUP_M")) prm.group_m = std::max(1, atoi(g));
   if (const char* g = getenv("TK_DBG_SKIP_EPI")) prm.dbg_skip_epi = atoi(g);
   if (const char* g = getenv("TK_DBG_NO_LOAD")) prm.dbg_skip_epi |= atoi(g) ? 2 : 0;
+  if (const char* g = getenv("TK_DBG_CTA")) prm.dbg_cta = atoi(g);
   if (const char* g = getenv("TK_DBG_NO_MMA")) prm.dbg_skip_epi |= atoi(g) ? 4 : 0;
   prm.pol_ab = 1;  // A/B panels are re-read by neighbouring tiles: keep them in L2
   if (const char* g = getenv("TK_POLICY_AB")) prm.pol_ab = atoi(g);
+  prm.pol_a = prm.pol_b = prm.pol_ab ? 1 : 0;
+  if (const char* g = getenv("TK_POL_A")) prm.pol_a = atoi(g);
+  if (const char* g = getenv("TK_POL_B")) prm.pol_b = atoi(g);
   const bool pair = op != TK_OP_REAL;
   // real operator: C/D rows may follow any digit map (GETT outputs whose M indices are not
   // one contiguous run) as long as columns are one strided digit -- the register epilogue
@@ -882,6 +939,19 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
       pp.num_mb = int((p->m + 255) / 256);
       pp.num_nb = int((p->n + bni * nsub - 1) / (bni * nsub));
       pp.num_tiles = pp.num_mb * pp.num_nb;
+      pp.num_units = pp.sk_first = pp.num_tiles;
+      pp.sk_parts = 1;
+      if (nsub == 1 && dense && w.splitk >= 0 && !getenv("TK_PAIR_GRID")) {
+        const SplitPlan sp = split_plan(pp.num_tiles, pair_clusters(), pp.kb_total, bni);
+        if (sp.parts > 1 && sp.ws_bytes <= split_ws_bytes(p->m, p->n, p->k, p->b)) {
+          pp.sk_first = sp.first;
+          pp.sk_parts = sp.parts;
+          pp.num_units = sp.first + sp.tiles * sp.parts;
+          pp.sk_ws = reinterpret_cast<float*>(ws + w.splitk);
+          pp.sk_flags = reinterpret_cast<int32_t*>(ws + w.splitk + (sp.ws_bytes - align256(sp.tiles * 4)));
+          TK_CUDA(cudaMemsetAsync(pp.sk_flags, 0, sp.tiles * 4, s));
+        }
+      }
       // per-CTA halves: A box 128 rows / B box bni/2 columns
       tma_operand(p->a, mn, pitch);
       pp.mn3d = 0;

@@ -95,6 +95,13 @@ struct TcParams {
   int32_t d_tma, mn3d;           // C-streaming epilogue: D via TMA; MN-major operands via 3-D maps (bit0 A, bit1 B)
   int32_t c_pf_kb, pad2;         // pair kernel: prefetch the tile's C into L2 this many k-blocks before its end
   int32_t c_rmap, d_rmap;        // dense epilogue: C / D row offsets through c_map / d_map (GETT outputs)
+  int32_t pol_a, pol_b;          // pair kernel L2 policies for A / B loads: 0 normal, 1 evict_last, 2 evict_first
+  // split-K of a poorly filled last wave (pair kernel): units [0, sk_first) are whole tiles,
+  // units sk_first + r*sk_parts + s are K-part s of tile sk_first + r; parts < sk_parts-1
+  // leave raw FP32 partials in sk_ws and count down sk_flags[r], the last part reduces them.
+  int32_t num_units, sk_first, sk_parts, dbg_cta;
+  float* sk_ws;
+  int32_t* sk_flags;
 };
 
 __device__ __forceinline__ void tile_coords(const TcParams& p, int t, int& mb, int& nb) {
@@ -142,6 +149,28 @@ __device__ __forceinline__ void write_diag_tile(uint8_t* dst, const HT* diag, in
 }
 
 
+// Split-K partials to fold into the accumulator before the epilogue: this thread's row of the
+// first partial block (column stride 128), n blocks `pstride` floats apart, summed in order.
+struct SkIn {
+  const float* p;
+  int n;
+  int64_t pstride;
+};
+// sum of the partials of 32 consecutive columns starting at `col` (all loads issued before
+// any use, so their latency overlaps the TMEM load instead of stalling element by element)
+__device__ __forceinline__ void sk_gather(const SkIn& sk, int col, float (&pv)[32]) {
+  const float* q = sk.p + int64_t(col) * 128;
+#pragma unroll
+  for (int jj = 0; jj < 32; ++jj) pv[jj] = __ldcg(q + jj * 128);
+  for (int s = 1; s < sk.n; ++s) {
+    float t[32];
+#pragma unroll
+    for (int jj = 0; jj < 32; ++jj) t[jj] = __ldcg(q + s * sk.pstride + jj * 128);
+#pragma unroll
+    for (int jj = 0; jj < 32; ++jj) pv[jj] += t[jj];
+  }
+}
+
 // ---------------------------------------------------------------- epilogue bodies
 __device__ __forceinline__ float relu_if(float v, int on) { return on ? np_relu(v) : v; }
 
@@ -149,9 +178,10 @@ __device__ __forceinline__ float relu_if(float v, int on) { return on ? np_relu(
 // per lane, TMEM lane quarter) x COLS columns in chunks of 32; C for the next chunk is in
 // flight while the current chunk computes and stores (streaming cache hints: C and D are
 // touched once and must not evict the A/B panels from L2).
-template <int OP, int COLS, int BN>
+template <int OP, int COLS, int BN, bool SK = false>
 __device__ __forceinline__ void epilogue_dense(const TcParams& p, uint64_t* tfull, uint32_t aphase,
-                                               uint32_t tbase, int i, int jbase, int lane) {
+                                               uint32_t tbase, int i, int jbase, int lane,
+                                               SkIn sk = SkIn{nullptr, 0, 0}) {
   const bool row_ok = i < p.m;
   const bool has_c = !p.c_zero;
   if (OP == OP_REAL) {
@@ -181,11 +211,14 @@ __device__ __forceinline__ void epilogue_dense(const TcParams& p, uint64_t* tful
       const int jl = j0 + lane;
       const float bcol = (p.bias_axis == 1 && jl < p.n) ? p.bias[jl] : 0.f;
       const float qcol = (p.affine && p.colsum_b && jl < p.n) ? p.aff_q * p.colsum_b[jl] : 0.f;
+      float pv[SK ? 32 : 1];
+      if constexpr (SK) sk_gather(sk, j0 - jbase + (jbase % BN), pv);
       tmem_ld_wait();
       float out[32];
 #pragma unroll
       for (int jj = 0; jj < 32; ++jj) {
         float v = __uint_as_float(r[jj]);
+        if constexpr (SK) v = pv[jj] + v;
         if (p.affine) v = p.aff_s * v + (rterm + __shfl_sync(0xffffffffu, qcol, jj));
         if (has_c) v = relu_if(cv[jj] * p.c_mul[0] + p.c_add[0], p.c_relu) + v;
         v = relu_if(v * p.r_mul[0] + p.r_add[0], p.r_relu);
@@ -256,11 +289,11 @@ __device__ __forceinline__ void epilogue_dense(const TcParams& p, uint64_t* tful
 // Dense column-major epilogue for HBM-bound shapes: C arrives in a per-warp ring of TMA boxes
 // filled by the loader warp; D is written back into the same slot and stored with one TMA
 // bulk store per 32x32 box (the slot is handed back to the loader once that store has read it).
-template <int COLS, int BN, int CSLOTS = TC_CSLOTS>
+template <int COLS, int BN, int CSLOTS = TC_CSLOTS, bool SK = false>
 __device__ __forceinline__ void epilogue_stream(const TcParams& p, uint64_t* tfull, uint32_t aphase,
                                                 uint32_t tbase, int i, int jbase, int lane,
                                                 float* ring, uint64_t* cfull, uint64_t* cempty,
-                                                uint32_t& cq, int row0) {
+                                                uint32_t& cq, int row0, SkIn sk = SkIn{nullptr, 0, 0}) {
   const bool row_ok = i < p.m;
   const bool has_c = !p.c_zero;
   float* dp = reinterpret_cast<float*>(p.d_ptr) + (row_ok ? i : 0);
@@ -287,11 +320,14 @@ __device__ __forceinline__ void epilogue_stream(const TcParams& p, uint64_t* tfu
       if (lane == 0) bulk_wait_read<CSLOTS - 1>();  // slot's previous store has read it
       __syncwarp();
     }
+    float pv[SK ? 32 : 1];
+    if constexpr (SK) sk_gather(sk, j0 - jbase + (jbase % BN), pv);
     tmem_ld_wait();
     float out[32];
 #pragma unroll
     for (int jj = 0; jj < 32; ++jj) {
       float v = __uint_as_float(r[jj]);
+      if constexpr (SK) v = pv[jj] + v;
       if (p.affine) v = p.aff_s * v + (rterm + __shfl_sync(0xffffffffu, qcol, jj));
       if (has_c) v = relu_if(cv[jj] * p.c_mul[0] + p.c_add[0], p.c_relu) + v;
       v = relu_if(v * p.r_mul[0] + p.r_add[0], p.r_relu);

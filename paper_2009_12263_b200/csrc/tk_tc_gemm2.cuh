@@ -26,7 +26,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-#define TK_TS(i) do { if (blockIdx.x == 0) g_dbg_ts[i] = gtimer(); } while (0)
+#define TK_TS(i) do { if (blockIdx.x == p.dbg_cta) g_dbg_ts[i] = gtimer(); } while (0)
 
 constexpr int TC2_BN = 256;                 // pair tile N per MMA (instruction N)
 #ifndef TK_TC2_STAGES
@@ -68,6 +68,18 @@ struct Tc2Plan {
   static constexpr int TMEM_COLS = NSUB == 2 ? 512 : 2 * BNI;  // double-buffered for NSUB 1
   static constexpr int WCOLS = BNI / 2;                        // columns per epilogue warp per pass
 };
+
+// One unit of the pair kernel's static schedule: a whole tile, or K-part `part` of a split tile
+// (role 1: leaves a partial, role 2: the last part, reduces the partials in its epilogue).
+struct PairUnit {
+  int tile, kb0, kb1, role, sk_tile, part;
+};
+__device__ __forceinline__ PairUnit pair_unit(const TcParams& p, int u) {
+  if (u < p.sk_first) return PairUnit{u, 0, p.kb_total, 0, 0, 0};
+  const int v = u - p.sk_first, r = v / p.sk_parts, s = v - r * p.sk_parts;
+  return PairUnit{p.sk_first + r, s * p.kb_total / p.sk_parts, (s + 1) * p.kb_total / p.sk_parts,
+                  s == p.sk_parts - 1 ? 2 : 1, r, s};
+}
 
 template <bool DENSE_EPI, bool CSTREAM = false, int NSUB = 1, int BNI = 256>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
@@ -141,9 +153,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     // ------------------------------------------------------------ C loader (both CTAs)
     if (!p.c_zero && lane == 0) {
       uint32_t q = 0;
-      for (int t = cluster; t < p.num_tiles; t += nclusters) {
+      for (int u = cluster; u < p.num_units; u += nclusters) {
+        const PairUnit un = pair_unit(p, u);
+        if (un.role == 1) continue;  // partial K-parts never read C
         int mb, nb;
-        tile_coords(p, t, mb, nb);
+        tile_coords(p, un.tile, mb, nb);
         for (int ch = 0; ch < NSUB * CH; ++ch, ++q) {
           const uint32_t slot = q % TC2S_CSLOTS, ph = (q / TC2S_CSLOTS) & 1;
           for (int w = 0; w < TC_EPI_WARPS; ++w) {
@@ -161,15 +175,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
   } else if (warp == 0) {
     // ------------------------------------------------------------ producer (both CTAs)
     if (lane == 0) {
-      const uint64_t pol = p.pol_ab ? policy_evict_last() : policy_evict_normal();
+      const uint64_t pol = policy_code(p.pol_a), pol_b = policy_code(p.pol_b);
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cluster; t < p.num_tiles; t += nclusters) {
+      for (int u = cluster; u < p.num_units; u += nclusters) {
+        const PairUnit un = pair_unit(p, u);
         int mb, nb;
-        tile_coords(p, t, mb, nb);
+        tile_coords(p, un.tile, mb, nb);
         const int m0 = mb * 256 + int(rank) * 128;     // this CTA's rows of A
         const int n0 = nb * BNP + int(rank) * (BNI / 2);  // this CTA's columns of B (per MMA)
-        for (int kb = 0; kb < p.kb_total; ++kb) {
+        for (int kb = un.kb0; kb < un.kb1; ++kb) {
           const int k0 = kb * TC_BK;
           mbar_wait(&empty[stage], phase ^ 1);
           if (p.dbg_skip_epi & 2) {  // diagnostic: MMA issue rate without operand traffic
@@ -198,12 +213,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
             uint8_t* bt = b_tile(stage) + sub * PL::B_BYTES;
             const int nn = n0 + sub * BNI;
             if (p.b_mn && (p.mn3d & 2)) {
-              tma_load_3d_pair(bt, &p.tb[0], fb, 0, k0, nn >> 6, pol);
+              tma_load_3d_pair(bt, &p.tb[0], fb, 0, k0, nn >> 6, pol_b);
             } else if (p.b_mn) {  // 64-column atoms (BNI >= 128)
               for (int h = 0; h < BNI / 128; ++h)
-                tma_load_2d_pair(bt + h * 8192, &p.tb[0], fb, nn + 64 * h, k0, pol);
+                tma_load_2d_pair(bt + h * 8192, &p.tb[0], fb, nn + 64 * h, k0, pol_b);
             } else {
-              tma_load_2d_pair(bt, &p.tb[0], fb, k0, nn, pol);
+              tma_load_2d_pair(bt, &p.tb[0], fb, k0, nn, pol_b);
             }
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -231,18 +246,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           tc_mma_f16_pair(d, a0, b0, idesc, (!first || kk > 0) ? 1u : 0u);
         }
       };
-      for (int t = cluster; t < p.num_tiles; t += nclusters, ++local) {
+      for (int u = cluster; u < p.num_units; u += nclusters, ++local) {
+        const PairUnit un = pair_unit(p, u);
         if (NSUB == 1) {
           const int as = local & 1;
           const uint32_t aphase = (local >> 1) & 1;
           mbar_wait(&tempty[as], aphase ^ 1);
           tc_fence_after();
           const uint32_t d0 = tmem_base + uint32_t(as * BNI);
-          for (int kb = 0; kb < p.kb_total; ++kb) {
+          for (int kb = un.kb0; kb < un.kb1; ++kb) {
             mbar_wait(&full[stage], phase);
-            if (local == 0 && kb == 0) TK_TS(2);
+            if (local == 0 && kb == un.kb0) TK_TS(2);
             tc_fence_after();
-            issue(stage, 0, d0, kb == 0);
+            issue(stage, 0, d0, kb == un.kb0);
             tc_commit_pair(&empty[stage], 0x3);
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
@@ -295,10 +311,57 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     const int row_local = quarter * 32 + lane;
     int local = 0;
     uint32_t cq = 0;
-    for (int t = cluster; t < p.num_tiles; t += nclusters, ++local) {
+    for (int u = cluster; u < p.num_units; u += nclusters, ++local) {
+      const PairUnit un = pair_unit(p, u);
+      const int t = un.tile;
       int mb, nb;
       tile_coords(p, t, mb, nb);
       const int i = mb * 256 + int(rank) * 128 + row_local;
+      // split-K: partial blocks of tile r live at sk_ws + ((r*(S-1) + s)*2 + rank) * 128*BNP,
+      // column-major 128 x BNP (this thread's row at +row_local)
+      const int64_t blk = int64_t(128) * BNP;
+      float* sk_row = p.sk_ws ? p.sk_ws + (int64_t(un.sk_tile) * (p.sk_parts - 1) * 2 + int(rank)) * blk +
+                                    row_local
+                              : nullptr;
+      if (NSUB == 1 && un.role == 1) {
+        // K-part: raw FP32 accumulator -> workspace, then count this warp in
+        const int as = local & 1;
+        const uint32_t aphase = (local >> 1) & 1;
+        mbar_wait_sleep(tfull + as, aphase);
+        tc_fence_after();
+        const uint32_t tbase = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(as * BNI);
+        float* out = sk_row + int64_t(un.part) * 2 * blk;
+#pragma unroll 1
+        for (int ch = 0; ch < CH; ++ch) {
+          const int col = half * PL::WCOLS + ch * 32;
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tbase + uint32_t(col), r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) __stcg(out + int64_t(col + jj) * 128, __uint_as_float(r[jj]));
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[as]), 0));
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(p.sk_flags + un.sk_tile, 1);
+        continue;
+      }
+      SkIn sk{nullptr, 0, 0};
+      if (NSUB == 1 && un.role == 2) {
+        // last K-part: wait until every warp of every other part has published its partial
+        if (lane == 0) {
+          const int want = (p.sk_parts - 1) * 2 * TC_EPI_WARPS;
+          int got;
+          do {
+            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(got) : "l"(p.sk_flags + un.sk_tile) : "memory");
+            if (got < want) __nanosleep(256);
+          } while (got < want);
+        }
+        __syncwarp();
+        sk = SkIn{sk_row, p.sk_parts - 1, 2 * blk};
+      }
       const int row0 = mb * 256 + int(rank) * 128 + quarter * 32;
       float* my_ring = cring + ew * TC2S_CSLOTS * (TC_CBOX_BYTES / 4);
       // NSUB 1: accumulator `local & 1`, one pass over this warp's 128 columns.
@@ -309,19 +372,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         const uint32_t aphase = NSUB == 1 ? ((local >> 1) & 1) : (local & 1);
         const uint32_t tbase = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(as * BNI);
         const int jbase = nb * BNP + pass * BNI + half * PL::WCOLS;
-        if (blockIdx.x == 0 && warp == 4 && lane == 0 && t + nclusters >= p.num_tiles) {
+        if (blockIdx.x == p.dbg_cta && warp == 4 && lane == 0 && u + nclusters >= p.num_units) {
           mbar_wait(tfull + as, aphase);
           TK_TS(4);
         }
         if (CSTREAM) {
-          epilogue_stream<PL::WCOLS, BNP, TC2S_CSLOTS>(p, tfull + as, aphase, tbase, i, jbase, lane, my_ring,
-                                                 cfull + ew * TC2S_CSLOTS, cempty + ew * TC2S_CSLOTS, cq, row0);
+          if (sk.p)
+            epilogue_stream<PL::WCOLS, BNP, TC2S_CSLOTS, true>(p, tfull + as, aphase, tbase, i, jbase, lane, my_ring,
+                                                   cfull + ew * TC2S_CSLOTS, cempty + ew * TC2S_CSLOTS, cq,
+                                                   row0, sk);
+          else
+            epilogue_stream<PL::WCOLS, BNP, TC2S_CSLOTS>(p, tfull + as, aphase, tbase, i, jbase, lane, my_ring,
+                                                   cfull + ew * TC2S_CSLOTS, cempty + ew * TC2S_CSLOTS, cq, row0);
         } else if (p.dbg_skip_epi) {
           mbar_wait_sleep(tfull + as, aphase);
           tc_fence_after();
-        } else if (DENSE_EPI)
-          epilogue_dense<OP_REAL, PL::WCOLS, BNP>(p, tfull + as, aphase, tbase, i, jbase, lane);
-        else
+        } else if (DENSE_EPI) {
+          if (sk.p)
+            epilogue_dense<OP_REAL, PL::WCOLS, BNP, true>(p, tfull + as, aphase, tbase, i, jbase, lane, sk);
+          else
+            epilogue_dense<OP_REAL, PL::WCOLS, BNP>(p, tfull + as, aphase, tbase, i, jbase, lane);
+        } else
           epilogue_generic<OP_REAL, PL::WCOLS, BNP>(p, tfull + as, aphase, tbase, i, jbase);
         tc_fence_before();
         __syncwarp();

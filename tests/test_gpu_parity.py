@@ -6,6 +6,8 @@ Bars:
 * simt lane (reference dtypes): bitwise equal -- it replays the reference's operation order.
 """
 
+import dataclasses
+
 import numpy as np
 import pytest
 
@@ -94,6 +96,39 @@ def test_dense_random_within_tolerance(cuda, dtype, mnk, tc_kernel):
     exact = O.exact_gemm(_f32(a), _f32(b), c, beta=1.0)
     assert O.rel_err(got, want) <= O.tolerance(k), O.rel_err(got, want)
     assert O.rel_err(got, exact) <= O.tolerance(k), O.rel_err(got, exact)
+
+
+_SPLITK_WANT = {}
+
+
+@pytest.mark.parametrize("mnk", [(2560, 2560, 8192), (1536, 4096, 8192), (1280, 1280, 16384)])
+@pytest.mark.parametrize("splitk", ["0", "1"])
+def test_split_k_last_wave(cuda, mnk, splitk, monkeypatch):
+    """Pair kernel with the poorly filled last wave cut into K-parts (FP32 partials in the
+    workspace, reduced in a fixed order by the last part): integer inputs stay bitwise exact,
+    random inputs within tolerance, with or without the split."""
+    monkeypatch.setenv("TK_SPLITK", splitk)
+    monkeypatch.setenv("TK_PAIR_BNI", "256")  # 256-wide tiles: the last wave is R = T % 74 tiles
+    m, n, k = mnk
+    rng = np.random.default_rng(17)
+    for integer in (True, False):
+        a, b = _half(rng, (m, k), np.float16, integer), _half(rng, (k, n), np.float16, integer)
+        c = (rng.integers(-4, 5, (m, n)) if integer else rng.standard_normal((m, n))).astype(np.float32)
+        bias = rng.standard_normal(n).astype(np.float32)
+        cfg = dataclasses.replace(tk.build_dense_config(m, n, k, np.float16),
+                                  epilogue=tk.components.BiasEpilogue(torch.from_numpy(bias).cuda()),
+                                  transform_s2g_d=tk.components.relu)
+        d = torch.zeros(m * n, dtype=torch.float32, device=cuda)
+        tk.matmul(cfg, _dev(a), _dev(b), _dev(c), d)
+        got = _host(d, (m, n))
+        key = (mnk, integer)
+        if key not in _SPLITK_WANT:  # the oracle is shared by the split / unsplit runs
+            _SPLITK_WANT[key] = np.maximum(O.gemm_real(_f32(a), _f32(b), c) + bias[None, :], 0)
+        want = _SPLITK_WANT[key]
+        if integer:
+            assert np.array_equal(got, want), float(np.abs(got - want).max())
+        else:
+            assert O.rel_err(got, want) <= O.tolerance(k), O.rel_err(got, want)
 
 
 def test_fused_affine_bias_relu(cuda):

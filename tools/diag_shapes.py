@@ -9,7 +9,7 @@ import torch  # noqa: E402
 import tools.bench_variants as bv  # noqa: E402
 
 KN = ("TK_PAIR_CSTREAM", "TK_DBG_SKIP_EPI", "TK_DBG_NO_LOAD", "TK_DBG_NO_MMA", "TK_PAIR_NSUB",
-      "TK_GROUP_M", "TK_DBG_C_ZERO")
+      "TK_GROUP_M", "TK_DBG_C_ZERO", "TK_POL_A", "TK_POL_B")
 CASES = {
     "full": {},
     "mainloop": dict(TK_PAIR_CSTREAM=0, TK_DBG_SKIP_EPI=1),
@@ -22,13 +22,15 @@ CASES = {
 shapes = [tuple(int(x) for x in s.split("x")) for s in
           os.environ.get("SHAPES", "8192x8192x2048,8192x8192x4096,8192x8192x8192").split(",")]
 cases = os.environ.get("CASES", "full,mainloop,loads,mma").split(",")
-extra = dict(kv.split("=") for kv in os.environ.get("EXTRA", "").split(",") if kv)
+extras = [dict(kv.split("=") for kv in e.split("+") if kv)
+          for e in os.environ.get("EXTRAS", os.environ.get("EXTRA", "").replace(",", "+")).split(",")]
 for (m, n, k) in shapes:
-    for c in cases:
-        for key in KN:
-            os.environ.pop(key, None)
-        os.environ.update({a: str(b) for a, b in {**CASES[c], **extra}.items()})
-        bv.dense(n, m=m, k=k, name=f"{m}x{n}x{k} {c} {extra}")
+    for extra in extras:
+        for c in cases:
+            for key in KN:
+                os.environ.pop(key, None)
+            os.environ.update({a: str(b) for a, b in {**CASES[c], **extra}.items()})
+            bv.dense(n, m=m, k=k, name=f"{m}x{n}x{k} {c} {extra}")
     for key in KN:
         os.environ.pop(key, None)
     if os.environ.get("CUBLAS", "1") == "1":

@@ -12,7 +12,9 @@ from paper_2009_12263_b200 import _lib, kernel  # noqa: E402
 lib = _lib.load()
 names = ["entry", "prologue", "1st full", "last MMA issued", "last acc full", "epilogue done", "stores drained",
          "exit"]
-for (m, n, k) in [(1024, 1024, 320), (1024, 1024, 1024), (1024, 1024, 4096), (2048, 2048, 2048)]:
+SHAPES = [tuple(int(x) for x in s.split("x")) for s in
+          os.environ.get("SHAPES", "1024x1024x320,1024x1024x1024,1024x1024x4096,2048x2048x2048").split(",")]
+for (m, n, k) in SHAPES:
     cfg = kernel.resolve_config(tk.build_dense_config(m, n, k, tk.FLOAT16))
     a = torch.randn(m * k, device="cuda").half()
     b = torch.randn(k * n, device="cuda").half()
