@@ -191,6 +191,17 @@ def run_ours(args):
         torch.cuda.synchronize(dev)
     barrier()
     ms = start.elapsed_time(end) / args.steps
+    # SM clock the kernel actually ran at (clock64 vs globaltimer in CTA 0 of the last timed
+    # launch): NVML reports the boost clock while the tensor-core step is power/current-limited
+    kernel_mhz = None
+    try:
+        import ctypes
+
+        f = tk._lib.load().tk_debug_pair_mhz
+        f.restype = ctypes.c_double
+        kernel_mhz = round(f(), 1) or None
+    except Exception:
+        pass
     t = torch.tensor([ms], device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -221,6 +232,29 @@ def run_ours(args):
     # e2e through the C ABI with host (pinned) buffers: H2D of A, B, C and D2H of C each step
     e2e = run_e2e(args, tk, api, torch, dev, m, n, k, world)
 
+    # context only (not the product, not in `value`): cuBLASLt on the same operation
+    # (fp16/bf16 A,B; fp32 C,D; D = A*B + C) timed the same way on this GPU
+    library = None
+    if rank == 0 and world == 1 and not args.no_library:
+        try:
+            # column-major D = A B + C is row-major D^T = B^T A^T + C^T: all operands contiguous
+            At, Bt, Ct = a.view(k, m), b.view(n, k), c.view(n, m)
+            f = lambda: torch.addmm(Ct, Bt, At, out_dtype=torch.float32)
+            for _ in range(3):
+                f()
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.steps):
+                f()
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            lms = e0.elapsed_time(e1) / args.steps
+            library = {"cublas_same_op_tflops": flops_rank / (lms * 1e-3) / 1e12,
+                       "call": "torch.addmm(C_fp32, A_half, B_half, out_dtype=float32)"}
+        except Exception as exc:  # older torch without out_dtype
+            library = {"unavailable": str(exc)[:120]}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_sample(m, k, len(os.sched_getaffinity(0)))
@@ -239,7 +273,8 @@ def run_ours(args):
                            "l2": "inputs (A+B+C+D) exceed the 126 MB L2; no flush",
                            "lane": tk.last_run()["lane"]},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "clocks": sampler.summary(),
+                "clocks": {**sampler.summary(), "sm_mhz_in_kernel": kernel_mhz},
+                "library_baseline": library,
                 "gpu_launches": launches_per_step * args.steps}
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -292,6 +327,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-library", action="store_true", help="skip the cuBLAS same-op context line")
     ap.add_argument("--traffic", type=float, default=None,
                     help="dram bytes per launch from an ncu --set full capture")
     args = ap.parse_args()
