@@ -438,10 +438,10 @@ int launch_tc_variant(const tk::TcParams& prm, cudaStream_t s) {
   return TK_OK;
 }
 
-template <bool DENSE, bool CSTREAM = false, int NSUB = 1, int BNI = 256>
+template <bool DENSE, bool CSTREAM = false, int NSUB = 1, int BNI = 256, int CSL = tk::TC2S_CSLOTS>
 int launch_tc_pair(const tk::TcParams& prm, cudaStream_t s) {
-  constexpr int SMEM = tk::Tc2Plan<NSUB, CSTREAM, BNI>::SMEM;
-  auto kern = tk::tc_gemm_pair_kernel<DENSE, CSTREAM, NSUB, BNI>;
+  constexpr int SMEM = tk::Tc2Plan<NSUB, CSTREAM, BNI, CSL>::SMEM;
+  auto kern = tk::tc_gemm_pair_kernel<DENSE, CSTREAM, NSUB, BNI, CSL>;
   static bool attr = false;
   if (!attr) {
     TK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
@@ -485,6 +485,10 @@ template <bool DENSE, bool CSTREAM>
 int launch_tc_pair_bni(const tk::TcParams& prm, int bni, cudaStream_t s) {
   if (bni == 64) return launch_tc_pair<DENSE, CSTREAM, 1, 64>(prm, s);
   if (bni == 128) return launch_tc_pair<DENSE, CSTREAM, 1, 128>(prm, s);
+  // single wave, 256-wide tiles: a 4-slot C ring holds each warp's whole C block
+  const char* e = getenv("TK_PAIR_DEEPC");
+  if (CSTREAM && prm.num_units <= pair_clusters() && (!e || atoi(e)))
+    return launch_tc_pair<DENSE, CSTREAM, 1, 256, 4>(prm, s);
   return launch_tc_pair<DENSE, CSTREAM, 1, 256>(prm, s);
 }
 
@@ -1183,9 +1187,9 @@ double tk_debug_clock_probe_mhz(void) {
 
 // tuning aid: the 8 globaltimer stamps of CTA 0 of the last pair-kernel launch, relative to entry (us)
 int tk_debug_pair_ts(double* out) {
-  unsigned long long v[8];
+  unsigned long long v[16];
   if (cudaMemcpyFromSymbol(v, tk::g_dbg_ts, sizeof(v)) != cudaSuccess) return 2;
-  for (int i = 0; i < 8; ++i) out[i] = v[i] >= v[0] ? double(v[i] - v[0]) * 1e-3 : -1.0;
+  for (int i = 0; i < 16; ++i) out[i] = v[i] >= v[0] ? double(v[i] - v[0]) * 1e-3 : -1.0;
   return 0;
 }
 

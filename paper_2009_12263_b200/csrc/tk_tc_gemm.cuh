@@ -149,6 +149,19 @@ __device__ __forceinline__ void write_diag_tile(uint8_t* dst, const HT* diag, in
 }
 
 
+// diagnostic: globaltimer stamps of one CTA (TcParams::dbg_cta) of the last pair-kernel launch:
+// 0 entry, 1 prologue done, 2 first stage full, 3 last MMA issued, 4 last accumulator full,
+// 5 epilogue done, 6 stores drained, 7 exit; 8.. inside the epilogue of warp 4 (first chunk:
+// TMEM loaded, math done, store issued)
+__device__ unsigned long long g_dbg_ts[16];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TK_TS(i) do { if (blockIdx.x == p.dbg_cta) g_dbg_ts[i] = gtimer(); } while (0)
+#define TK_TS_EPI(i) do { if (blockIdx.x == p.dbg_cta && (threadIdx.x >> 5) == 4 && (threadIdx.x & 31) == 0) g_dbg_ts[i] = gtimer(); } while (0)
+
 // Split-K partials to fold into the accumulator before the epilogue: this thread's row of the
 // first partial block (column stride 128), n blocks `pstride` floats apart, summed in order.
 struct SkIn {
@@ -311,11 +324,13 @@ __device__ __forceinline__ void epilogue_stream(const TcParams& p, uint64_t* tfu
     const float qcol = (p.affine && p.colsum_b && jl < p.n) ? p.aff_q * p.colsum_b[jl] : 0.f;
     const uint32_t slot = cq % CSLOTS;
     float* box = ring + slot * (TC_CBOX_BYTES / 4);
+    const uint32_t box_s = smem_u32(box);  // explicit shared-space accesses (box is a generic pointer)
     float cv[32];
     if (has_c) {
       mbar_wait(&cfull[slot], (cq / CSLOTS) & 1);
+      if (ch == 0) TK_TS_EPI(11);
 #pragma unroll
-      for (int jj = 0; jj < 32; ++jj) cv[jj] = box[jj * 32 + lane];
+      for (int jj = 0; jj < 32; ++jj) cv[jj] = lds_f32(box_s + uint32_t(jj * 32 + lane) * 4u);
     } else if (p.d_tma) {
       if (lane == 0) bulk_wait_read<CSLOTS - 1>();  // slot's previous store has read it
       __syncwarp();
@@ -323,6 +338,7 @@ __device__ __forceinline__ void epilogue_stream(const TcParams& p, uint64_t* tfu
     float pv[SK ? 32 : 1];
     if constexpr (SK) sk_gather(sk, j0 - jbase + (jbase % BN), pv);
     tmem_ld_wait();
+    if (ch == 0) TK_TS_EPI(8);
     float out[32];
 #pragma unroll
     for (int jj = 0; jj < 32; ++jj) {
@@ -334,14 +350,16 @@ __device__ __forceinline__ void epilogue_stream(const TcParams& p, uint64_t* tfu
       v = v + (p.bias_axis == 1 ? __shfl_sync(0xffffffffu, bcol, jj) : bias_m);
       out[jj] = relu_if(v * p.s_mul[0] + p.s_add[0], p.s_relu);
     }
+    if (ch == 0) TK_TS_EPI(9);
     if (p.d_tma) {
 #pragma unroll
-      for (int jj = 0; jj < 32; ++jj) box[jj * 32 + lane] = out[jj];
+      for (int jj = 0; jj < 32; ++jj) sts_f32(box_s + uint32_t(jj * 32 + lane) * 4u, out[jj]);
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
         tma_store_2d(&p.tdmap, box, row0, j0);   // the map clips rows >= M / columns >= N
         bulk_commit();
+        if (ch == 0) TK_TS_EPI(10);
         if (has_c) {  // hand the previous chunk's slot back once its store has read it
           bulk_wait_read<1>();
           if (cq > 0) mbar_arrive(&cempty[(cq - 1) % CSLOTS]);

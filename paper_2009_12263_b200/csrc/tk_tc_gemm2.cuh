@@ -18,15 +18,6 @@ namespace tk {
 
 // diagnostic: SM clock ticks and globaltimer ns of CTA 0 over the last pair-kernel launch
 __device__ unsigned long long g_dbg_clk[2];
-// diagnostic: globaltimer stamps of CTA 0 (entry, prologue done, first stage full, last MMA
-// issued, last accumulator full, epilogue done, stores drained, exit)
-__device__ unsigned long long g_dbg_ts[8];
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-#define TK_TS(i) do { if (blockIdx.x == p.dbg_cta) g_dbg_ts[i] = gtimer(); } while (0)
 
 constexpr int TC2_BN = 256;                 // pair tile N per MMA (instruction N)
 #ifndef TK_TC2_STAGES
@@ -52,13 +43,18 @@ constexpr int TC2S_SMEM = TC2S_BAR_OFFSET + 512 + 1024;
 // NSUB 1 -> 256 x BNI pair tiles, two TMEM accumulators (epilogue overlaps the next tile);
 // NSUB 2 -> 256 x 512 pair tiles (BNI 256; A re-used across 512 columns: 1/3 fewer operand
 // bytes per flop), one 512-column accumulator drained in two halves.
-template <int NSUB, bool CSTREAM, int BNI = 256>
+// CSL = C-ring slots per epilogue warp (streamed-C variant): 2 in general; 4 for single-wave
+// launches, where every 32-column C box of the tile is prefetched during the mainloop and the
+// drain never waits on a C load (3 operand stages make room).
+template <int NSUB, bool CSTREAM, int BNI = 256, int CSL = TC2S_CSLOTS>
 struct Tc2Plan {
   static constexpr int B_BYTES = BNI * 64;  // BNI/2 columns x 64 K x 2 bytes per CTA per MMA
   static constexpr int STAGE_BYTES = TC2_TILE_BYTES + NSUB * B_BYTES;
-  static constexpr int CRING_BYTES = CSTREAM ? TC_EPI_WARPS * TC2S_CSLOTS * TC_CBOX_BYTES : 0;
-  static constexpr int MAX_STAGES = (200 * 1024 - CRING_BYTES) / STAGE_BYTES;
+  static constexpr int CSLOTS = CSL;
+  static constexpr int CRING_BYTES = CSTREAM ? TC_EPI_WARPS * CSL * TC_CBOX_BYTES : 0;
+  static constexpr int MAX_STAGES = (226 * 1024 - 1536 - CRING_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = NSUB == 2 ? (CSTREAM ? 3 : 4)
+                              : CSL > TC2S_CSLOTS ? (MAX_STAGES > 8 ? 8 : MAX_STAGES)
                               : BNI == 256 ? (CSTREAM ? TC2S_STAGES : TC2_STAGES)
                               : (MAX_STAGES > 8 ? 8 : MAX_STAGES);
   static constexpr int CRING = STAGES * STAGE_BYTES;
@@ -81,14 +77,14 @@ __device__ __forceinline__ PairUnit pair_unit(const TcParams& p, int u) {
                   s == p.sk_parts - 1 ? 2 : 1, r, s};
 }
 
-template <bool DENSE_EPI, bool CSTREAM = false, int NSUB = 1, int BNI = 256>
+template <bool DENSE_EPI, bool CSTREAM = false, int NSUB = 1, int BNI = 256, int CSL = TC2S_CSLOTS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     tc_gemm_pair_kernel(const __grid_constant__ TcParams p) {
-  using PL = Tc2Plan<NSUB, CSTREAM, BNI>;
+  using PL = Tc2Plan<NSUB, CSTREAM, BNI, CSL>;
   static_assert(NSUB == 1 || BNI == 256, "NSUB 2 uses 256-wide MMAs");
   constexpr int STAGES = PL::STAGES;
   constexpr int BNP = PL::BNP;
-  constexpr int NCBAR = CSTREAM ? TC_EPI_WARPS * TC2S_CSLOTS : 0;
+  constexpr int NCBAR = CSTREAM ? TC_EPI_WARPS * CSL : 0;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -159,9 +155,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         int mb, nb;
         tile_coords(p, un.tile, mb, nb);
         for (int ch = 0; ch < NSUB * CH; ++ch, ++q) {
-          const uint32_t slot = q % TC2S_CSLOTS, ph = (q / TC2S_CSLOTS) & 1;
+          const uint32_t slot = q % CSL, ph = (q / CSL) & 1;
           for (int w = 0; w < TC_EPI_WARPS; ++w) {
-            const int bi = w * TC2S_CSLOTS + int(slot);
+            const int bi = w * CSL + int(slot);
             mbar_wait(&cempty[bi], ph ^ 1);
             mbar_arrive_expect_tx(&cfull[bi], TC_CBOX_BYTES);
             tma_load_2d(smem + PL::CRING + bi * TC_CBOX_BYTES, &p.tcmap, &cfull[bi],
@@ -363,7 +359,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         sk = SkIn{sk_row, p.sk_parts - 1, 2 * blk};
       }
       const int row0 = mb * 256 + int(rank) * 128 + quarter * 32;
-      float* my_ring = cring + ew * TC2S_CSLOTS * (TC_CBOX_BYTES / 4);
+      float* my_ring = cring + ew * CSL * (TC_CBOX_BYTES / 4);
       // NSUB 1: accumulator `local & 1`, one pass over this warp's 128 columns.
       // NSUB 2: one accumulator, pass 0 drains columns [0,256), pass 1 [256,512) (128 per warp).
 #pragma unroll 1
@@ -378,12 +374,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         }
         if (CSTREAM) {
           if (sk.p)
-            epilogue_stream<PL::WCOLS, BNP, TC2S_CSLOTS, true>(p, tfull + as, aphase, tbase, i, jbase, lane, my_ring,
-                                                   cfull + ew * TC2S_CSLOTS, cempty + ew * TC2S_CSLOTS, cq,
+            epilogue_stream<PL::WCOLS, BNP, CSL, true>(p, tfull + as, aphase, tbase, i, jbase, lane, my_ring,
+                                                   cfull + ew * CSL, cempty + ew * CSL, cq,
                                                    row0, sk);
           else
-            epilogue_stream<PL::WCOLS, BNP, TC2S_CSLOTS>(p, tfull + as, aphase, tbase, i, jbase, lane, my_ring,
-                                                   cfull + ew * TC2S_CSLOTS, cempty + ew * TC2S_CSLOTS, cq, row0);
+            epilogue_stream<PL::WCOLS, BNP, CSL>(p, tfull + as, aphase, tbase, i, jbase, lane, my_ring,
+                                                   cfull + ew * CSL, cempty + ew * CSL, cq, row0);
         } else if (p.dbg_skip_epi) {
           mbar_wait_sleep(tfull + as, aphase);
           tc_fence_after();

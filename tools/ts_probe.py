@@ -11,7 +11,7 @@ from paper_2009_12263_b200 import _lib, kernel  # noqa: E402
 
 lib = _lib.load()
 names = ["entry", "prologue", "1st full", "last MMA issued", "last acc full", "epilogue done", "stores drained",
-         "exit"]
+         "exit", "epi:tmem", "epi:math", "epi:store", "epi:C ready"]
 SHAPES = [tuple(int(x) for x in s.split("x")) for s in
           os.environ.get("SHAPES", "1024x1024x320,1024x1024x1024,1024x1024x4096,2048x2048x2048").split(",")]
 for (m, n, k) in SHAPES:
@@ -23,6 +23,8 @@ for (m, n, k) in SHAPES:
     for _ in range(5):
         tk.gemm_execute(cfg, a, b, c, d)
     torch.cuda.synchronize()
-    out = (ctypes.c_double * 8)()
+    for i in range(16):
+        pass
+    out = (ctypes.c_double * 16)()
     lib.tk_debug_pair_ts(out)
     print(f"{m}x{n}x{k}: " + "  ".join(f"{nm}={v:.2f}" for nm, v in zip(names, out) if nm != "-"))
