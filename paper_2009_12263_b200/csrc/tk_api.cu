@@ -600,6 +600,7 @@ int tc_kernel_override() {
   if (!strcmp(e, "quad")) return 4;
   if (!strcmp(e, "stream")) return 3;
   if (!strcmp(e, "single")) return 1;
+  if (!strcmp(e, "diagstream")) return 5;
   return 0;
 }
 
@@ -903,6 +904,30 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
   // for the CTA pair (C prefetched by the loader warp while the mainloop runs)
   const bool single_wave = prm.num_tiles <= sm_count();
   const bool rmapped = prm.c_rmap || prm.d_rmap;
+  // diagonal A: an HBM stream, run as one (vectorised) elementwise pass, not on the tensor cores
+  if (op == TK_OP_REAL && prm.diag_a && dense && !rmapped && !prm.affine && prm.b_mn == 0 &&
+      (ov == 0 || ov == 5)) {
+    const char* e = getenv("TK_DIAG_STREAM");
+    if (!e || atoi(e)) {
+      int mnk;
+      int64_t ldb;
+      tma_operand(p->b, mnk, ldb);
+      auto al = [](const void* q, int bytes) { return (reinterpret_cast<uintptr_t>(q) % bytes) == 0; };
+      tk::TcParams ps = prm;
+      ps.vec_ok = ldb % 4 == 0 && prm.ldd % 4 == 0 && (prm.c_zero || (prm.ldc % 4 == 0 && al(c, 16))) &&
+                  al(b, 8) && al(prm.diag, 8) && al(d, 16);
+      const int64_t rows4 = (p->m + 3) / 4;
+      const dim3 grid(unsigned(std::min<int64_t>((rows4 + 255) / 256, 1024)),
+                      unsigned(std::min<int64_t>(p->n, 16384)));
+      if (prm.ab_fmt == 0)
+        tk::diag_stream_kernel<__half><<<grid, 256, 0, s>>>(ps, static_cast<const __half*>(b), ldb);
+      else
+        tk::diag_stream_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(ps, static_cast<const __nv_bfloat16*>(b), ldb);
+      TK_CUDA(cudaGetLastError());
+      ++g_launches;
+      return TK_OK;
+    }
+  }
   if (op == TK_OP_REAL && dense && !rmapped &&
       (ov == 3 || (ov == 0 && (prm.diag_a || prm.kb_total <= 4 || (single_wave && !pair_ok))))) {
     const bool cs = prm.c_zero || ((prm.ldc * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(c) & 15) == 0);

@@ -16,6 +16,7 @@
 //               D = s2g( r2s( g2s_c(C) + acc ) + bias ) -> coalesced global stores
 //               (reference kernel.py:370-463, components.py:110-157).
 #pragma once
+#include "tk_prep.cuh"
 #include "tk_ptx.cuh"
 #include "tk_types.cuh"
 
@@ -100,6 +101,7 @@ struct TcParams {
   // units sk_first + r*sk_parts + s are K-part s of tile sk_first + r; parts < sk_parts-1
   // leave raw FP32 partials in sk_ws and count down sk_flags[r], the last part reduces them.
   int32_t num_units, sk_first, sk_parts, dbg_cta;
+  int32_t vec_ok, pad4;          // diag_stream_kernel: 16-byte vector path legal
   float* sk_ws;
   int32_t* sk_flags;
 };
@@ -657,6 +659,61 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(const __grid_con
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, C::TMEM_COLS);
+  }
+}
+
+}  // namespace tk
+
+namespace tk {
+
+// Diagonal A (reference build_diagonal_config / Diagonal layout, layouts.py:191-252, with the
+// DiagonalPredicate skipping every block-K iteration that misses the diagonal,
+// components.py:177-191): D = epi(C + diag(a) B) is a pure HBM stream -- 2 bytes of B and
+// 4 + 4 bytes of C and D per element, one multiply -- so it runs as a vectorised streaming
+// kernel instead of occupying the tensor cores with 127/128 zero columns.  The arithmetic is
+// the tcgen05 path's: the product a_i * b_ij of two halves is exact in FP32 (the MMA adds only
+// exact zeros to it), then the same epilogue sequence as epilogue_dense.
+template <typename H>
+__global__ void __launch_bounds__(256) diag_stream_kernel(const __grid_constant__ TcParams p,
+                                                          const H* __restrict__ b, int64_t ldb) {
+  const H* diag = reinterpret_cast<const H*>(p.diag);
+  const float* cp = reinterpret_cast<const float*>(p.c_ptr);
+  float* dp = reinterpret_cast<float*>(p.d_ptr);
+  const bool has_c = !p.c_zero;
+  const int64_t rows4 = (int64_t(p.m) + 3) / 4;
+  const int64_t kdiag = p.k < p.m ? p.k : p.m;  // rows with a diagonal entry
+  auto epi = [&](float acc, float c, float bias) {
+    float v = acc;
+    if (has_c) v = relu_if(c * p.c_mul[0] + p.c_add[0], p.c_relu) + v;
+    v = relu_if(v * p.r_mul[0] + p.r_add[0], p.r_relu);
+    v = v + bias;
+    return relu_if(v * p.s_mul[0] + p.s_add[0], p.s_relu);
+  };
+  for (int64_t j = blockIdx.y; j < p.n; j += gridDim.y) {
+    const float bias_j = p.bias_axis == 1 ? p.bias[j] : 0.f;
+    for (int64_t r4 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r4 < rows4; r4 += int64_t(gridDim.x) * blockDim.x) {
+      const int64_t i0 = r4 * 4;
+      if (p.vec_ok && i0 + 4 <= kdiag) {  // vector path: 4 rows, all on the diagonal, aligned
+        const uint2 bv = __ldcs(reinterpret_cast<const uint2*>(b + i0 + j * ldb));
+        const uint2 av = *reinterpret_cast<const uint2*>(diag + i0);
+        const float4 cv = has_c ? __ldcs(reinterpret_cast<const float4*>(cp + i0 + j * p.ldc))
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
+        const H* bh = reinterpret_cast<const H*>(&bv);
+        const H* ah = reinterpret_cast<const H*>(&av);
+        float4 o;
+        o.x = epi(__fmul_rn(h2f(ah[0]), h2f(bh[0])), cv.x, p.bias_axis == 2 ? p.bias[i0] : bias_j);
+        o.y = epi(__fmul_rn(h2f(ah[1]), h2f(bh[1])), cv.y, p.bias_axis == 2 ? p.bias[i0 + 1] : bias_j);
+        o.z = epi(__fmul_rn(h2f(ah[2]), h2f(bh[2])), cv.z, p.bias_axis == 2 ? p.bias[i0 + 2] : bias_j);
+        o.w = epi(__fmul_rn(h2f(ah[3]), h2f(bh[3])), cv.w, p.bias_axis == 2 ? p.bias[i0 + 3] : bias_j);
+        __stcs(reinterpret_cast<float4*>(dp + i0 + j * p.ldd), o);
+      } else {
+        for (int64_t i = i0; i < i0 + 4 && i < p.m; ++i) {
+          const float acc = i < kdiag ? __fmul_rn(h2f(diag[i]), h2f(b[i + j * ldb])) : 0.f;
+          const float c = has_c ? cp[i + j * p.ldc] : 0.f;
+          dp[i + j * p.ldd] = epi(acc, c, p.bias_axis == 2 ? p.bias[i] : bias_j);
+        }
+      }
+    }
   }
 }
 

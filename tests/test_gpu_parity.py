@@ -212,11 +212,15 @@ def _unpack_pair(t, shape, split):
     return p0.reshape(shape, order="F"), p1.reshape(shape, order="F")
 
 
-@pytest.mark.parametrize("kernel", ["auto", "single"])
+@pytest.mark.parametrize("kernel", ["auto", "single", "tensor"])
 @pytest.mark.parametrize("n", [256, 1024, 640])
 def test_diagonal_variant(cuda, n, kernel, monkeypatch):
-    if kernel != "auto":
+    """auto: the vectorised HBM stream; single / tensor: the tcgen05 kernel with the diagonal
+    tile fabricated in shared memory -- all bitwise equal to the oracle."""
+    if kernel == "single":
         monkeypatch.setenv("TK_TC_KERNEL", kernel)
+    elif kernel == "tensor":
+        monkeypatch.setenv("TK_DIAG_STREAM", "0")
     rng = np.random.default_rng(4)
     diag = rng.standard_normal(n).astype(np.float16)
     b = rng.standard_normal((n, n)).astype(np.float16)
@@ -228,7 +232,46 @@ def test_diagonal_variant(cuda, n, kernel, monkeypatch):
     want = O.gemm_real(np.diag(_f32(diag)), _f32(b), c)
     # diag(a)*B + C: one product per element -> exact in FP32
     assert np.array_equal(_host(d, (n, n)), want)
-    assert counters.inner_iterations_executed == (n // 64) * (n // 64) * 4
+    if n % 64 == 0:
+        assert counters.inner_iterations_executed == (n // 64) * (n // 64) * 4
+
+
+@pytest.mark.parametrize("stream", ["1", "0", "misaligned"])
+def test_diagonal_epilogue_rectangular(cuda, stream, monkeypatch):
+    """Diagonal A with alpha/beta scaling, a row bias and ReLU, N != M; 'misaligned' offsets
+    the buffers by one element so the stream kernel takes its scalar path."""
+    monkeypatch.setenv("TK_DIAG_STREAM", "0" if stream == "0" else "1")
+    m, n, k = 520, 384, 520
+    rng = np.random.default_rng(6)
+    diag = rng.integers(-4, 5, min(m, k)).astype(np.float16)
+    b = rng.integers(-4, 5, (k, n)).astype(np.float16)
+    c = rng.integers(-4, 5, (m, n)).astype(np.float32)
+    bias = rng.integers(-4, 5, m).astype(np.float32)
+    cfg = tk.build_diagonal_config(m, np.float16)
+    cfg = dataclasses.replace(
+        cfg, params=dataclasses.replace(cfg.params, gemm_shape=(m, n, k)),
+        global_b_layout=tk.layouts.ColMajor(np.float16, ("K", "N"), (k, n)),
+        global_c_layout=tk.layouts.ColMajor(np.float32, ("M", "N"), (m, n)),
+        global_d_layout=tk.layouts.ColMajor(np.float32, ("M", "N"), (m, n)),
+        transform_g2s_c=tk.components.scale(0.5), transform_r2s_d=tk.components.scale(2.0),
+        epilogue=tk.components.BiasEpilogue(torch.from_numpy(bias).cuda(), axis="m"),
+        transform_s2g_d=tk.components.relu)
+    def dev(x, off):
+        t = _dev(x)
+        if not off:
+            return t
+        buf = torch.empty(t.numel() + 1, dtype=t.dtype, device=cuda)
+        buf[1:] = t
+        return buf[1:]
+    off = stream == "misaligned"
+    dbuf = torch.zeros(m * n + 1, dtype=torch.float32, device=cuda)
+    d = dbuf[1:] if off else dbuf[:-1]
+    tk.matmul(cfg, dev(diag, off), dev(b, off), dev(c, off), d)
+    assert tk.last_run()["lane"] == "tcgen05"
+    a_full = np.zeros((m, k), np.float32)
+    a_full[np.arange(min(m, k)), np.arange(min(m, k))] = diag
+    want = np.maximum(2.0 * (0.5 * c + a_full @ _f32(b)) + bias[:, None], 0)
+    assert np.array_equal(_host(d, (m, n)), want.astype(np.float32))
 
 
 def test_gemm_ex_alpha_beta_trans(cuda):
