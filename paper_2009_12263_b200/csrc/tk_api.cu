@@ -873,6 +873,9 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
   if (const char* g = getenv("TK_DBG_SKIP_EPI")) prm.dbg_skip_epi = atoi(g);
   if (const char* g = getenv("TK_DBG_NO_LOAD")) prm.dbg_skip_epi |= atoi(g) ? 2 : 0;
   if (const char* g = getenv("TK_DBG_CTA")) prm.dbg_cta = atoi(g);
+  // serpentine K order on the pair kernel: DRAM reads 1.43 -> 1.29 GB at 8192^3, ~+1 %
+  prm.serp = 1;
+  if (const char* g = getenv("TK_SERPENTINE")) prm.serp = atoi(g);
   if (const char* g = getenv("TK_DBG_NO_MMA")) prm.dbg_skip_epi |= atoi(g) ? 4 : 0;
   prm.pol_ab = 1;  // A/B panels are re-read by neighbouring tiles: keep them in L2
   if (const char* g = getenv("TK_POLICY_AB")) prm.pol_ab = atoi(g);

@@ -101,7 +101,7 @@ struct TcParams {
   // units sk_first + r*sk_parts + s are K-part s of tile sk_first + r; parts < sk_parts-1
   // leave raw FP32 partials in sk_ws and count down sk_flags[r], the last part reduces them.
   int32_t num_units, sk_first, sk_parts, dbg_cta;
-  int32_t vec_ok, pad4;          // diag_stream_kernel: 16-byte vector path legal
+  int32_t vec_ok, serp;          // diag_stream_kernel: 16-byte vector path legal; pair kernel: serpentine K
   float* sk_ws;
   int32_t* sk_flags;
 };

@@ -174,13 +174,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       const uint64_t pol = policy_code(p.pol_a), pol_b = policy_code(p.pol_b);
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = cluster; u < p.num_units; u += nclusters) {
+      int lu = 0;
+      for (int u = cluster; u < p.num_units; u += nclusters, ++lu) {
         const PairUnit un = pair_unit(p, u);
         int mb, nb;
         tile_coords(p, un.tile, mb, nb);
         const int m0 = mb * 256 + int(rank) * 128;     // this CTA's rows of A
         const int n0 = nb * BNP + int(rank) * (BNI / 2);  // this CTA's columns of B (per MMA)
-        for (int kb = un.kb0; kb < un.kb1; ++kb) {
+        // serpentine K (opt-in): every other tile of a cluster walks K downwards, so the next
+        // wave starts on the K-slices the previous one loaded last (still in L2)
+        const bool rev = NSUB == 1 && p.serp && (lu & 1);
+        for (int ki = 0; ki < un.kb1 - un.kb0; ++ki) {
+          const int kb = rev ? un.kb1 - 1 - ki : un.kb0 + ki;
           const int k0 = kb * TC_BK;
           mbar_wait(&empty[stage], phase ^ 1);
           if (p.dbg_skip_epi & 2) {  // diagnostic: MMA issue rate without operand traffic
@@ -250,7 +255,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           mbar_wait(&tempty[as], aphase ^ 1);
           tc_fence_after();
           const uint32_t d0 = tmem_base + uint32_t(as * BNI);
-          for (int kb = un.kb0; kb < un.kb1; ++kb) {
+          for (int kb = un.kb0; kb < un.kb1; ++kb) {  // (operand order is the producer's)
             mbar_wait(&full[stage], phase);
             if (local == 0 && kb == un.kb0) TK_TS(2);
             tc_fence_after();

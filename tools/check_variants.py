@@ -15,6 +15,7 @@ VARIANTS = [dict(TK_PAIR_BNI="256"), dict(TK_PAIR_BNI="128"), dict(TK_PAIR_BNI="
 if os.environ.get("VARIANTS"):
     VARIANTS = [dict(kv.split("=") for kv in v.split("+")) for v in os.environ["VARIANTS"].split(",")]
 KEYS = {k for v in VARIANTS for k in v}
+os.environ["TK_SERPENTINE"] = "0"  # same k order in every tile, so variants must agree bitwise
 shapes = [(1024, 1024, 1024), (4096, 4096 + 256, 4096), (3000, 5000, 1000), (8192, 2048, 512),
           (2048, 8192 + 64, 2048), (640, 200, 704)]
 g = torch.Generator(device="cuda")
