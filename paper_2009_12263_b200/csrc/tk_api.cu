@@ -474,8 +474,25 @@ int launch_tc_pair(const tk::TcParams& prm, cudaStream_t s) {
   int clusters = std::min(run.num_units, max_clusters);
   if (const char* e = getenv("TK_PAIR_GRID")) clusters = std::max(1, std::min(clusters, atoi(e)));
   const int grid = 2 * clusters;
-  kern<<<grid, tk::TC_THREADS, SMEM, s>>>(run);
-  TK_CUDA(cudaGetLastError());
+  // programmatic dependent launch: the next GEMM in the stream may be scheduled while this one
+  // drains; its CTAs run their prologue (barriers, TMEM, tensor-map prefetch) and then wait in
+  // griddepcontrol.wait until this grid has completed and its writes are visible
+  static const bool pdl = [] {
+    const char* e = getenv("TK_PDL");
+    return !e || atoi(e);
+  }();
+  run.pdl = pdl ? 1 : 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(tk::TC_THREADS);
+  cfg.dynamicSmemBytes = SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  TK_CUDA(cudaLaunchKernelEx(&cfg, kern, run));
   ++g_launches;
   return TK_OK;
 }

@@ -102,6 +102,7 @@ struct TcParams {
   // leave raw FP32 partials in sk_ws and count down sk_flags[r], the last part reduces them.
   int32_t num_units, sk_first, sk_parts, dbg_cta;
   int32_t vec_ok, serp;          // diag_stream_kernel: 16-byte vector path legal; pair kernel: serpentine K
+  int32_t pdl, pad5;             // pair kernel launched with programmatic stream serialisation
   float* sk_ws;
   int32_t* sk_flags;
 };

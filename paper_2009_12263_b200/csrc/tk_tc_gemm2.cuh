@@ -134,6 +134,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (p.pdl) {
+    // let the next launch in the stream start its prologue as our CTAs retire, and do not touch
+    // global memory before the previous grid (the producer of our inputs) has completed
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
   if (threadIdx.x == 0) TK_TS(1);
   unsigned long long clk0 = 0, ns0 = 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -158,7 +164,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           const uint32_t slot = q % CSL, ph = (q / CSL) & 1;
           for (int w = 0; w < TC_EPI_WARPS; ++w) {
             const int bi = w * CSL + int(slot);
-            mbar_wait(&cempty[bi], ph ^ 1);
+            mbar_wait_sleep(&cempty[bi], ph ^ 1);
             mbar_arrive_expect_tx(&cfull[bi], TC_CBOX_BYTES);
             tma_load_2d(smem + PL::CRING + bi * TC_CBOX_BYTES, &p.tcmap, &cfull[bi],
                         mb * 256 + int(rank) * 128 + (w & 3) * 32,
