@@ -229,6 +229,34 @@ def run_ours(args):
                 "frac_of_sustained": achieved / sustained if sustained else None,
                 "frac_of_spec_2250": achieved / 2250.0}
 
+    # optional collective, timed separately (north star: "an optional NCCL all-gather of C over
+    # NVLink is timed separately"): every rank's D slab gathered into the full M x (n*G) D
+    allgather = None
+    if world > 1:
+        try:
+            full = torch.empty(m * n * world, device=dev)
+            for _ in range(2):
+                dist.all_gather_into_tensor(full, d)
+            barrier()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = max(3, min(args.steps, 10))
+            g0.record(stream)
+            for _ in range(reps):
+                dist.all_gather_into_tensor(full, d)
+            g1.record(stream)
+            torch.cuda.synchronize(dev)
+            gms = torch.tensor([g0.elapsed_time(g1) / reps], device=dev)
+            dist.all_reduce(gms, op=dist.ReduceOp.MAX)
+            gms = float(gms.item())
+            recv = (world - 1) * m * n * 4  # bytes each rank receives
+            allgather = {"ms": gms, "bytes_received_per_rank": recv,
+                         "GB_per_s_per_rank": recv / (gms * 1e-3) / 1e9,
+                         "collective": "torch.distributed.all_gather_into_tensor (NCCL)",
+                         "in_value": False}
+            del full
+        except Exception as exc:
+            allgather = {"unavailable": str(exc)[:160]}
+
     # e2e through the C ABI with host (pinned) buffers: H2D of A, B, C and D2H of C each step
     e2e = run_e2e(args, tk, api, torch, dev, m, n, k, world)
 
@@ -275,6 +303,7 @@ def run_ours(args):
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "clocks": {**sampler.summary(), "sm_mhz_in_kernel": kernel_mhz},
                 "library_baseline": library,
+                "allgather_d": allgather,
                 "gpu_launches": launches_per_step * args.steps}
         print(json.dumps(line), flush=True)
     if world > 1:

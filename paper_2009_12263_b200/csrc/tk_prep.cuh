@@ -122,10 +122,17 @@ struct PackDesc {
   int64_t tiles_s, tiles_d, outer;  // tiles along X, along Y, outer digit combinations
 };
 
+// tile element (y, x) of the 64 x 64 staging tile: 16-byte chunks of each 128-byte row are
+// XOR-swizzled by y/8, so both the row-wise (vector) phase and the column-wise (transpose)
+// phase hit 32 distinct banks per warp
+__device__ __forceinline__ int pack_tile_off(int y, int x) {
+  return y * 64 + ((((x >> 3) ^ (y >> 3)) & 7) << 3) + (x & 7);
+}
+
 __global__ void __launch_bounds__(256) pack_half_kernel(const uint16_t* __restrict__ src, uint16_t* __restrict__ dst,
                                                         const __grid_constant__ PackDesc pd, int pair,
                                                         int64_t plane_stride, int plane) {
-  __shared__ __align__(16) uint16_t tile[64][72];  // [y][x]; 144-byte rows keep 16-byte alignment
+  __shared__ __align__(16) uint16_t tile[64 * 64];
   const int64_t nblocks = pd.tiles_s * pd.tiles_d * pd.outer;
   const int64_t sx = pd.ss[pd.fs], sy = pd.ss[pd.fd], dx = pd.ds[pd.fs], dy = pd.ds[pd.fd];
   for (int64_t blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
@@ -152,7 +159,7 @@ __global__ void __launch_bounds__(256) pack_half_kernel(const uint16_t* __restri
       for (int idx = threadIdx.x; idx < 64 * 8; idx += blockDim.x) {
         const int x = (idx & 7) * 8, y = idx >> 3;
         if (y < ny && x < nx)
-          *reinterpret_cast<uint4*>(&tile[y][x]) =
+          *reinterpret_cast<uint4*>(&tile[pack_tile_off(y, x)]) =
               *reinterpret_cast<const uint4*>(src + so + y * sy + x + int64_t(plane) * plane_stride);
       }
     } else {
@@ -160,7 +167,7 @@ __global__ void __launch_bounds__(256) pack_half_kernel(const uint16_t* __restri
         const int x = idx & 63, y = idx >> 6;
         if (x < nx && y < ny) {
           const int64_t off = so + x * sx + y * sy;
-          tile[y][x] = src[pair == P_INTERLEAVED ? 2 * off + plane : off + int64_t(plane) * plane_stride];
+          tile[pack_tile_off(y, x)] = src[pair == P_INTERLEAVED ? 2 * off + plane : off + int64_t(plane) * plane_stride];
         }
       }
     }
@@ -170,12 +177,12 @@ __global__ void __launch_bounds__(256) pack_half_kernel(const uint16_t* __restri
         for (int idx = threadIdx.x; idx < 64 * 8; idx += blockDim.x) {
           const int x = (idx & 7) * 8, y = idx >> 3;
           if (y < ny && x < nx)
-            *reinterpret_cast<uint4*>(dst + dof + y * dy + x) = *reinterpret_cast<const uint4*>(&tile[y][x]);
+            *reinterpret_cast<uint4*>(dst + dof + y * dy + x) = *reinterpret_cast<const uint4*>(&tile[pack_tile_off(y, x)]);
         }
       } else {
         for (int idx = threadIdx.x; idx < 64 * 64; idx += blockDim.x) {
           const int x = idx & 63, y = idx >> 6;
-          if (x < nx && y < ny) dst[dof + x * dx + y * dy] = tile[y][x];
+          if (x < nx && y < ny) dst[dof + x * dx + y * dy] = tile[pack_tile_off(y, x)];
         }
       }
     } else {  // destination runs along Y: transpose through shared memory
@@ -186,14 +193,14 @@ __global__ void __launch_bounds__(256) pack_half_kernel(const uint16_t* __restri
             uint4 v;
             uint16_t* h = reinterpret_cast<uint16_t*>(&v);
 #pragma unroll
-            for (int e = 0; e < 8; ++e) h[e] = tile[y + e][x];
+            for (int e = 0; e < 8; ++e) h[e] = tile[pack_tile_off(y + e, x)];
             *reinterpret_cast<uint4*>(dst + dof + x * dx + y) = v;
           }
         }
       } else {
         for (int idx = threadIdx.x; idx < 64 * 64; idx += blockDim.x) {
           const int y = idx & 63, x = idx >> 6;
-          if (x < nx && y < ny) dst[dof + x * dx + y * dy] = tile[y][x];
+          if (x < nx && y < ny) dst[dof + x * dx + y * dy] = tile[pack_tile_off(y, x)];
         }
       }
     }

@@ -1,5 +1,5 @@
 """Run one named GEMM case a few times (for ncu captures): dense8192, c3_8192, fused8192,
-complex8192, dual8192, diag16384, skinny128, tc_large, tc_paper."""
+complex8192, dual8192, diag16384, skinny128, tc_large, tc_paper, gett2, splitk."""
 import os
 import sys
 
@@ -19,4 +19,6 @@ bv.timeit = lambda fn, reps=3, warm=2: [fn() for _ in range(warm + reps)] and 1.
     "skinny128": lambda: bv.skinny(8192, 128),
     "tc_large": lambda: bv.contraction(64, 128, 8192, 8192),
     "tc_paper": lambda: bv.contraction(64, 32, 2048, 2048),
+    "gett2": lambda: bv.gett_case("abcd-aebf-dfce", dict(a=128, b=64, c=128, d=64, e=128, f=64)),
+    "splitk": lambda: bv.dense(4096, m=1536, k=16384),
 }[case]()
