@@ -1068,8 +1068,20 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
           attr[oi][dense] = true;
         }
         const int grid = 2 * std::min(pp.num_tiles, sm_count() / 2);
-        kern<<<grid, tk::TC_THREADS, tk::TC2C_SMEM, s>>>(pp);
-        TK_CUDA(cudaGetLastError());
+        const char* e = getenv("TK_PDL");
+        tk::TcParams run = pp;
+        run.pdl = (!e || atoi(e)) ? 1 : 0;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(tk::TC_THREADS);
+        cfg.dynamicSmemBytes = tk::TC2C_SMEM;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = run.pdl ? 1 : 0;
+        TK_CUDA(cudaLaunchKernelEx(&cfg, kern, run));
         ++g_launches;
         return TK_OK;
       };

@@ -64,6 +64,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (p.pdl) {  // programmatic dependent launch (see tc_gemm_pair_kernel)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
 
   auto a_tile = [&](int s, int pl) -> uint8_t* { return smem + s * TC2C_STAGE_BYTES + pl * TC2C_A_BYTES; };
   auto b_tile = [&](int s, int pl) -> uint8_t* {
@@ -75,12 +79,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       const uint64_t pol = p.pol_ab ? policy_evict_last() : policy_evict_normal();
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cluster; t < p.num_tiles; t += nclusters) {
+      int lu = 0;
+      for (int t = cluster; t < p.num_tiles; t += nclusters, ++lu) {
         int mb, nb;
         tile_coords(p, t, mb, nb);
         const int m0 = mb * 256 + int(rank) * 128;
         const int n0 = nb * TC2C_BN + int(rank) * 64;
-        for (int kb = 0; kb < p.kb_total; ++kb) {
+        const bool rev = p.serp && (lu & 1);  // serpentine K (see tc_gemm_pair_kernel)
+        for (int ki = 0; ki < p.kb_total; ++ki) {
+          const int kb = rev ? p.kb_total - 1 - ki : ki;
           const int k0 = kb * TC_BK;
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * TC2C_STAGE_BYTES);
