@@ -136,6 +136,23 @@ int tk_last_launch_count(void);
 /* Message of the last failure in this thread ("" if none). */
 const char* tk_last_error(void);
 
+/* ---- diagnostics (no reference counterpart; used by bench.py and tools/) ---------------- */
+
+/* Effective SM clock (MHz) of CTA 0 over the last CTA-pair GEMM launch: clock64 ticks over
+ * %globaltimer ns, read after the launch completed.  NVML reports the boost clock while a
+ * tensor-core GEMM runs power/current-limited; this is the clock the kernel actually saw. */
+double tk_debug_pair_mhz(void);
+
+/* globaltimer stamps (us after entry) of the CTA selected by TK_DBG_CTA in the last pair-kernel
+ * launch: entry, prologue, first stage full, last MMA issued, last accumulator full, epilogue
+ * done, stores drained, exit, then four epilogue-internal stamps (16 doubles; -1 if unset). */
+int tk_debug_pair_ts(double* out16);
+
+/* Launch a 1-CTA sleeper on `stream` for `us` microseconds that measures the SM clock while
+ * other work runs; read the result with tk_debug_clock_probe_mhz() after synchronising. */
+int tk_debug_clock_probe(double us, void* stream);
+double tk_debug_clock_probe_mhz(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -59,7 +59,8 @@ GEMM_EX_ARGTYPES = [c_int, c_int, c_int, c_longlong, c_longlong, c_longlong, c_d
 
 # every symbol include/tk_sm100.h declares
 EXPORTED = ("tk_abi_version", "tk_plan_lane", "tk_workspace_bytes", "tk_gemm", "tk_gemm_ex_raw",
-            "tk_gemm_ex_raw_async", "tk_last_launch_count", "tk_last_error")
+            "tk_gemm_ex_raw_async", "tk_last_launch_count", "tk_last_error", "tk_debug_pair_mhz",
+            "tk_debug_pair_ts", "tk_debug_clock_probe", "tk_debug_clock_probe_mhz")
 
 _lib = None
 _load_error = None

@@ -889,6 +889,7 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
   if (const char* g = getenv("TK_GROUP_M")) prm.group_m = std::max(1, atoi(g));
   if (const char* g = getenv("TK_DBG_SKIP_EPI")) prm.dbg_skip_epi = atoi(g);
   if (const char* g = getenv("TK_DBG_NO_LOAD")) prm.dbg_skip_epi |= atoi(g) ? 2 : 0;
+  prm.dbg_cta = -1;  // timestamp probes off unless a CTA is selected (tools/ts_probe.py)
   if (const char* g = getenv("TK_DBG_CTA")) prm.dbg_cta = atoi(g);
   // serpentine K order on the pair kernel: DRAM reads 1.43 -> 1.29 GB at 8192^3, ~+1 %
   prm.serp = 1;

@@ -4,6 +4,7 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ.setdefault("TK_DBG_CTA", "0")
 import torch  # noqa: E402
 
 import paper_2009_12263_b200 as tk  # noqa: E402
