@@ -47,7 +47,10 @@ struct TcCfg<OP_DUAL> {
 // fp32), refilled by the loader warp.  CS = 1 (HBM-bound shapes: diagonal A, K <= 256):
 // 2 mainloop stages, 3 ring slots.  CS = 2 (single-wave dense shapes): 3 stages, 2 slots.
 constexpr int TC_CBOX_BYTES = 32 * 32 * 4;
-__host__ __device__ constexpr int tc_cslots(int cs) { return cs == 1 ? 3 : 2; }
+#ifndef TK_HBM_CSLOTS
+#define TK_HBM_CSLOTS 3
+#endif
+__host__ __device__ constexpr int tc_cslots(int cs) { return cs == 1 ? TK_HBM_CSLOTS : 2; }
 constexpr int TC_CSLOTS = 3;
 
 template <int OP, int CSTREAM = 0>
@@ -187,8 +190,52 @@ __device__ __forceinline__ void sk_gather(const SkIn& sk, int col, float (&pv)[3
   }
 }
 
-// ---------------------------------------------------------------- epilogue bodies
 __device__ __forceinline__ float relu_if(float v, int on) { return on ? np_relu(v) : v; }
+
+// The fused real epilogue on one 32-column chunk (row = lane), in the reference's order
+// (components.py:110-157): v = acc [+ split-K partials]; affine operand terms; + t_c(C);
+// r2s; + bias; s2g.  Uniform decisions are taken once per chunk (a branch around every
+// element's shuffle costs ~1 us per chunk), the per-element arithmetic is unchanged.
+template <bool SK>
+__device__ __forceinline__ void epi_math_real(const TcParams& p, const uint32_t (&r)[32],
+                                              const float (&cv)[32], const float (&pv)[SK ? 32 : 1],
+                                              bool has_c, float rterm, float bias_m, float bcol,
+                                              float qcol, float (&out)[32]) {
+  float v[32], add[32];
+#pragma unroll
+  for (int jj = 0; jj < 32; ++jj) v[jj] = __uint_as_float(r[jj]);
+  if constexpr (SK) {
+#pragma unroll
+    for (int jj = 0; jj < 32; ++jj) v[jj] = pv[jj] + v[jj];
+  }
+  if (p.affine) {
+#pragma unroll
+    for (int jj = 0; jj < 32; ++jj) v[jj] = p.aff_s * v[jj] + (rterm + __shfl_sync(0xffffffffu, qcol, jj));
+  }
+  if (p.bias_axis == 1) {
+#pragma unroll
+    for (int jj = 0; jj < 32; ++jj) add[jj] = __shfl_sync(0xffffffffu, bcol, jj);
+  } else {
+#pragma unroll
+    for (int jj = 0; jj < 32; ++jj) add[jj] = bias_m;
+  }
+  if (has_c) {
+    const float cm = p.c_mul[0], ca = p.c_add[0];
+    const int cr = p.c_relu;
+#pragma unroll
+    for (int jj = 0; jj < 32; ++jj) v[jj] = relu_if(cv[jj] * cm + ca, cr) + v[jj];
+  }
+  const float rm = p.r_mul[0], ra = p.r_add[0], sm = p.s_mul[0], sa = p.s_add[0];
+  const int rr = p.r_relu, sr = p.s_relu;
+#pragma unroll
+  for (int jj = 0; jj < 32; ++jj) {
+    float x = relu_if(v[jj] * rm + ra, rr);
+    x = x + add[jj];
+    out[jj] = relu_if(x * sm + sa, sr);
+  }
+}
+
+// ---------------------------------------------------------------- epilogue bodies
 
 // Dense column-major C/D, transforms pre-decoded to affine(+relu).  Per warp: 32 rows (one
 // per lane, TMEM lane quarter) x COLS columns in chunks of 32; C for the next chunk is in
@@ -231,16 +278,7 @@ __device__ __forceinline__ void epilogue_dense(const TcParams& p, uint64_t* tful
       if constexpr (SK) sk_gather(sk, j0 - jbase + (jbase % BN), pv);
       tmem_ld_wait();
       float out[32];
-#pragma unroll
-      for (int jj = 0; jj < 32; ++jj) {
-        float v = __uint_as_float(r[jj]);
-        if constexpr (SK) v = pv[jj] + v;
-        if (p.affine) v = p.aff_s * v + (rterm + __shfl_sync(0xffffffffu, qcol, jj));
-        if (has_c) v = relu_if(cv[jj] * p.c_mul[0] + p.c_add[0], p.c_relu) + v;
-        v = relu_if(v * p.r_mul[0] + p.r_add[0], p.r_relu);
-        v = v + (p.bias_axis == 1 ? __shfl_sync(0xffffffffu, bcol, jj) : bias_m);
-        out[jj] = relu_if(v * p.s_mul[0] + p.s_add[0], p.s_relu);
-      }
+      epi_math_real<SK>(p, r, cv, pv, has_c, rterm, bias_m, bcol, qcol, out);
       if (ch + 1 < COLS / 32) load_c(j0 + 32);
       if (row_ok) {
 #pragma unroll
@@ -343,16 +381,7 @@ __device__ __forceinline__ void epilogue_stream(const TcParams& p, uint64_t* tfu
     tmem_ld_wait();
     if (ch == 0) TK_TS_EPI(8);
     float out[32];
-#pragma unroll
-    for (int jj = 0; jj < 32; ++jj) {
-      float v = __uint_as_float(r[jj]);
-      if constexpr (SK) v = pv[jj] + v;
-      if (p.affine) v = p.aff_s * v + (rterm + __shfl_sync(0xffffffffu, qcol, jj));
-      if (has_c) v = relu_if(cv[jj] * p.c_mul[0] + p.c_add[0], p.c_relu) + v;
-      v = relu_if(v * p.r_mul[0] + p.r_add[0], p.r_relu);
-      v = v + (p.bias_axis == 1 ? __shfl_sync(0xffffffffu, bcol, jj) : bias_m);
-      out[jj] = relu_if(v * p.s_mul[0] + p.s_add[0], p.s_relu);
-    }
+    epi_math_real<SK>(p, r, cv, pv, has_c, rterm, bias_m, bcol, qcol, out);
     if (ch == 0) TK_TS_EPI(9);
     if (p.d_tma) {
 #pragma unroll
