@@ -392,9 +392,13 @@ __device__ __forceinline__ void epilogue_stream(const TcParams& p, uint64_t* tfu
         tma_store_2d(&p.tdmap, box, row0, j0);   // the map clips rows >= M / columns >= N
         bulk_commit();
         if (ch == 0) TK_TS_EPI(10);
-        if (has_c) {  // hand the previous chunk's slot back once its store has read it
-          bulk_wait_read<1>();
-          if (cq > 0) mbar_arrive(&cempty[(cq - 1) % CSLOTS]);
+        if (has_c) {
+          // hand a slot back once its store has read it.  Streaming rings release the previous
+          // chunk's slot (the loader runs one chunk ahead); a deep ring (>= 4 slots, used when
+          // the whole C block is prefetched) lets CSLOTS-1 stores stay in flight instead
+          constexpr int LAG = CSLOTS >= 4 ? CSLOTS - 1 : 1;
+          bulk_wait_read<LAG>();
+          if (cq >= uint32_t(LAG)) mbar_arrive(&cempty[(cq - LAG) % CSLOTS]);
         }
       }
     } else {
