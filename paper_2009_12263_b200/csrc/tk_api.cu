@@ -916,6 +916,9 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
                decode_affine(p->t_c, pair, prm.c_mul, prm.c_add, prm.c_relu) &&
                decode_affine(p->t_r2s, pair, prm.r_mul, prm.r_add, prm.r_relu) &&
                decode_affine(p->t_s2g, pair, prm.s_mul, prm.s_add, prm.s_relu);
+  prm.c_ident = p->t_c.n == 0;
+  prm.r_ident = p->t_r2s.n == 0;
+  prm.s_ident = p->t_s2g.n == 0;
   // HBM-bound shapes (diagonal A, K <= 4 block-K steps): C streamed through TMA by a loader warp
   const int ov = tc_kernel_override();
   // the CTA pair takes every real-operator shape with more than 4 block-K steps and at least

@@ -106,6 +106,7 @@ struct TcParams {
   int32_t num_units, sk_first, sk_parts, dbg_cta;
   int32_t vec_ok, serp;          // diag_stream_kernel: 16-byte vector path legal; pair kernel: serpentine K
   int32_t pdl, pad5;             // pair kernel launched with programmatic stream serialisation
+  int32_t c_ident, r_ident, s_ident, pad6;  // empty transform programs: skip the stage entirely
   float* sk_ws;
   int32_t* sk_flags;
 };
@@ -201,7 +202,7 @@ __device__ __forceinline__ void epi_math_real(const TcParams& p, const uint32_t 
                                               const float (&cv)[32], const float (&pv)[SK ? 32 : 1],
                                               bool has_c, float rterm, float bias_m, float bcol,
                                               float qcol, float (&out)[32]) {
-  float v[32], add[32];
+  float v[32];
 #pragma unroll
   for (int jj = 0; jj < 32; ++jj) v[jj] = __uint_as_float(r[jj]);
   if constexpr (SK) {
@@ -212,26 +213,38 @@ __device__ __forceinline__ void epi_math_real(const TcParams& p, const uint32_t 
 #pragma unroll
     for (int jj = 0; jj < 32; ++jj) v[jj] = p.aff_s * v[jj] + (rterm + __shfl_sync(0xffffffffu, qcol, jj));
   }
+  if (has_c) {
+    if (p.c_ident) {  // identity g2s_c (the reference's default): acc starts from C itself
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) v[jj] = cv[jj] + v[jj];
+    } else {
+      const float cm = p.c_mul[0], ca = p.c_add[0];
+      const int cr = p.c_relu;
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) v[jj] = relu_if(cv[jj] * cm + ca, cr) + v[jj];
+    }
+  }
+  if (!p.r_ident) {
+    const float rm = p.r_mul[0], ra = p.r_add[0];
+    const int rr = p.r_relu;
+#pragma unroll
+    for (int jj = 0; jj < 32; ++jj) v[jj] = relu_if(v[jj] * rm + ra, rr);
+  }
   if (p.bias_axis == 1) {
 #pragma unroll
-    for (int jj = 0; jj < 32; ++jj) add[jj] = __shfl_sync(0xffffffffu, bcol, jj);
+    for (int jj = 0; jj < 32; ++jj) v[jj] = v[jj] + __shfl_sync(0xffffffffu, bcol, jj);
+  } else if (p.bias_axis == 2) {
+#pragma unroll
+    for (int jj = 0; jj < 32; ++jj) v[jj] = v[jj] + bias_m;
+  }
+  if (!p.s_ident) {
+    const float sm = p.s_mul[0], sa = p.s_add[0];
+    const int sr = p.s_relu;
+#pragma unroll
+    for (int jj = 0; jj < 32; ++jj) out[jj] = relu_if(v[jj] * sm + sa, sr);
   } else {
 #pragma unroll
-    for (int jj = 0; jj < 32; ++jj) add[jj] = bias_m;
-  }
-  if (has_c) {
-    const float cm = p.c_mul[0], ca = p.c_add[0];
-    const int cr = p.c_relu;
-#pragma unroll
-    for (int jj = 0; jj < 32; ++jj) v[jj] = relu_if(cv[jj] * cm + ca, cr) + v[jj];
-  }
-  const float rm = p.r_mul[0], ra = p.r_add[0], sm = p.s_mul[0], sa = p.s_add[0];
-  const int rr = p.r_relu, sr = p.s_relu;
-#pragma unroll
-  for (int jj = 0; jj < 32; ++jj) {
-    float x = relu_if(v[jj] * rm + ra, rr);
-    x = x + add[jj];
-    out[jj] = relu_if(x * sm + sa, sr);
+    for (int jj = 0; jj < 32; ++jj) out[jj] = v[jj];
   }
 }
 
@@ -716,12 +729,12 @@ __global__ void __launch_bounds__(256) diag_stream_kernel(const __grid_constant_
   const bool has_c = !p.c_zero;
   const int64_t rows4 = (int64_t(p.m) + 3) / 4;
   const int64_t kdiag = p.k < p.m ? p.k : p.m;  // rows with a diagonal entry
-  auto epi = [&](float acc, float c, float bias) {
+  auto epi = [&](float acc, float c, float bias) {  // epi_math_real, one element
     float v = acc;
-    if (has_c) v = relu_if(c * p.c_mul[0] + p.c_add[0], p.c_relu) + v;
-    v = relu_if(v * p.r_mul[0] + p.r_add[0], p.r_relu);
-    v = v + bias;
-    return relu_if(v * p.s_mul[0] + p.s_add[0], p.s_relu);
+    if (has_c) v = (p.c_ident ? c : relu_if(c * p.c_mul[0] + p.c_add[0], p.c_relu)) + v;
+    if (!p.r_ident) v = relu_if(v * p.r_mul[0] + p.r_add[0], p.r_relu);
+    if (p.bias_axis) v = v + bias;
+    return p.s_ident ? v : relu_if(v * p.s_mul[0] + p.s_add[0], p.s_relu);
   };
   for (int64_t j = blockIdx.y; j < p.n; j += gridDim.y) {
     const float bias_j = p.bias_axis == 1 ? p.bias[j] : 0.f;
