@@ -982,7 +982,12 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
     }
     if (ov == 2 || (ov == 0 && pair_ok)) {
       tk::TcParams pp = prm;
-      int nsub = 1;
+      // 256 x 512 pair tiles (two MMAs share each A tile: 25 % fewer L2->SM bytes per flop, so
+      // more flops per joule under the power cap) once K is long enough to amortise their
+      // exposed single-accumulator drain and there are >= 4 waves of them; measured:
+      // 8192^3 +1 %, 16384^3 +13 % (burst) / +22 % (sustained), 6144^3 -3 % (so not there)
+      const int64_t tiles2 = ((p->m + 255) / 256) * ((p->n + 511) / 512);
+      int nsub = (p->k >= 8192 && tiles2 >= 4 * int64_t(pair_clusters())) ? 2 : 1;
       if (const char* e = getenv("TK_PAIR_NSUB")) nsub = atoi(e) == 2 ? 2 : 1;
       int mn;
       int64_t pitch;
@@ -1031,7 +1036,7 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
         if (!prm.c_zero && (rc = make_map_2d(&pp.tcmap, c, TK_F32, p->m, p->n, prm.ldc, 32, 32))) return rc;
         if ((rc = make_map_2d(&pp.tdmap, d, TK_F32, p->m, p->n, prm.ldd, 32, 32))) return rc;
         pp.d_tma = 1;
-        pp.c_pf_kb = nsub == 2 ? 16 : 0;
+        pp.c_pf_kb = 0;  // L2 prefetch of the next drain's C: measured neutral-to-negative
         if (const char* e = getenv("TK_C_PF")) pp.c_pf_kb = atoi(e);
         pp.c_pf_kb = std::min(pp.c_pf_kb, pp.kb_total);
         return nsub == 2 ? launch_tc_pair<true, true, 2>(pp, s) : launch_tc_pair_bni<true, true>(pp, bni, s);
