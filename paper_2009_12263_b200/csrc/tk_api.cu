@@ -198,7 +198,7 @@ void dense_operand(TkLayout& L, int64_t rows, int64_t cols) {
 // GETT-as-GEMM (tensor contraction, reference api.py:259-290): A's M index has two digits
 // (e0, s0), (e1, s1) and D's M digits are the same extents with the order swapped into a
 // dense run (t1 == 1, t0 == e1).  Rewrite to a plain column-major GEMM over m' = m1 + e1*m0:
-// A is permuted once into a dense M' x K workspace (swap_digits_kernel), D (and C) become
+// A is permuted once into a dense M' x K workspace (pack_half_kernel), D (and C) become
 // column-major with the N stride as leading dimension.
 bool permuted_plan(const TkGemmPlan* p, TkGemmPlan* out) {
   const TkLayout& A = p->a;
@@ -652,91 +652,111 @@ bool colmajor_dense(const TkLayout& L, int64_t& ld) {
   return true;
 }
 
+// Gather one half operand (any digit map, both planes of a pair) into a dense column-major
+// rows x cols workspace with pack_half_kernel.  Digits chained in both the source and the
+// destination (e.g. a GETT index that stays adjacent to its neighbour) are merged first, so a
+// permutation of two blocks becomes one wide 2-D transpose instead of many narrow ones.
+int launch_pack(const TkLayout& L, const void* src, uint16_t* dst, int64_t rows, int64_t cols, cudaStream_t s) {
+  tk::PackDesc pd;
+  memset(&pd, 0, sizeof(pd));
+  int64_t q = 1;
+  for (int d = 0; d < 2; ++d) {
+    if (d == 1) q = rows;
+    for (int t = 0; t < L.ndigits[d]; ++t) {
+      pd.ext[pd.n] = L.ext[d][t];
+      pd.ss[pd.n] = L.stride[d][t];
+      pd.ds[pd.n] = q;
+      q *= L.ext[d][t];
+      ++pd.n;
+    }
+  }
+  // merge digit j into i when j continues i in both tensors
+  for (bool again = true; again;) {
+    again = false;
+    for (int i = 0; i < pd.n && !again; ++i)
+      for (int j = 0; j < pd.n && !again; ++j)
+        if (i != j && pd.ss[j] == pd.ss[i] * pd.ext[i] && pd.ds[j] == pd.ds[i] * pd.ext[i]) {
+          pd.ext[i] *= pd.ext[j];
+          for (int t = j; t + 1 < pd.n; ++t) {
+            pd.ext[t] = pd.ext[t + 1];
+            pd.ss[t] = pd.ss[t + 1];
+            pd.ds[t] = pd.ds[t + 1];
+          }
+          --pd.n;
+          again = true;
+        }
+  }
+  for (int t = 0; t < pd.n; ++t)
+    if (pd.ss[t] < pd.ss[pd.fs] || (pd.ss[t] == pd.ss[pd.fs] && pd.ext[t] > pd.ext[pd.fs])) pd.fs = t;
+  pd.fd = 0;  // first row digit: destination stride 1
+  if (pd.fd == pd.fs) {
+    pd.fd = -1;
+    for (int t = 0; t < pd.n; ++t)
+      if (t != pd.fs && (pd.fd < 0 || pd.ds[t] < pd.ds[pd.fd])) pd.fd = t;
+    if (pd.fd < 0) {  // single digit: pad with a unit digit
+      pd.ext[pd.n] = 1;
+      pd.ss[pd.n] = pd.ds[pd.n] = 0;
+      pd.fd = pd.n++;
+    }
+  }
+  // 16-byte vectors: unit stride along the vector digit, extents and every other stride
+  // multiples of 8 elements, 16-byte aligned base (interleaved pairs read scalar-wise)
+  auto all8 = [&](const int64_t* st, int skip) {
+    for (int t = 0; t < pd.n; ++t)
+      if (t != skip && (st[t] % 8) != 0) return false;
+    return true;
+  };
+  const int64_t pl_off = L.pair == TK_PAIR_SPLIT ? L.plane_stride : 0;
+  pd.vec_rd = L.pair != TK_PAIR_INTERLEAVED && pd.ss[pd.fs] == 1 && pd.ext[pd.fs] % 8 == 0 &&
+              all8(pd.ss, pd.fs) && pl_off % 8 == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+  pd.wr_x = pd.ds[pd.fs] < pd.ds[pd.fd];
+  const int wd = pd.wr_x ? pd.fs : pd.fd;
+  pd.vec_wr = pd.ds[wd] == 1 && pd.ext[wd] % 8 == 0 && all8(pd.ds, wd) &&
+              (rows * cols) % 8 == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+  pd.tiles_s = (pd.ext[pd.fs] + 63) / 64;
+  pd.tiles_d = (pd.ext[pd.fd] + 63) / 64;
+  pd.outer = 1;
+  for (int t = 0; t < pd.n; ++t)
+    if (t != pd.fs && t != pd.fd) pd.outer *= pd.ext[t];
+  const int64_t blocks = pd.tiles_s * pd.tiles_d * pd.outer;
+  const unsigned grid = unsigned(std::min<int64_t>(blocks, 64 * sm_count()));
+  for (int pl = 0; pl < (L.pair ? 2 : 1); ++pl) {
+    tk::pack_half_kernel<<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(src), dst + pl * rows * cols, pd,
+                                              L.pair, L.plane_stride, pl);
+    TK_CUDA(cudaGetLastError());
+    ++g_launches;
+  }
+  return TK_OK;
+}
+
 int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, void* d, const void* bias,
            uint8_t* ws, const Workspace& w, cudaStream_t s) {
   TkGemmPlan rewritten;
   const TkGemmPlan* p = p0;
   if (w.a_perm >= 0 && permuted_plan(p0, &rewritten)) {
-    const TkLayout& A = p0->a;
+    // A's two M digits swapped (m' = m1 + e1*m0) and gathered into a dense M' x K workspace
+    TkLayout A = p0->a;
+    std::swap(A.ext[0][0], A.ext[0][1]);
+    std::swap(A.stride[0][0], A.stride[0][1]);
     uint16_t* at = reinterpret_cast<uint16_t*>(ws + w.a_perm);
-    const dim3 grid(unsigned((A.ext[0][0] + 63) / 64), unsigned((A.ext[0][1] + 63) / 64), unsigned(p0->k));
-    tk::swap_digits_kernel<<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(a), at, A.ext[0][0],
-                                                A.stride[0][0], A.ext[0][1], A.stride[0][1], p0->k,
-                                                A.stride[1][0]);
-    TK_CUDA(cudaGetLastError());
-    ++g_launches;
+    int rc0 = launch_pack(A, a, at, p0->m, p0->k, s);
+    if (rc0) return rc0;
     a = at;
     p = &rewritten;
   }
   TkGemmPlan packed;
   if (w.a_pack >= 0 || w.b_pack >= 0) {
     packed = *p;
-    auto pack = [&](const TkLayout& L, const void* src, uint16_t* dst, int64_t rows, int64_t cols) -> int {
-      tk::PackDesc pd;
-      memset(&pd, 0, sizeof(pd));
-      int64_t q = 1;
-      for (int d = 0; d < 2; ++d) {
-        if (d == 1) q = rows;
-        for (int t = 0; t < L.ndigits[d]; ++t) {
-          pd.ext[pd.n] = L.ext[d][t];
-          pd.ss[pd.n] = L.stride[d][t];
-          pd.ds[pd.n] = q;
-          q *= L.ext[d][t];
-          ++pd.n;
-        }
-      }
-      for (int t = 0; t < pd.n; ++t)
-        if (pd.ss[t] < pd.ss[pd.fs] || (pd.ss[t] == pd.ss[pd.fs] && pd.ext[t] > pd.ext[pd.fs])) pd.fs = t;
-      pd.fd = 0;  // first row digit: destination stride 1
-      if (pd.fd == pd.fs) {
-        pd.fd = -1;
-        for (int t = 0; t < pd.n; ++t)
-          if (t != pd.fs && (pd.fd < 0 || pd.ds[t] < pd.ds[pd.fd])) pd.fd = t;
-        if (pd.fd < 0) {  // single digit: pad with a unit digit
-          pd.ext[pd.n] = 1;
-          pd.ss[pd.n] = pd.ds[pd.n] = 0;
-          pd.fd = pd.n++;
-        }
-      }
-      // 16-byte vectors: unit stride along the vector digit, extents and every other stride
-      // multiples of 8 elements, 16-byte aligned base (interleaved pairs read scalar-wise)
-      auto all8 = [&](const int64_t* st, int skip) {
-        for (int t = 0; t < pd.n; ++t)
-          if (t != skip && (st[t] % 8) != 0) return false;
-        return true;
-      };
-      const int64_t pl_off = L.pair == TK_PAIR_SPLIT ? L.plane_stride : 0;
-      pd.vec_rd = L.pair != TK_PAIR_INTERLEAVED && pd.ss[pd.fs] == 1 && pd.ext[pd.fs] % 8 == 0 &&
-                  all8(pd.ss, pd.fs) && pl_off % 8 == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0;
-      pd.wr_x = pd.ds[pd.fs] < pd.ds[pd.fd];
-      const int wd = pd.wr_x ? pd.fs : pd.fd;
-      pd.vec_wr = pd.ds[wd] == 1 && pd.ext[wd] % 8 == 0 && all8(pd.ds, wd) &&
-                  (rows * cols) % 8 == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
-      pd.tiles_s = (pd.ext[pd.fs] + 63) / 64;
-      pd.tiles_d = (pd.ext[pd.fd] + 63) / 64;
-      pd.outer = 1;
-      for (int t = 0; t < pd.n; ++t)
-        if (t != pd.fs && t != pd.fd) pd.outer *= pd.ext[t];
-      const int64_t blocks = pd.tiles_s * pd.tiles_d * pd.outer;
-      const unsigned grid = unsigned(std::min<int64_t>(blocks, 64 * sm_count()));
-      for (int pl = 0; pl < (L.pair ? 2 : 1); ++pl) {
-        tk::pack_half_kernel<<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(src), dst + pl * rows * cols, pd,
-                                                  L.pair, L.plane_stride, pl);
-        TK_CUDA(cudaGetLastError());
-        ++g_launches;
-      }
-      return TK_OK;
-    };
     int rc;
     if (w.a_pack >= 0) {
       uint16_t* dst = reinterpret_cast<uint16_t*>(ws + w.a_pack);
-      if ((rc = pack(p->a, a, dst, p->m, p->k))) return rc;
+      if ((rc = launch_pack(p->a, a, dst, p->m, p->k, s))) return rc;
       dense_operand(packed.a, p->m, p->k);
       a = dst;
     }
     if (w.b_pack >= 0) {
       uint16_t* dst = reinterpret_cast<uint16_t*>(ws + w.b_pack);
-      if ((rc = pack(p->b, b, dst, p->k, p->n))) return rc;
+      if ((rc = launch_pack(p->b, b, dst, p->k, p->n, s))) return rc;
       dense_operand(packed.b, p->k, p->n);
       b = dst;
     }

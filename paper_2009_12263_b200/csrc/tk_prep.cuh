@@ -76,33 +76,6 @@ __global__ void strided_sum_unit_kernel(const H* __restrict__ x, float* __restri
 }  // namespace tk
 
 namespace tk {
-// Two-digit M permutation of the A operand (tensor contraction, reference api.py:259-290):
-// A(m, k) lives at (m % e0) * s0 + (m / e0) * s1 + k * sk  (M digits (e0, s0), (e1, s1));
-// write the dense column-major M' x K matrix At with m' = (m / e0) + e1 * (m % e0), i.e. the
-// M digits swapped so that D's fastest index becomes A's fastest row.  64x64 tiles through
-// shared memory keep both the reads (along digit 0) and the writes (along digit 1) coalesced.
-__global__ void swap_digits_kernel(const uint16_t* __restrict__ a, uint16_t* __restrict__ at,
-                                   int64_t e0, int64_t s0, int64_t e1, int64_t s1, int64_t k,
-                                   int64_t sk) {
-  __shared__ uint16_t tile[64][65];
-  const int64_t kk = blockIdx.z;
-  const int64_t i0 = int64_t(blockIdx.x) * 64;  // digit-0 index block
-  const int64_t j0 = int64_t(blockIdx.y) * 64;  // digit-1 index block
-  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 256 threads: 64 x 4
-  for (int r = ty; r < 64; r += 4) {
-    const int64_t i = i0 + tx, j = j0 + r;
-    if (i < e0 && j < e1) tile[r][tx] = a[i * s0 + j * s1 + kk * sk];
-  }
-  __syncthreads();
-  const int64_t mtot = e0 * e1;
-  for (int r = ty; r < 64; r += 4) {
-    const int64_t i = i0 + r, j = j0 + tx;
-    if (i < e0 && j < e1) at[(j + e1 * i) + kk * mtot] = tile[tx][r];
-  }
-}
-}  // namespace tk
-
-namespace tk {
 
 // Gather one plane of a half-precision operand stored under an arbitrary digit map (the
 // StridedPermutation / GETT layouts, reference layouts.py:435-506) into a dense column-major
