@@ -481,7 +481,9 @@ int launch_tc_pair(const tk::TcParams& prm, cudaStream_t s) {
     const char* e = getenv("TK_PDL");
     return !e || atoi(e);
   }();
-  run.pdl = pdl ? 1 : 0;
+  // not after the split-K flag memset: a programmatic launch may start before a preceding
+  // memset node completes, and the flags must be zero before any part counts in
+  run.pdl = (pdl && run.sk_parts == 1) ? 1 : 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(tk::TC_THREADS);
@@ -491,7 +493,7 @@ int launch_tc_pair(const tk::TcParams& prm, cudaStream_t s) {
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = run.pdl ? 1 : 0;
   TK_CUDA(cudaLaunchKernelEx(&cfg, kern, run));
   ++g_launches;
   return TK_OK;
@@ -525,7 +527,9 @@ SplitPlan split_plan(int64_t tiles, int clusters, int kb_total, int bnp) {
   if (r == 0 || r > clusters / 2) return sp;
   // >= 64 block-K steps per part: below that the partial hand-off costs what the wave gains
   // (measured: 4096^3 -2 %, 4096x4096x16384 +6.5 %, 1536x4096x16384 +13 %)
-  int parts = int(std::min<int64_t>(std::min<int64_t>(4, clusters / r), kb_total / 64));
+  int min_kb = 64;
+  if (const char* e = getenv("TK_SPLITK_MINKB")) min_kb = std::max(1, atoi(e));
+  int parts = int(std::min<int64_t>(std::min<int64_t>(4, clusters / r), kb_total / min_kb));
   if (const char* e = getenv("TK_SPLITK_S")) parts = std::max(1, std::min(parts, atoi(e)));
   if (parts < 2) return sp;
   sp.first = int(tiles - r);
