@@ -131,6 +131,43 @@ def test_split_k_last_wave(cuda, mnk, splitk, monkeypatch):
             assert O.rel_err(got, want) <= O.tolerance(k), O.rel_err(got, want)
 
 
+@pytest.mark.parametrize("trans", ["nn", "tt"])
+def test_full_size_c3_tile_shapes_agree(cuda, trans, monkeypatch):
+    """The bench-size (8192^3) C3 epilogue (alpha/beta, bias, ReLU) on the default 256 x 512
+    pair tiles against 256 x 256 tiles (same k order with serpentine off: bitwise equal), and
+    sampled rows against the float64 product (size-independent checks at full size)."""
+    m = n = k = 8192
+    ta, tb = trans[0] == "t", trans[1] == "t"
+    g = torch.Generator(device=cuda)
+    g.manual_seed(21)
+    a = torch.randn(m * k, generator=g, device=cuda).half()
+    b = torch.randn(k * n, generator=g, device=cuda).half()
+    c = torch.randn(m * n, generator=g, device=cuda)
+    bias = torch.randn(n, generator=g, device=cuda)
+    al, be = 1.5, 0.5
+    cfg = dataclasses.replace(
+        tk.build_dense_config(m, n, k, np.float16, trans_a=ta, trans_b=tb),
+        transform_g2s_c=tk.components.scale(be / al), transform_r2s_d=tk.components.scale(al),
+        epilogue=tk.components.BiasEpilogue(bias), transform_s2g_d=tk.components.relu)
+    monkeypatch.setenv("TK_SERPENTINE", "0")
+    outs = []
+    for nsub in ("2", "1"):
+        monkeypatch.setenv("TK_PAIR_NSUB", nsub)
+        d = torch.empty(m * n, device=cuda)
+        tk.matmul(cfg, a, b, c, d)
+        outs.append(d)
+    assert torch.equal(outs[0], outs[1])
+    # rows 0..3 and 4096..4099 against float64
+    A = (a.view(m, k) if ta else a.view(k, m).t()).double()     # logical m x k
+    B = (b.view(k, n) if tb else b.view(n, k).t()).double()     # logical k x n
+    C = c.view(n, m).t().double()
+    D = outs[0].view(n, m).t()
+    for r0 in (0, 4096):
+        ref = torch.relu(al * (A[r0:r0 + 4] @ B + (be / al) * C[r0:r0 + 4]) + bias.double()[None, :])
+        err = ((D[r0:r0 + 4].double() - ref).abs().max() / ref.abs().max()).item()
+        assert err <= O.tolerance(k), err
+
+
 def test_fused_affine_bias_relu(cuda):
     m, n, k = 512, 384, 256
     rng = np.random.default_rng(2)
