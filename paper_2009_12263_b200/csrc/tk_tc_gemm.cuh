@@ -106,7 +106,8 @@ struct TcParams {
   int32_t num_units, sk_first, sk_parts, dbg_cta;
   int32_t vec_ok, serp;          // diag_stream_kernel: 16-byte vector path legal; pair kernel: serpentine K
   int32_t pdl, pad5;             // pair kernel launched with programmatic stream serialisation
-  int32_t c_ident, r_ident, s_ident, pad6;  // empty transform programs: skip the stage entirely
+  int32_t c_ident, r_ident, s_ident, nar_units;  // empty transform programs: skip the stage;
+                                                 // pair NSUB 2: half-width first units (stagger)
   float* sk_ws;
   int32_t* sk_flags;
 };

@@ -68,13 +68,22 @@ struct Tc2Plan {
 // One unit of the pair kernel's static schedule: a whole tile, or K-part `part` of a split tile
 // (role 1: leaves a partial, role 2: the last part, reduces the partials in its epilogue).
 struct PairUnit {
-  int tile, kb0, kb1, role, sk_tile, part;
+  int tile, kb0, kb1, role, sk_tile, part, noff, narrow;
 };
+// NSUB 2 with a staggered start: units [0, nar_units) are the two 256-column halves of the
+// first nar_units/2 wide tiles; dealt round-robin, half of the clusters begin with a half-width
+// tile and run half a tile out of phase with the other half for the rest of the launch, so the
+// clusters' single-accumulator drains (C read + D write, HBM-bound when all clusters drain
+// together) alternate instead of coinciding.
 __device__ __forceinline__ PairUnit pair_unit(const TcParams& p, int u) {
-  if (u < p.sk_first) return PairUnit{u, 0, p.kb_total, 0, 0, 0};
+  if (p.nar_units > 0) {
+    if (u < p.nar_units) return PairUnit{u >> 1, 0, p.kb_total, 0, 0, 0, (u & 1) * 256, 1};
+    return PairUnit{(p.nar_units >> 1) + u - p.nar_units, 0, p.kb_total, 0, 0, 0, 0, 0};
+  }
+  if (u < p.sk_first) return PairUnit{u, 0, p.kb_total, 0, 0, 0, 0, 0};
   const int v = u - p.sk_first, r = v / p.sk_parts, s = v - r * p.sk_parts;
   return PairUnit{p.sk_first + r, s * p.kb_total / p.sk_parts, (s + 1) * p.kb_total / p.sk_parts,
-                  s == p.sk_parts - 1 ? 2 : 1, r, s};
+                  s == p.sk_parts - 1 ? 2 : 1, r, s, 0, 0};
 }
 
 template <bool DENSE_EPI, bool CSTREAM = false, int NSUB = 1, int BNI = 256, int CSL = TC2S_CSLOTS>
@@ -160,7 +169,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         if (un.role == 1) continue;  // partial K-parts never read C
         int mb, nb;
         tile_coords(p, un.tile, mb, nb);
-        for (int ch = 0; ch < NSUB * CH; ++ch, ++q) {
+        for (int ch = 0; ch < (un.narrow ? 1 : NSUB) * CH; ++ch, ++q) {
           const uint32_t slot = q % CSL, ph = (q / CSL) & 1;
           for (int w = 0; w < TC_EPI_WARPS; ++w) {
             const int bi = w * CSL + int(slot);
@@ -168,7 +177,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
             mbar_arrive_expect_tx(&cfull[bi], TC_CBOX_BYTES);
             tma_load_2d(smem + PL::CRING + bi * TC_CBOX_BYTES, &p.tcmap, &cfull[bi],
                         mb * 256 + int(rank) * 128 + (w & 3) * 32,
-                        nb * BNP + (ch / CH) * BNI + (w >> 2) * PL::WCOLS + (ch % CH) * 32,
+                        nb * BNP + un.noff + (ch / CH) * BNI + (w >> 2) * PL::WCOLS + (ch % CH) * 32,
                         policy_evict_normal());
           }
         }
@@ -186,7 +195,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         int mb, nb;
         tile_coords(p, un.tile, mb, nb);
         const int m0 = mb * 256 + int(rank) * 128;     // this CTA's rows of A
-        const int n0 = nb * BNP + int(rank) * (BNI / 2);  // this CTA's columns of B (per MMA)
+        const int n0 = nb * BNP + un.noff + int(rank) * (BNI / 2);  // this CTA's columns of B (per MMA)
+        const int nsub_u = un.narrow ? 1 : NSUB;
         // serpentine K (opt-in): every other tile of a cluster walks K downwards, so the next
         // wave starts on the K-slices the previous one loaded last (still in L2)
         const bool rev = NSUB == 1 && p.serp && (lu & 1);
@@ -205,7 +215,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
               for (int c = 0; c < BNP / 32; ++c)
                 tma_prefetch_l2_2d(&p.tcmap, mb * 256 + int(rank) * 128 + r * 32, nb * BNP + c * 32);
           }
-          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * PL::STAGE_BYTES);
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (TC2_TILE_BYTES + nsub_u * PL::B_BYTES));
           const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
           if (p.a_mn && (p.mn3d & 1)) {
             tma_load_3d_pair(a_tile(stage), &p.ta[0], fb, 0, k0, m0 >> 6, pol);
@@ -217,6 +227,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           }
 #pragma unroll
           for (int sub = 0; sub < NSUB; ++sub) {
+            if (sub >= nsub_u) break;
             uint8_t* bt = b_tile(stage) + sub * PL::B_BYTES;
             const int nn = n0 + sub * BNI;
             if (p.b_mn && (p.mn3d & 2)) {
@@ -278,6 +289,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           const uint32_t tph = (local & 1) ^ 1;
           mbar_wait(&tempty[0], tph);
           tc_fence_after();
+          if (un.narrow) {  // half-width tile: lo columns only (its epilogue also releases hi)
+            for (int kb = 0; kb < p.kb_total; ++kb) {
+              mbar_wait(&full[stage], phase);
+              tc_fence_after();
+              issue(stage, 0, tmem_base, kb == 0);
+              tc_commit_pair(&empty[stage], 0x3);
+              if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            }
+            tc_commit_pair(&tfull[0], 0x3);
+            continue;
+          }
           bool hi_ok = false;
           int held = 0, st0 = stage;
           for (int kb = 0; kb < p.kb_total; ++kb) {
@@ -374,37 +396,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       // NSUB 1: accumulator `local & 1`, one pass over this warp's 128 columns.
       // NSUB 2: one accumulator, pass 0 drains columns [0,256), pass 1 [256,512) (128 per warp).
 #pragma unroll 1
-      for (int pass = 0; pass < NSUB; ++pass) {
+      for (int pass = 0; pass < (un.narrow ? 1 : NSUB); ++pass) {
         const int as = NSUB == 1 ? (local & 1) : 0;
         const uint32_t aphase = NSUB == 1 ? ((local >> 1) & 1) : (local & 1);
         const uint32_t tbase = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(as * BNI);
-        const int jbase = nb * BNP + pass * BNI + half * PL::WCOLS;
+        // (a half-width tile sits in TMEM columns [0,256): shift the base by its column offset)
+        const uint32_t tb = tbase - uint32_t(un.noff);
+        const int jbase = nb * BNP + un.noff + pass * BNI + half * PL::WCOLS;
         if (blockIdx.x == p.dbg_cta && warp == 4 && lane == 0 && u + nclusters >= p.num_units) {
           mbar_wait(tfull + as, aphase);
           TK_TS(4);
         }
         if (CSTREAM) {
           if (sk.p)
-            epilogue_stream<PL::WCOLS, BNP, CSL, true>(p, tfull + as, aphase, tbase, i, jbase, lane, my_ring,
+            epilogue_stream<PL::WCOLS, BNP, CSL, true>(p, tfull + as, aphase, tb, i, jbase, lane, my_ring,
                                                    cfull + ew * CSL, cempty + ew * CSL, cq,
                                                    row0, sk);
           else
-            epilogue_stream<PL::WCOLS, BNP, CSL>(p, tfull + as, aphase, tbase, i, jbase, lane, my_ring,
+            epilogue_stream<PL::WCOLS, BNP, CSL>(p, tfull + as, aphase, tb, i, jbase, lane, my_ring,
                                                    cfull + ew * CSL, cempty + ew * CSL, cq, row0);
         } else if (p.dbg_skip_epi) {
           mbar_wait_sleep(tfull + as, aphase);
           tc_fence_after();
         } else if (DENSE_EPI) {
           if (sk.p)
-            epilogue_dense<OP_REAL, PL::WCOLS, BNP, true>(p, tfull + as, aphase, tbase, i, jbase, lane, sk);
+            epilogue_dense<OP_REAL, PL::WCOLS, BNP, true>(p, tfull + as, aphase, tb, i, jbase, lane, sk);
           else
-            epilogue_dense<OP_REAL, PL::WCOLS, BNP>(p, tfull + as, aphase, tbase, i, jbase, lane);
+            epilogue_dense<OP_REAL, PL::WCOLS, BNP>(p, tfull + as, aphase, tb, i, jbase, lane);
         } else
-          epilogue_generic<OP_REAL, PL::WCOLS, BNP>(p, tfull + as, aphase, tbase, i, jbase);
+          epilogue_generic<OP_REAL, PL::WCOLS, BNP>(p, tfull + as, aphase, tb, i, jbase);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[NSUB == 1 ? as : pass]), 0));
         if (warp == 4 && lane == 0) TK_TS(5);
+      }
+      if (NSUB == 2 && un.narrow) {  // nothing in the hi columns: release them for the next tile
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[1]), 0));
       }
     }
   }
