@@ -1075,8 +1075,17 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
         pp.d_tma = 1;
         pp.c_pf_kb = 0;  // L2 prefetch of the next drain's C: measured neutral-to-negative
         if (const char* e = getenv("TK_C_PF")) pp.c_pf_kb = atoi(e);
+        pp.c_pf_spread = 0;
+        if (const char* e = getenv("TK_C_PF_SPREAD")) pp.c_pf_spread = atoi(e);
         pp.c_pf_kb = std::min(pp.c_pf_kb, pp.kb_total);
-        return nsub == 2 ? launch_tc_pair<true, true, 2>(pp, s) : launch_tc_pair_bni<true, true>(pp, bni, s);
+        if (nsub == 2) {
+          const char* e = getenv("TK_NSUB2_CSL");  // C-ring slots per warp (tuning)
+          const int csl = e ? atoi(e) : 2;
+          if (csl == 3) return launch_tc_pair<true, true, 2, 256, 3>(pp, s);
+          if (csl == 4) return launch_tc_pair<true, true, 2, 256, 4>(pp, s);
+          return launch_tc_pair<true, true, 2>(pp, s);
+        }
+        return launch_tc_pair_bni<true, true>(pp, bni, s);
       }
       if (nsub == 2) return dense ? launch_tc_pair<true, false, 2>(pp, s) : launch_tc_pair<false, false, 2>(pp, s);
       return dense ? launch_tc_pair_bni<true, false>(pp, bni, s) : launch_tc_pair_bni<false, false>(pp, bni, s);

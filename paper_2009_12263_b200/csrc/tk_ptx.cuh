@@ -111,6 +111,13 @@ __device__ __forceinline__ void tma_prefetch_l2_2d(const CUtensorMap* m, int32_t
                "r"(c0), "r"(c1)
                : "memory");
 }
+__device__ __forceinline__ void tma_prefetch_l2_2d_hint(const CUtensorMap* m, int32_t c0, int32_t c1,
+                                                        uint64_t policy) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile.L2::cache_hint [%0, {%1, %2}], %3;" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(c1), "l"(policy)
+               : "memory");
+}
 // L2 eviction-priority policies (createpolicy.fractional)
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;

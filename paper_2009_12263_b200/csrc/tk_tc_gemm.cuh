@@ -97,7 +97,8 @@ struct TcParams {
   int32_t c_relu, r_relu, s_relu, pad1;
   int32_t dbg_skip_epi, pol_ab;  // tuning/diagnostic knobs (TK_DBG_SKIP_EPI, TK_POLICY_AB)
   int32_t d_tma, mn3d;           // C-streaming epilogue: D via TMA; MN-major operands via 3-D maps (bit0 A, bit1 B)
-  int32_t c_pf_kb, pad2;         // pair kernel: prefetch the tile's C into L2 this many k-blocks before its end
+  int32_t c_pf_kb, c_pf_spread;  // pair kernel: prefetch the tile's C into L2 this many k-blocks before
+                                 // its end; spread: one 4 KB box per k-block over that span (evict_last)
   int32_t c_rmap, d_rmap;        // dense epilogue: C / D row offsets through c_map / d_map (GETT outputs)
   int32_t pol_a, pol_b;          // pair kernel L2 policies for A / B loads: 0 normal, 1 evict_last, 2 evict_first
   // split-K of a poorly filled last wave (pair kernel): units [0, sk_first) are whole tiles,

@@ -53,7 +53,7 @@ struct Tc2Plan {
   static constexpr int CSLOTS = CSL;
   static constexpr int CRING_BYTES = CSTREAM ? TC_EPI_WARPS * CSL * TC_CBOX_BYTES : 0;
   static constexpr int MAX_STAGES = (226 * 1024 - 1536 - CRING_BYTES) / STAGE_BYTES;
-  static constexpr int STAGES = NSUB == 2 ? (CSTREAM ? 3 : 4)
+  static constexpr int STAGES = NSUB == 2 ? (CSTREAM ? (CSL > TC2S_CSLOTS ? MAX_STAGES : 3) : 4)
                               : CSL > TC2S_CSLOTS ? (MAX_STAGES > 8 ? 8 : MAX_STAGES)
                               : BNI == 256 ? (CSTREAM ? TC2S_STAGES : TC2_STAGES)
                               : (MAX_STAGES > 8 ? 8 : MAX_STAGES);
@@ -209,11 +209,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
             continue;
           }
-          if (CSTREAM && kb == p.kb_total - p.c_pf_kb && p.c_pf_kb > 0 && !p.c_zero) {
+          if (CSTREAM && p.c_pf_kb > 0 && !p.c_zero) {
             // warm L2 with this CTA's C block so the (non-overlapped part of the) drain hits L2
-            for (int r = 0; r < 4; ++r)
-              for (int c = 0; c < BNP / 32; ++c)
-                tma_prefetch_l2_2d(&p.tcmap, mb * 256 + int(rank) * 128 + r * 32, nb * BNP + c * 32);
+            const int at = ki - (un.kb1 - un.kb0 - p.c_pf_kb);  // k-blocks into the prefetch span
+            const int nbox = 4 * ((un.narrow ? 256 : BNP) / 32);
+            const int cw = nbox / 4;
+            if (p.c_pf_spread) {
+              if (at >= 0) {
+                const uint64_t pl = policy_evict_last();
+                for (int b = at * nbox / p.c_pf_kb; b < (at + 1) * nbox / p.c_pf_kb; ++b)
+                  tma_prefetch_l2_2d_hint(&p.tcmap, mb * 256 + int(rank) * 128 + (b % 4) * 32,
+                                          nb * BNP + un.noff + (b / 4) * 32, pl);
+                (void)cw;
+              }
+            } else if (at == 0) {
+              for (int r = 0; r < 4; ++r)
+                for (int c = 0; c < cw; ++c)
+                  tma_prefetch_l2_2d(&p.tcmap, mb * 256 + int(rank) * 128 + r * 32, nb * BNP + un.noff + c * 32);
+            }
           }
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (TC2_TILE_BYTES + nsub_u * PL::B_BYTES));
           const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
