@@ -1073,6 +1073,7 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
         if (!prm.c_zero && (rc = make_map_2d(&pp.tcmap, c, TK_F32, p->m, p->n, prm.ldc, 32, 32))) return rc;
         if ((rc = make_map_2d(&pp.tdmap, d, TK_F32, p->m, p->n, prm.ldd, 32, 32))) return rc;
         pp.d_tma = 1;
+        if (const char* e = getenv("TK_PAIR_DTMA")) pp.d_tma = atoi(e);
         pp.c_pf_kb = 0;  // L2 prefetch of the next drain's C: measured neutral-to-negative
         if (const char* e = getenv("TK_C_PF")) pp.c_pf_kb = atoi(e);
         pp.c_pf_spread = 0;
