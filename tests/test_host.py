@@ -473,3 +473,20 @@ def test_gett_config_wiring():
     for bad in ("abc-bd", "abc-bda-dcc", "ab-abc-bc", "abe-bda-dc"):
         with pytest.raises(tk.ConfigError):
             tk.build_gett_config(bad, dict(a=2, b=2, c=2, d=2, e=2), np.float32)
+
+
+@pytest.mark.parametrize("spec,sizes,packed", [
+    ("abc-acd-db", dict(a=64, b=96, c=8, d=136), ()),                 # chained digits merge: no gather
+    ("abc-bda-dc", dict(a=64, b=32, c=128, d=256), ("A",)),          # A's M digits out of order
+    ("abcd-aebf-dfce", dict(a=32, b=8, c=16, d=24, e=16, f=24), ("A", "B")),
+])
+def test_gett_operand_packing_plan(spec, sizes, packed):
+    """Host-side planning of a GETT on the tensor cores (no GPU needed): operands whose digit
+    maps normalise to one strided matrix go straight to the TMA, the others get a dense
+    gather workspace of exactly rows x cols halves."""
+    cfg = kernel.resolve_config(tk.build_gett_config(spec, sizes, np.float16))
+    plan, _, _ = kernel.lower(cfg)
+    assert kernel.plan_lane(plan) == "tcgen05"
+    m, n, k = cfg.params.gemm_shape
+    want = (2 * m * k if "A" in packed else 0) + (2 * k * n if "B" in packed else 0)
+    assert _lib.load().tk_workspace_bytes(plan) == want
