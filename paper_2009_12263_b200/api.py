@@ -431,6 +431,10 @@ def build_gett_config(spec, sizes, dtype=np.float32, *, operator_shape=None,
         raise ConfigError(f"GETT sizes missing {sorted(missing)}")
     ext = {i: int(sizes[i]) for i in set(d_idx + a_idx + b_idx)}
     dtype = np.dtype(dtype)
+    if dtypes.pair_kind(dtype):
+        raise ConfigError("build_gett_config takes real element types (the reference's "
+                          "StridedPermutation GETT is real); use build_complex_config / "
+                          "build_dual_config for pair operators")
     acc = accumulator_dtype(dtype)
     vol = lambda idx: int(np.prod([ext[i] for i in idx]))
     m, n, k = vol(m_idx), vol(n_idx), vol(k_idx)
