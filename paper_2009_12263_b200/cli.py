@@ -119,6 +119,13 @@ def _wide(x):
 
 def prepare(args, rng) -> Case:
     name = args.dtype
+    # like the reference CLI (bench.py:223-254): a pair variant given a real dtype takes the
+    # matching pair type of the same storage width
+    if args.variant == "complex" and not name.startswith("c"):
+        name = {"f16": "c32", "bf16": "c32", "f32": "c64"}.get(name, "c128")
+    elif args.variant == "dual" and not name.startswith("dual"):
+        name = {"f16": "dual16", "bf16": "dual16", "f32": "dual32"}.get(name, "dual64")
+    args.dtype = name
     dt = DTYPES[name]
     v = args.variant
     half = dtypes.is_half(dt)

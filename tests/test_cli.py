@@ -9,7 +9,9 @@ from paper_2009_12263_b200 import cli
 
 
 def test_configuration_errors_exit_2(capsys, tmp_path):
-    assert cli.main(["check", "--variant", "complex", "--dtype", "f16"]) == 2
+    # a real variant with a pair dtype (pair variants map real dtypes to their pair type,
+    # like the reference CLI)
+    assert cli.main(["check", "--variant", "dense", "--dtype", "c64"]) == 2
     assert "configuration error" in capsys.readouterr().err
     sweep = tmp_path / "s.txt"
     sweep.write_text("variant=dense\nbogus=1\n")
