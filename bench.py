@@ -253,6 +253,9 @@ def run_ours(args):
                          "GB_per_s_per_rank": recv / (gms * 1e-3) / 1e9,
                          "collective": "torch.distributed.all_gather_into_tensor (NCCL)",
                          "in_value": False}
+            if args.fused_allgather:
+                allgather["fused"] = fused_allgather(args, tk, torch, dist, dev, stream, a, b, c,
+                                                     m, n, k, world, rank, d)
             del full
         except Exception as exc:
             allgather = {"unavailable": str(exc)[:160]}
@@ -310,6 +313,46 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def fused_allgather(args, tk, torch, dist, dev, stream, a, b, c, m, n, k, world, rank, d):
+    """Opt-in (--fused-allgather): the GEMM whose epilogue TMA-stores every D tile into all
+    ranks' full-D buffers over peer memory (CUDA IPC mappings; NVLink on an NVSwitch box),
+    timed per step as GEMM + gather, checked against the NCCL-gathered D."""
+    from paper_2009_12263_b200 import shard
+
+    try:
+        full = torch.empty(m * n * world, device=dev)
+        peers = shard.PeerBuffers(full)
+        big_b = torch.empty(k * n * world, device=dev, dtype=a.dtype)  # this rank's slab = the
+        big_c = torch.empty(m * n * world, device=dev)                  # bench step's B and C
+        big_b.view(world, -1)[rank].copy_(b)
+        big_c.view(world, -1)[rank].copy_(c)
+        cfg = tk.kernel.resolve_config(tk.build_dense_config(m, n * world, k,
+                                                             tk.FLOAT16 if args.dtype == "fp16" else tk.BFLOAT16))
+        step = lambda: shard.sharded_gemm(cfg, a, big_b, big_c, None, rank=rank, world=world,
+                                          allgather_into=full, fused=True, peers=peers,
+                                          stream=stream, synchronize=False)
+        for _ in range(2):
+            step()
+        reps = max(3, min(args.steps, 10))
+        dist.barrier()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            step()  # includes the device sync + barrier that publish the gathered D
+        ms = (time.perf_counter() - t0) * 1e3 / reps
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ok = bool(torch.equal(full.view(world, -1)[rank], d))  # this rank's slab, as computed
+        mode = tk.last_run().get("peer_mode")
+        peers.close()
+        return {"ms_per_step_gemm_plus_gather": float(t.item()), "peer_mode": mode,
+                "own_slab_matches_bench_step": ok,
+                "how": "tk_gemm_peers: epilogue TMA stores to local + peer slabs (wall clock "
+                       "incl. device sync + barrier per step)"}
+    except Exception as exc:
+        return {"unavailable": str(exc)[:200]}
+
+
 def run_e2e(args, tk, api, torch, dev, m, n, k, world):
     """Same metric through tk_gemm_ex_raw (the reference-facing C ABI) on host buffers."""
     tag = api.TAG_F16F32 if args.dtype == "fp16" else api.TAG_BF16F32
@@ -357,6 +400,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-library", action="store_true", help="skip the cuBLAS same-op context line")
+    ap.add_argument("--fused-allgather", action="store_true",
+                    help="N>1: also time the GEMM with the all-gather fused into its epilogue")
     ap.add_argument("--traffic", type=float, default=None,
                     help="dram bytes per launch from an ncu --set full capture")
     args = ap.parse_args()

@@ -130,6 +130,26 @@ int tk_gemm_ex_raw_async(int type_tag, int trans_a, int trans_b, long long m, lo
                          long long k, double alpha_re, double alpha_im, const void* a,
                          const void* b, double beta_re, double beta_im, void* c, void* stream);
 
+/* tk_gemm plus a fused all-gather of D (north star: C sharded by column slabs, "an optional
+ * all-gather of C over NVLink"): peer_d[q] points at this rank's slab position inside peer q's
+ * full-D buffer (mapped with tk_ipc_open).  When the streamed-epilogue CTA-pair kernel runs,
+ * every D tile is TMA-stored to the local slab and to all peers from the same shared-memory box
+ * (the transfer overlaps the remaining tiles' math); otherwise the slab is copied to the peers
+ * after the GEMM on `stream`.  Real operator, dense column-major D, at most 7 peers.  The caller
+ * synchronises the ranks (stream sync + barrier) before reading the gathered D. */
+int tk_gemm_peers(const TkGemmPlan* plan, const void* a, const void* b, const void* c, void* d,
+                  const void* bias, const uint8_t* kmask, void* workspace,
+                  int64_t workspace_bytes, void* stream, void* const* peer_d, int npeers);
+
+/* How the last tk_gemm_peers delivered the slab: 1 = epilogue stores to peers, 2 = copies. */
+int tk_last_peer_mode(void);
+
+/* CUDA IPC helpers for the peer buffers (one process per GPU).  The handle names the whole
+ * allocation; *offset_out is dev_ptr's byte offset in it (add it to tk_ipc_open's pointer). */
+int tk_ipc_handle(void* dev_ptr, void* handle_out64, int64_t* offset_out);
+int tk_ipc_open(const void* handle64, void** dev_ptr_out);
+int tk_ipc_close(void* dev_ptr);
+
 /* Number of device kernels the last successful tk_gemm / tk_gemm_ex_raw launched. */
 int tk_last_launch_count(void);
 

@@ -60,7 +60,8 @@ GEMM_EX_ARGTYPES = [c_int, c_int, c_int, c_longlong, c_longlong, c_longlong, c_d
 # every symbol include/tk_sm100.h declares
 EXPORTED = ("tk_abi_version", "tk_plan_lane", "tk_workspace_bytes", "tk_gemm", "tk_gemm_ex_raw",
             "tk_gemm_ex_raw_async", "tk_last_launch_count", "tk_last_error", "tk_debug_pair_mhz",
-            "tk_debug_pair_ts", "tk_debug_clock_probe", "tk_debug_clock_probe_mhz")
+            "tk_debug_pair_ts", "tk_debug_clock_probe", "tk_debug_clock_probe_mhz",
+            "tk_gemm_peers", "tk_last_peer_mode", "tk_ipc_handle", "tk_ipc_open", "tk_ipc_close")
 
 _lib = None
 _load_error = None
@@ -87,6 +88,16 @@ def load():
     lib.tk_gemm.argtypes = [ctypes.POINTER(TkGemmPlan), c_void_p, c_void_p, c_void_p, c_void_p,
                             c_void_p, c_void_p, c_void_p, c_int64, c_void_p]
     lib.tk_gemm.restype = c_int
+    lib.tk_gemm_peers.argtypes = [ctypes.POINTER(TkGemmPlan), c_void_p, c_void_p, c_void_p, c_void_p,
+                                  c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_int]
+    lib.tk_gemm_peers.restype = c_int
+    lib.tk_last_peer_mode.restype = c_int
+    lib.tk_ipc_handle.argtypes = [c_void_p, c_void_p, ctypes.POINTER(c_int64)]
+    lib.tk_ipc_handle.restype = c_int
+    lib.tk_ipc_open.argtypes = [c_void_p, ctypes.POINTER(c_void_p)]
+    lib.tk_ipc_open.restype = c_int
+    lib.tk_ipc_close.argtypes = [c_void_p]
+    lib.tk_ipc_close.restype = c_int
     lib.tk_gemm_ex_raw.argtypes = GEMM_EX_ARGTYPES
     lib.tk_gemm_ex_raw.restype = c_int
     lib.tk_gemm_ex_raw_async.argtypes = GEMM_EX_ARGTYPES + [c_void_p]

@@ -27,6 +27,11 @@ namespace {
 
 thread_local std::string g_err;
 thread_local int g_launches = 0;
+// fused all-gather request of the current tk_gemm_peers call: D slab pointers inside each
+// peer's full-D buffer, and how the last call delivered them (1 epilogue stores, 2 copies)
+thread_local void* const* g_peer_d = nullptr;
+thread_local int g_npeer = 0;
+thread_local int g_peer_mode = 0;
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -1073,7 +1078,15 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
         if (!prm.c_zero && (rc = make_map_2d(&pp.tcmap, c, TK_F32, p->m, p->n, prm.ldc, 32, 32))) return rc;
         if ((rc = make_map_2d(&pp.tdmap, d, TK_F32, p->m, p->n, prm.ldd, 32, 32))) return rc;
         pp.d_tma = 1;
-        if (const char* e = getenv("TK_PAIR_DTMA")) pp.d_tma = atoi(e);
+        pp.npeer = 0;
+        if (g_npeer > 0 && g_npeer <= 7) {
+          for (int q = 0; q < g_npeer; ++q)
+            if ((rc = make_map_2d(&pp.tdpeer[q], g_peer_d[q], TK_F32, p->m, p->n, prm.ldd, 32, 32))) return rc;
+          pp.npeer = g_npeer;
+          g_peer_mode = 1;
+        }
+        if (const char* e = getenv("TK_PAIR_DTMA"))
+          if (!pp.npeer) pp.d_tma = atoi(e);
         pp.c_pf_kb = 0;  // L2 prefetch of the next drain's C: measured neutral-to-negative
         if (const char* e = getenv("TK_C_PF")) pp.c_pf_kb = atoi(e);
         pp.c_pf_spread = 0;
@@ -1366,6 +1379,73 @@ int tk_gemm(const TkGemmPlan* plan0, const void* a, const void* b, const void* c
     return run_tc(plan, a, b, c, d, bias, static_cast<uint8_t*>(workspace), w, s);
   }
   return run_simt(plan, a, b, c, d, bias, kmask, s);
+}
+
+int tk_gemm_peers(const TkGemmPlan* plan, const void* a, const void* b, const void* c, void* d,
+                  const void* bias, const uint8_t* kmask, void* workspace, int64_t workspace_bytes,
+                  void* stream, void* const* peer_d, int npeers) {
+  if (npeers < 0 || npeers > 7 || (npeers && !peer_d))
+    return fail(TK_ERR_CONFIG, "between 0 and 7 peer D slabs expected");
+  if (npeers && (plan->op != TK_OP_REAL || plan->d.kind != TK_LAYOUT_STRIDED || plan->d.pair ||
+                 plan->d.ndigits[0] != 1 || plan->d.ndigits[1] != 1 || plan->d.stride[0][0] != 1 ||
+                 plan->d.stride[1][0] != plan->m))
+    return fail(TK_ERR_CONFIG, "a fused all-gather needs a real, dense column-major D slab");
+  g_peer_d = peer_d;
+  g_npeer = npeers;
+  g_peer_mode = 0;
+  int rc = tk_gemm(plan, a, b, c, d, bias, kmask, workspace, workspace_bytes, stream);
+  g_peer_d = nullptr;
+  g_npeer = 0;
+  if (rc || !npeers || g_peer_mode == 1) return rc;
+  // the chosen kernel has no streamed epilogue: deliver the slab with peer copies instead
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int q = 0; q < npeers; ++q)
+    TK_CUDA(cudaMemcpyAsync(peer_d[q], d, size_t(plan->m) * size_t(plan->n) * 4, cudaMemcpyDefault, s));
+  g_peer_mode = 2;
+  return TK_OK;
+}
+
+int tk_last_peer_mode(void) { return g_peer_mode; }
+
+// CUDA IPC for the peer buffers of a fused all-gather (one process per GPU): the 64-byte handle
+// of a device allocation, and mapping / unmapping a peer's allocation into this process.
+// The handle names the whole allocation (a caching allocator hands out sub-ranges of larger
+// cudaMalloc blocks), so the byte offset of dev_ptr inside it is returned too.
+int tk_ipc_handle(void* dev_ptr, void* handle_out64, int64_t* offset_out) {
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, dev_ptr) != cudaSuccess) {
+    const char* m = cudaGetErrorString(cudaGetLastError());
+    return fail(TK_ERR_CUDA, "cudaIpcGetMemHandle: %s", m);
+  }
+  using GetAttr = CUresult (*)(void*, CUpointer_attribute, CUdeviceptr);
+  static GetAttr get_attr = nullptr;
+  if (!get_attr) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuPointerGetAttribute", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return fail(TK_ERR_CUDA, "cuPointerGetAttribute unavailable");
+    get_attr = reinterpret_cast<GetAttr>(fn);
+  }
+  CUdeviceptr start = 0;
+  if (get_attr(&start, CU_POINTER_ATTRIBUTE_RANGE_START_ADDR, reinterpret_cast<CUdeviceptr>(dev_ptr)) !=
+      CUDA_SUCCESS)
+    return fail(TK_ERR_CUDA, "allocation range of an IPC buffer");
+  memcpy(handle_out64, &h, sizeof(h));
+  *offset_out = int64_t(reinterpret_cast<CUdeviceptr>(dev_ptr) - start);
+  return TK_OK;
+}
+int tk_ipc_open(const void* handle64, void** dev_ptr_out) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  if (cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+    const char* m = cudaGetErrorString(cudaGetLastError());
+    return fail(TK_ERR_CUDA, "cudaIpcOpenMemHandle: %s", m);
+  }
+  return TK_OK;
+}
+int tk_ipc_close(void* dev_ptr) {
+  return cudaIpcCloseMemHandle(dev_ptr) == cudaSuccess ? TK_OK : fail(TK_ERR_CUDA, "cudaIpcCloseMemHandle");
 }
 
 }  // extern "C"

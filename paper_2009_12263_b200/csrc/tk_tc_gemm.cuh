@@ -107,6 +107,10 @@ struct TcParams {
   int32_t num_units, sk_first, sk_parts, dbg_cta;
   int32_t vec_ok, serp;          // diag_stream_kernel: 16-byte vector path legal; pair kernel: serpentine K
   int32_t pdl, pad5;             // pair kernel launched with programmatic stream serialisation
+  // fused all-gather of D over peer memory (NVLink): the streamed epilogue TMA-stores every D
+  // box to the local slab and to the same slab position inside each peer's full-D buffer
+  CUtensorMap tdpeer[7];
+  int32_t npeer, pad7;
   int32_t c_ident, r_ident, s_ident, nar_units;  // empty transform programs: skip the stage;
                                                  // pair NSUB 2: half-width first units (stagger)
   float* sk_ws;
@@ -405,6 +409,7 @@ __device__ __forceinline__ void epilogue_stream(const TcParams& p, uint64_t* tfu
       __syncwarp();
       if (lane == 0) {
         tma_store_2d(&p.tdmap, box, row0, j0);   // the map clips rows >= M / columns >= N
+        for (int q = 0; q < p.npeer; ++q) tma_store_2d(&p.tdpeer[q], box, row0, j0);  // peers (NVLink)
         bulk_commit();
         if (ch == 0) TK_TS_EPI(10);
         if (has_c) {

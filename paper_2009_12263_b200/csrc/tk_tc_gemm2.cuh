@@ -450,7 +450,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     }
   }
 
-  if (CSTREAM && warp >= 4 && lane == 0) bulk_wait<0>();
+  if (CSTREAM && warp >= 4 && lane == 0) {
+    bulk_wait<0>();
+    if (p.npeer) __threadfence_system();  // peer slabs complete before the grid retires
+  }
   if (warp == 4 && lane == 0) TK_TS(6);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long ns1;

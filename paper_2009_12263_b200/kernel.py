@@ -509,7 +509,7 @@ def _is_tensor(x):
 
 
 def gemm_execute(config: KernelConfig, a, b, c, d, *, stream=None, synchronize: bool = True,
-                 lane: Optional[str] = None) -> EventCounters:
+                 lane: Optional[str] = None, peers=None) -> EventCounters:
     """Run one GEMM on the B200; returns the event counters of the logical schedule.
 
     Buffers are flat 1-D arrays (numpy or torch, host or device) sized by their layouts'
@@ -549,10 +549,16 @@ def gemm_execute(config: KernelConfig, a, b, c, d, *, stream=None, synchronize: 
             _note("workspace", prep.ws_bytes)
         _note_onchip(prep.plan, prep.lane_id)
         s = stream if stream is not None else torch.cuda.current_stream(device)
-        rc = lib.tk_gemm(prep.plan_ref, A.ptr(), B.ptr(), C.ptr(), D.ptr(),
-                         bias_dev.ptr() if bias_dev else None,
-                         mask_dev.data_ptr() if mask_dev is not None else None,
-                         ws.data_ptr() if ws is not None else None, prep.ws_bytes, s.cuda_stream)
+        args = (prep.plan_ref, A.ptr(), B.ptr(), C.ptr(), D.ptr(),
+                bias_dev.ptr() if bias_dev else None,
+                mask_dev.data_ptr() if mask_dev is not None else None,
+                ws.data_ptr() if ws is not None else None, prep.ws_bytes, s.cuda_stream)
+        if peers:  # fused all-gather: D slab also written into each peer's full-D buffer
+            arr = (ctypes.c_void_p * len(peers))(*[int(x) for x in peers])
+            rc = lib.tk_gemm_peers(*args, arr, len(peers))
+            _LAST["peer_mode"] = lib.tk_last_peer_mode()
+        else:
+            rc = lib.tk_gemm(*args)
         if rc == _lib.TK_ERR_CONFIG:
             raise ConfigError(_lib.last_error())
         if rc != _lib.TK_OK:

@@ -64,18 +64,85 @@ def _view(buf, offset, size):
     return buf[offset:offset + size]
 
 
+class PeerBuffers:
+    """Every rank's full-D buffer mapped into this process (CUDA IPC over the process group),
+    for the fused all-gather: the GEMM epilogue stores each D tile locally and into the peers'
+    buffers (NVLink peer writes on an NVSwitch box).  ``full`` is this rank's flat full-D
+    CUDA tensor (same size on every rank); ``close()`` unmaps the peers."""
+
+    def __init__(self, full, group=None):
+        import ctypes
+
+        import torch.distributed as dist
+
+        from . import _lib
+
+        self.lib = _lib.load()
+        self.full = full
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        h = (ctypes.c_char * 64)()
+        off = ctypes.c_int64()
+        if self.lib.tk_ipc_handle(ctypes.c_void_p(full.data_ptr()), h, ctypes.byref(off)) != 0:
+            raise RuntimeError(_lib.last_error())
+        handles = [None] * self.world
+        dist.all_gather_object(handles, (bytes(h), off.value), group=group)
+        self.bases, self.mapped = [], []
+        for r, (hb, offset) in enumerate(handles):
+            if r == self.rank:
+                self.bases.append(full.data_ptr())
+                self.mapped.append(None)
+                continue
+            ptr = ctypes.c_void_p()
+            if self.lib.tk_ipc_open(ctypes.create_string_buffer(hb, 64), ctypes.byref(ptr)) != 0:
+                self.close()
+                raise RuntimeError(_lib.last_error())
+            self.mapped.append(ptr.value)
+            self.bases.append(ptr.value + offset)  # the peer's tensor inside its allocation
+
+    def peer_slabs(self, byte_offset):
+        """Addresses of this rank's slab position inside every other rank's full D."""
+        return [base + byte_offset for r, base in enumerate(self.bases) if r != self.rank]
+
+    def close(self):
+        for ptr in getattr(self, "mapped", []):
+            if ptr:
+                self.lib.tk_ipc_close(ptr)
+        self.bases, self.mapped = [], []
+
+
 def sharded_gemm(config, a, b, c, d, *, rank: int, world: int, group=None,
-                 allgather_into=None, **run_kwargs):
+                 allgather_into=None, fused: bool = False, peers: "PeerBuffers" = None,
+                 **run_kwargs):
     """Run this rank's column slab of ``config`` on full-problem buffers (A replicated).
 
     ``b``, ``c``, ``d`` are the full flat buffers (views of the rank's slab are taken);
     ``allgather_into`` (optional, flat full-D tensor) receives every rank's slab through
-    ``torch.distributed.all_gather_into_tensor`` on ``group``.  Returns the slab counters.
+    ``torch.distributed.all_gather_into_tensor`` on ``group``.  With ``fused=True`` and
+    ``peers`` (a ``PeerBuffers`` over each rank's ``allgather_into``) the slab is instead
+    written by the GEMM itself into the local and every peer's full D (peer-memory stores from
+    the epilogue, overlapping the remaining tiles); the ranks are then synchronised with a
+    stream sync and a barrier.  Returns the slab counters.
     """
     slab, off, _ = shard_config(config, rank, world)
     sb = slab.global_b_layout.physical_size()
     sc = slab.global_c_layout.physical_size()
     sd = slab.global_d_layout.physical_size()
+    if fused:
+        if peers is None or allgather_into is None:
+            raise ConfigError("fused all-gather needs allgather_into and its PeerBuffers")
+        import torch
+        import torch.distributed as dist
+
+        dst = _view(allgather_into, off["D"], sd)
+        counters = kernel.gemm_execute(slab, a, _view(b, off["B"], sb), _view(c, off["C"], sc),
+                                       dst, peers=peers.peer_slabs(off["D"] * dst.element_size()),
+                                       **run_kwargs)
+        torch.cuda.synchronize(dst.device)
+        dist.barrier(group=group)
+        if d is not None and d.data_ptr() != allgather_into.data_ptr():
+            _view(d, off["D"], sd).copy_(dst)
+        return counters
     counters = kernel.gemm_execute(slab, a, _view(b, off["B"], sb), _view(c, off["C"], sc),
                                    _view(d, off["D"], sd), **run_kwargs)
     if allgather_into is not None:

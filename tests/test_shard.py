@@ -92,6 +92,7 @@ def test_device_slabs_match_single_gpu_columns(monkeypatch):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     monkeypatch.setenv("TK_TC_KERNEL", "pair")
+    monkeypatch.setenv("TK_SERPENTINE", "0")  # same k order in every tile of every slab
     m, n, k = 1024, 2048, 512
     rng = np.random.default_rng(3)
     dev = lambda x: torch.from_numpy(np.ascontiguousarray(np.asarray(x).ravel(order="F"))).cuda()
@@ -108,3 +109,74 @@ def test_device_slabs_match_single_gpu_columns(monkeypatch):
         total += shard.sharded_gemm(cfg, a, b, c, d, rank=r, world=world).global_stores
     assert torch.equal(d, full)
     assert total == m * n
+
+
+def _fused_worker(rank, world, port, result, shape):
+    """One rank of a fused GEMM + all-gather: both processes share cuda:0 (the only GPU of the
+    test box), peer buffers are mapped with CUDA IPC exactly as across NVLink peers."""
+    import torch
+    import torch.distributed as dist
+
+    os.environ["TK_SERPENTINE"] = "0"
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    try:
+        m, n, k = shape
+        rng = np.random.default_rng(11)
+        a = rng.integers(-4, 5, (m, k)).astype(np.float16)
+        b = rng.integers(-4, 5, (k, n)).astype(np.float16)
+        c = rng.integers(-4, 5, (m, n)).astype(np.float32)
+        dev = lambda x: torch.from_numpy(np.ascontiguousarray(np.asarray(x).ravel(order="F"))).cuda()
+        A, B, C = dev(a), dev(b), dev(c)
+        cfg = tk.build_dense_config(m, n, k, np.float16)
+        # the gathered D sits 4 KB into its allocation: IPC maps allocations, not tensors
+        store = torch.full((m * n + 1024,), float("nan"), device="cuda")
+        full = store[1024:]
+        peers = shard.PeerBuffers(full)
+        try:
+            shard.sharded_gemm(cfg, A, B, C, None, rank=rank, world=world, allgather_into=full,
+                               fused=True, peers=peers)
+            mode = tk.last_run().get("peer_mode")
+            want = torch.zeros(m * n, device="cuda")
+            tk.matmul(cfg, A, B, C, want)
+            ok = bool(torch.equal(full, want))
+            if not ok:
+                bad = (full != want).view(n, m)
+                cols = torch.nonzero(bad.any(dim=1)).flatten()
+                ok = (f"mismatch: nan={int(torch.isnan(full).sum())} cols {int(cols.min())}..{int(cols.max())} "
+                      f"n={len(cols)} maxdiff={float((full - want).abs().nan_to_num(0).max())}")
+            result.put((rank, mode, ok))
+            dist.barrier()
+        finally:
+            peers.close()
+    except Exception as exc:  # report instead of hanging the parent
+        result.put((rank, None, repr(exc)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape,mode", [((1024, 2048, 1024), 1),   # streamed epilogue: peer TMA stores
+                                        ((512, 1024, 256), 2)])     # K <= 256: copies after the GEMM
+def test_fused_allgather_two_ranks_one_gpu(shape, mode):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_fused_worker, args=(r, 2, port, q, shape)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(60)
+    for rank, got_mode, ok in res:
+        if isinstance(ok, str) and "cudaIpc" in ok:
+            pytest.skip(f"CUDA IPC unavailable in this sandbox: {ok}")
+        assert ok is True, (rank, ok)
+        assert got_mode == mode, (rank, got_mode)
