@@ -1112,8 +1112,13 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
       tk::TcParams pp = prm;
       // two A planes per tile: 8 M-blocks per group keep the panel L2-resident (16: -4 %)
       if (!getenv("TK_GROUP_M")) pp.group_m = 8;
+      // 256-wide pair tiles (N=256 MMAs: 96 instead of 128 B/clk of shared-memory operand
+      // reads) when there are >= 4 waves of them to amortise the single accumulator's drain
+      const int64_t tiles256 = ((p->m + 255) / 256) * ((p->n + 255) / 256);
+      int bn = tiles256 >= 4 * int64_t(pair_clusters()) ? 256 : 128;
+      if (const char* e = getenv("TK_PAIROPS_BN")) bn = atoi(e) == 256 ? 256 : 128;
       pp.num_mb = int((p->m + 255) / 256);
-      pp.num_nb = int((p->n + tk::TC2C_BN - 1) / tk::TC2C_BN);
+      pp.num_nb = int((p->n + bn - 1) / bn);
       pp.num_tiles = pp.num_mb * pp.num_nb;
       int mn;
       int64_t pitch;
@@ -1128,15 +1133,16 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
       }
       tma_operand(p->b, mn, pitch);
       if (p->b.pair == TK_PAIR_INTERLEAVED) pitch = mn ? p->k : p->n;
-      if (mn)  // K-major B: this CTA's 64-column half per box
+      if (mn)  // K-major B: this CTA's bn/2-column half per box
         for (int pl = 0; pl < 2; ++pl)
-          if ((rc = make_map_2d(&pp.tb[pl], planes_b[pl], p->b.scalar, p->k, p->n, pitch, 64, 64))) return rc;
-      static bool attr[2][2] = {{false, false}, {false, false}};
+          if ((rc = make_map_2d(&pp.tb[pl], planes_b[pl], p->b.scalar, p->k, p->n, pitch, 64, bn / 2))) return rc;
+      static bool attr[2][2][2] = {};
       const int oi = op == TK_OP_COMPLEX ? 0 : 1;
+      const int smem_bytes = bn == 256 ? tk::Tc2cPlan<256>::SMEM : tk::Tc2cPlan<128>::SMEM;
       auto launch = [&](auto kern) -> int {
-        if (!attr[oi][dense]) {
-          TK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tk::TC2C_SMEM));
-          attr[oi][dense] = true;
+        if (!attr[oi][dense][bn == 256]) {
+          TK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
+          attr[oi][dense][bn == 256] = true;
         }
         const int grid = 2 * std::min(pp.num_tiles, sm_count() / 2);
         const char* e = getenv("TK_PDL");
@@ -1145,7 +1151,7 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(grid);
         cfg.blockDim = dim3(tk::TC_THREADS);
-        cfg.dynamicSmemBytes = tk::TC2C_SMEM;
+        cfg.dynamicSmemBytes = smem_bytes;
         cfg.stream = s;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1156,6 +1162,13 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
         ++g_launches;
         return TK_OK;
       };
+      if (bn == 256) {
+        if (op == TK_OP_COMPLEX)
+          return dense ? launch(tk::tc_gemm_pair_ops_kernel<tk::OP_COMPLEX, true, 256>)
+                       : launch(tk::tc_gemm_pair_ops_kernel<tk::OP_COMPLEX, false, 256>);
+        return dense ? launch(tk::tc_gemm_pair_ops_kernel<tk::OP_DUAL, true, 256>)
+                     : launch(tk::tc_gemm_pair_ops_kernel<tk::OP_DUAL, false, 256>);
+      }
       if (op == TK_OP_COMPLEX)
         return dense ? launch(tk::tc_gemm_pair_ops_kernel<tk::OP_COMPLEX, true>)
                      : launch(tk::tc_gemm_pair_ops_kernel<tk::OP_COMPLEX, false>);

@@ -12,7 +12,7 @@
 
 namespace tk {
 
-constexpr int TC2C_BN = 128;                        // pair tile N (instruction N)
+constexpr int TC2C_BN = 128;                        // default pair tile N (instruction N)
 constexpr int TC2C_STAGES = 4;
 constexpr int TC2C_A_BYTES = 128 * 64 * 2;          // one A plane, 128 rows
 constexpr int TC2C_B_BYTES = 64 * 64 * 2;           // one B plane, 64 columns (this CTA's half)
@@ -20,15 +20,31 @@ constexpr int TC2C_STAGE_BYTES = 2 * (TC2C_A_BYTES + TC2C_B_BYTES);
 constexpr int TC2C_BAR_OFFSET = TC2C_STAGES * TC2C_STAGE_BYTES;
 constexpr int TC2C_SMEM = TC2C_BAR_OFFSET + 256 + 1024;
 
-template <int OP, bool DENSE_EPI>
+// Pair-tile width BN (= instruction N): 128 -> two double-buffered 256-column accumulator
+// pairs (Re/Im or v/eps of 128 columns each), 4 stages; 256 -> one 512-column accumulator pair,
+// 3 stages.  N=128 MMAs read 8 KB of shared memory per 64 clocks (128 B/clk: the SM's shared
+// memory port is the bound, ~80 % tensor activity); N=256 MMAs read 12 KB per 128 clocks.
+template <int BN>
+struct Tc2cPlan {
+  static constexpr int B_BYTES = BN * 64;  // BN/2 columns x 64 K x 2 bytes, one plane
+  static constexpr int STAGE_BYTES = 2 * (TC2C_A_BYTES + B_BYTES);
+  static constexpr int STAGES = BN == 128 ? TC2C_STAGES : 3;
+  static constexpr int BAR_OFFSET = STAGES * STAGE_BYTES;
+  static constexpr int SMEM = BAR_OFFSET + 256 + 1024;
+  static constexpr int NACC = BN == 128 ? 2 : 1;  // accumulator pairs in TMEM
+};
+
+template <int OP, bool DENSE_EPI, int BN = TC2C_BN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     tc_gemm_pair_ops_kernel(const __grid_constant__ TcParams p) {
+  using PL = Tc2cPlan<BN>;
+  constexpr int STAGES = PL::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + TC2C_BAR_OFFSET);
-  uint64_t* empty = full + TC2C_STAGES;
-  uint64_t* tfull = empty + TC2C_STAGES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + PL::BAR_OFFSET);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -46,7 +62,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     }
   }
   if (warp == 1 && lane == 0) {
-    for (int s = 0; s < TC2C_STAGES; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -64,14 +80,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  unsigned long long clk0 = 0, ns0 = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    clk0 = clock64();
+    ns0 = gtimer();
+  }
   if (p.pdl) {  // programmatic dependent launch (see tc_gemm_pair_kernel)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
   }
 
-  auto a_tile = [&](int s, int pl) -> uint8_t* { return smem + s * TC2C_STAGE_BYTES + pl * TC2C_A_BYTES; };
+  auto a_tile = [&](int s, int pl) -> uint8_t* { return smem + s * PL::STAGE_BYTES + pl * TC2C_A_BYTES; };
   auto b_tile = [&](int s, int pl) -> uint8_t* {
-    return smem + s * TC2C_STAGE_BYTES + 2 * TC2C_A_BYTES + pl * TC2C_B_BYTES;
+    return smem + s * PL::STAGE_BYTES + 2 * TC2C_A_BYTES + pl * PL::B_BYTES;
   };
 
   if (warp == 0) {
@@ -84,13 +105,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         int mb, nb;
         tile_coords(p, t, mb, nb);
         const int m0 = mb * 256 + int(rank) * 128;
-        const int n0 = nb * TC2C_BN + int(rank) * 64;
+        const int n0 = nb * BN + int(rank) * (BN / 2);
         const bool rev = p.serp && (lu & 1);  // serpentine K (see tc_gemm_pair_kernel)
         for (int ki = 0; ki < p.kb_total; ++ki) {
           const int kb = rev ? p.kb_total - 1 - ki : ki;
           const int k0 = kb * TC_BK;
           mbar_wait(&empty[stage], phase ^ 1);
-          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * TC2C_STAGE_BYTES);
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * PL::STAGE_BYTES);
           const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
 #pragma unroll
           for (int pl = 0; pl < 2; ++pl) {
@@ -102,19 +123,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
             } else {
               tma_load_2d_pair(a_tile(stage, pl), &p.ta[pl], fb, k0, m0, pol);
             }
-            if (p.b_mn)
-              tma_load_2d_pair(b_tile(stage, pl), &p.tb[pl], fb, n0, k0, pol);
-            else
+            if (p.b_mn) {  // 64-column MN-major atoms
+              for (int h = 0; h < BN / 128; ++h)
+                tma_load_2d_pair(b_tile(stage, pl) + h * 8192, &p.tb[pl], fb, n0 + 64 * h, k0, pol);
+            } else {
               tma_load_2d_pair(b_tile(stage, pl), &p.tb[pl], fb, k0, n0, pol);
+            }
           }
-          if (++stage == TC2C_STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
     if (leader && lane == 0) {
-      const uint32_t idesc = idesc_f16(p.ab_fmt, p.a_mn, p.b_mn, 0, 256, TC2C_BN);
-      const uint32_t idesc_neg = idesc_f16(p.ab_fmt, p.a_mn, p.b_mn, 1, 256, TC2C_BN);
+      const uint32_t idesc = idesc_f16(p.ab_fmt, p.a_mn, p.b_mn, 0, 256, BN);
+      const uint32_t idesc_neg = idesc_f16(p.ab_fmt, p.a_mn, p.b_mn, 1, 256, BN);
       const uint32_t a_step = p.a_mn ? 2048u : 32u;
       const uint32_t b_step = p.b_mn ? 2048u : 32u;
       const uint32_t a_lbo = p.a_mn ? 8192u : 16u;
@@ -123,12 +146,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       uint32_t phase = 0;
       int local = 0;
       for (int t = cluster; t < p.num_tiles; t += nclusters, ++local) {
-        const int as = local & 1;
-        const uint32_t aphase = (local >> 1) & 1;
+        const int as = local % PL::NACC;
+        const uint32_t aphase = (local / PL::NACC) & 1;
         mbar_wait(&tempty[as], aphase ^ 1);
         tc_fence_after();
-        const uint32_t d0 = tmem_base + uint32_t(as * 256);
-        const uint32_t d1 = d0 + uint32_t(TC2C_BN);
+        const uint32_t d0 = tmem_base + uint32_t(as * 2 * BN);
+        const uint32_t d1 = d0 + uint32_t(BN);
         for (int kb = 0; kb < p.kb_total; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -151,7 +174,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
             }
           }
           tc_commit_pair(&empty[stage], 0x3);
-          if (++stage == TC2C_STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
         tc_commit_pair(&tfull[as], 0x3);
       }
@@ -165,21 +188,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     for (int t = cluster; t < p.num_tiles; t += nclusters, ++local) {
       int mb, nb;
       tile_coords(p, t, mb, nb);
-      const int as = local & 1;
-      const uint32_t aphase = (local >> 1) & 1;
+      const int as = local % PL::NACC;
+      const uint32_t aphase = (local / PL::NACC) & 1;
       const int i = mb * 256 + int(rank) * 128 + row_local;
-      const uint32_t tbase = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(as * 256);
-      const int jbase = nb * TC2C_BN + half * 64;
-      if (DENSE_EPI)
-        epilogue_dense<OP, 64, TC2C_BN>(p, tfull + as, aphase, tbase, i, jbase, lane);
+      const uint32_t tbase = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(as * 2 * BN);
+      const int jbase = nb * BN + half * (BN / 2);
+      if (p.dbg_skip_epi) {  // diagnostic: mainloop only
+        mbar_wait_sleep(tfull + as, aphase);
+        tc_fence_after();
+      } else if (DENSE_EPI)
+        epilogue_dense<OP, BN / 2, BN>(p, tfull + as, aphase, tbase, i, jbase, lane);
       else
-        epilogue_generic<OP, 64, TC2C_BN>(p, tfull + as, aphase, tbase, i, jbase);
+        epilogue_generic<OP, BN / 2, BN>(p, tfull + as, aphase, tbase, i, jbase);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[as]), 0));
     }
   }
 
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // effective SM clock (tk_debug_pair_mhz)
+    g_dbg_clk[0] = clock64() - clk0;
+    g_dbg_clk[1] = gtimer() - ns0;
+  }
   tc_fence_before();
   cluster_sync();
   if (warp == 2) {
