@@ -187,11 +187,14 @@ def test_fused_affine_bias_relu(cuda):
     assert counters.global_stores == m * n
 
 
-@pytest.mark.parametrize("kernel", ["auto", "single", "pair"])
+@pytest.mark.parametrize("kernel", ["auto", "single", "pair", "pair256"])
 @pytest.mark.parametrize("split", [False, True])
 @pytest.mark.parametrize("kind", ["complex", "dual"])
 def test_pair_operators(cuda, split, kind, kernel, monkeypatch):
-    if kernel != "auto":
+    if kernel == "pair256":  # 256-wide pair tiles, one accumulator pair
+        monkeypatch.setenv("TK_TC_KERNEL", "pair")
+        monkeypatch.setenv("TK_PAIROPS_BN", "256")
+    elif kernel != "auto":
         monkeypatch.setenv("TK_TC_KERNEL", kernel)
     m, n, k = 512, 384, 320
     rng = np.random.default_rng(3)
