@@ -197,9 +197,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         const int m0 = mb * 256 + int(rank) * 128;     // this CTA's rows of A
         const int n0 = nb * BNP + un.noff + int(rank) * (BNI / 2);  // this CTA's columns of B (per MMA)
         const int nsub_u = un.narrow ? 1 : NSUB;
-        // serpentine K (opt-in): every other tile of a cluster walks K downwards, so the next
+        // serpentine K: every other tile of a cluster walks K downwards, so the next
         // wave starts on the K-slices the previous one loaded last (still in L2)
-        const bool rev = NSUB == 1 && p.serp && (lu & 1);
+        const bool rev = p.serp && (lu & 1);
         for (int ki = 0; ki < un.kb1 - un.kb0; ++ki) {
           const int kb = rev ? un.kb1 - 1 - ki : un.kb0 + ki;
           const int k0 = kb * TC_BK;
