@@ -490,3 +490,21 @@ def test_gett_operand_packing_plan(spec, sizes, packed):
     m, n, k = cfg.params.gemm_shape
     want = (2 * m * k if "A" in packed else 0) + (2 * k * n if "B" in packed else 0)
     assert _lib.load().tk_workspace_bytes(plan) == want
+
+
+def test_fused_allgather_entry_validates_before_launch():
+    """tk_gemm_peers rejects what the fused all-gather cannot do before touching the device:
+    more than 7 peers, or a D that is not one dense column-major slab."""
+    lib = _lib.load()
+    dense = kernel.resolve_config(tk.build_dense_config(256, 256, 256, np.float16))
+    plan, _, _ = kernel.lower(dense)
+    peers = (ctypes.c_void_p * 8)(*([0x1000] * 8))
+    rc = lib.tk_gemm_peers(ctypes.byref(plan), None, None, None, None, None, None, None, 0, None,
+                           peers, 8)
+    assert rc == _lib.TK_ERR_CONFIG and "peer" in _lib.last_error()
+    gett = kernel.resolve_config(tk.build_gett_config("abc-acd-db", dict(a=64, b=96, c=8, d=136),
+                                                      np.float16))
+    plan2, _, _ = kernel.lower(gett)
+    rc = lib.tk_gemm_peers(ctypes.byref(plan2), None, None, None, None, None, None, None, 0, None,
+                           peers, 1)
+    assert rc == _lib.TK_ERR_CONFIG and "dense column-major" in _lib.last_error()
