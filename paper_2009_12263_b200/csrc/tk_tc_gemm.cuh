@@ -306,22 +306,17 @@ __device__ __forceinline__ void epilogue_dense(const TcParams& p, uint64_t* tful
       }
     }
   } else {
-    // pair operators: interleaved (float2) or split planes, column-major elements
+    // pair operators: interleaved (float2) or split planes, column-major elements.  16-column
+    // steps (two x16 TMEM loads) keep the Re/Im accumulators, C and D in registers without
+    // spills; the next step's C is in flight while this one computes and stores.
+    constexpr int W = 16;
     const float* cp = reinterpret_cast<const float*>(p.c_ptr);
     float* dp = reinterpret_cast<float*>(p.d_ptr);
     const int64_t ci = row_ok ? i : 0;
-    mbar_wait_sleep(tfull, aphase);
-    tc_fence_after();
-#pragma unroll 1
-    for (int ch = 0; ch < COLS / 32; ++ch) {
-      const int j0 = jbase + ch * 32;
-      const uint32_t col = uint32_t(j0 - jbase + (jbase % BN));
-      uint32_t r0[32], r1[32];
-      tmem_ld_32x32b_x32(tbase + col, r0);
-      tmem_ld_32x32b_x32(tbase + uint32_t(BN) + col, r1);
-      float2 cv[32];
+    float2 cv[W];
+    auto load_c = [&](int j0) {
 #pragma unroll
-      for (int jj = 0; jj < 32; ++jj) {
+      for (int jj = 0; jj < W; ++jj) {
         const int j = j0 + jj;
         cv[jj] = make_float2(0.f, 0.f);
         if (has_c && row_ok && j < p.n) {
@@ -330,27 +325,50 @@ __device__ __forceinline__ void epilogue_dense(const TcParams& p, uint64_t* tful
                                              : make_float2(__ldcs(cp + e), __ldcs(cp + e + p.c_plane));
         }
       }
+    };
+    load_c(jbase);
+    mbar_wait_sleep(tfull, aphase);
+    tc_fence_after();
+#pragma unroll 1
+    for (int ch = 0; ch < COLS / W; ++ch) {
+      const int j0 = jbase + ch * W;
+      const uint32_t col = uint32_t(j0 - jbase + (jbase % BN));
+      uint32_t r0[W], r1[W];
+      tmem_ld_32x32b_x16(tbase + col, r0);
+      tmem_ld_32x32b_x16(tbase + uint32_t(BN) + col, r1);
       tmem_ld_wait();
+      float2 v[W];
 #pragma unroll
-      for (int jj = 0; jj < 32; ++jj) {
-        float2 v = make_float2(__uint_as_float(r0[jj]), __uint_as_float(r1[jj]));
+      for (int jj = 0; jj < W; ++jj) {
+        float2 x = make_float2(__uint_as_float(r0[jj]), __uint_as_float(r1[jj]));
         if (has_c) {
-          const float cr = cv[jj].x * p.c_mul[0] - cv[jj].y * p.c_mul[1] + p.c_add[0];
-          const float ci_ = cv[jj].x * p.c_mul[1] + cv[jj].y * p.c_mul[0] + p.c_add[1];
-          v = make_float2(cr + v.x, ci_ + v.y);
+          if (p.c_ident) {
+            x = make_float2(cv[jj].x + x.x, cv[jj].y + x.y);
+          } else {
+            const float cr = cv[jj].x * p.c_mul[0] - cv[jj].y * p.c_mul[1] + p.c_add[0];
+            const float ci_ = cv[jj].x * p.c_mul[1] + cv[jj].y * p.c_mul[0] + p.c_add[1];
+            x = make_float2(cr + x.x, ci_ + x.y);
+          }
         }
-        float2 w = make_float2(v.x * p.r_mul[0] - v.y * p.r_mul[1] + p.r_add[0],
-                               v.x * p.r_mul[1] + v.y * p.r_mul[0] + p.r_add[1]);
-        v = make_float2(w.x * p.s_mul[0] - w.y * p.s_mul[1] + p.s_add[0],
-                        w.x * p.s_mul[1] + w.y * p.s_mul[0] + p.s_add[1]);
+        if (!p.r_ident)
+          x = make_float2(x.x * p.r_mul[0] - x.y * p.r_mul[1] + p.r_add[0],
+                          x.x * p.r_mul[1] + x.y * p.r_mul[0] + p.r_add[1]);
+        if (!p.s_ident)
+          x = make_float2(x.x * p.s_mul[0] - x.y * p.s_mul[1] + p.s_add[0],
+                          x.x * p.s_mul[1] + x.y * p.s_mul[0] + p.s_add[1]);
+        v[jj] = x;
+      }
+      if (ch + 1 < COLS / W) load_c(j0 + W);
+#pragma unroll
+      for (int jj = 0; jj < W; ++jj) {
         const int j = j0 + jj;
         if (row_ok && j < p.n) {
           const int64_t e = ci + int64_t(j) * p.ldd;
           if (p.d_pair == P_INTERLEAVED) {
-            __stcs(reinterpret_cast<float2*>(dp) + e, v);
+            __stcs(reinterpret_cast<float2*>(dp) + e, v[jj]);
           } else {
-            __stcs(dp + e, v.x);
-            __stcs(dp + e + p.d_plane, v.y);
+            __stcs(dp + e, v[jj].x);
+            __stcs(dp + e + p.d_plane, v[jj].y);
           }
         }
       }
