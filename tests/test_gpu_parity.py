@@ -233,6 +233,43 @@ def test_pair_operators(cuda, split, kind, kernel, monkeypatch):
     assert err <= O.tolerance(k, factor), err
 
 
+@pytest.mark.parametrize("bn", ["128", "256"])
+@pytest.mark.parametrize("split", [False, True])
+@pytest.mark.parametrize("kind", ["complex", "dual"])
+def test_pair_operators_bf16_integer_exact(cuda, kind, split, bn, monkeypatch):
+    """bf16 pair storage (COMPLEXBF16 / DUALBF16) on both pair-tile widths: small-integer
+    inputs make every product and sum exact, so the result is bitwise the oracle's."""
+    monkeypatch.setenv("TK_TC_KERNEL", "pair")
+    monkeypatch.setenv("TK_PAIROPS_BN", bn)
+    m, n, k = 512, 512, 320
+    rng = np.random.default_rng(8)
+    ints = lambda s: rng.integers(-4, 5, s).astype(np.float32)
+    a, b, c = (ints((m, k)), ints((m, k))), (ints((k, n)), ints((k, n))), (ints((m, n)), ints((m, n)))
+
+    def bf16_pair(x):  # flat bf16 buffer, interleaved or split planes, column-major
+        p0 = torch.from_numpy(np.ascontiguousarray(x[0].ravel(order="F")))
+        p1 = torch.from_numpy(np.ascontiguousarray(x[1].ravel(order="F")))
+        flat = torch.cat([p0, p1]) if split else torch.stack([p0, p1], dim=1).reshape(-1)
+        return flat.to(torch.bfloat16).cuda()
+
+    if kind == "complex":
+        cfg = tk.build_complex_config(m, n, k, tk.COMPLEXBF16, split=split)
+        z = lambda x: np.asfortranarray((x[0] + 1j * x[1]).astype(np.complex64))
+        want = O.gemm_pair(z(a), z(b), z(c))
+        w0, w1 = want.real, want.imag
+    else:
+        cfg = tk.build_dual_config(m, n, k, tk.DUALBF16, split=split)
+        dd = lambda x: np.asfortranarray(tk.dual_array(x[0], x[1], tk.DUAL32))
+        want = O.gemm_pair(dd(a), dd(b), dd(c), dual=True)
+        w0, w1 = want["value"], want["epsilon"]
+    cbuf = _pack_pair(c[0], c[1], None, split)
+    d = torch.zeros_like(cbuf)
+    tk.matmul(cfg, bf16_pair(a), bf16_pair(b), cbuf, d)
+    assert tk.last_run()["lane"] == "tcgen05"
+    got = _unpack_pair(d, (m, n), split)
+    assert np.array_equal(got[0], w0) and np.array_equal(got[1], w1)
+
+
 def _pack_pair(p0, p1, half, split):
     """Flat pair buffer (interleaved or split planes, column-major) as a CUDA tensor."""
     dt = np.float16 if half is not None else np.float32
