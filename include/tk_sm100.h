@@ -105,8 +105,9 @@ int tk_abi_version(void);
  * with tk_last_error() set when the plan is invalid. */
 int tk_plan_lane(const TkGemmPlan* plan);
 
-/* Device workspace (bytes) tk_gemm needs for this plan (de-interleave planes,
- * row/column sums of affine operand transforms).  Caller allocates it. */
+/* Device workspace (bytes) tk_gemm needs for this plan (de-interleave planes, gathered
+ * GETT operands, row/column sums of affine operand transforms, split-K partials and their
+ * counters).  Caller allocates it. */
 int64_t tk_workspace_bytes(const TkGemmPlan* plan);
 
 /* Execute one GEMM (replaces kernel.gemm_execute, kernel.py:253-330).
