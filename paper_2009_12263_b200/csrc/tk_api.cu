@@ -476,8 +476,13 @@ int launch_tc_pair(const tk::TcParams& prm, cudaStream_t s) {
     run.num_units = run.sk_first = run.num_tiles;
     run.sk_parts = 1;
   }
+  const char* eg = getenv("TK_PAIR_GRID");
+  if (run.nar_units > 0 && (max_clusters != pair_clusters() || eg)) {  // staggered lists assume P
+    run.num_units = run.num_tiles;
+    run.nar_units = 0;
+  }
   int clusters = std::min(run.num_units, max_clusters);
-  if (const char* e = getenv("TK_PAIR_GRID")) clusters = std::max(1, std::min(clusters, atoi(e)));
+  if (eg) clusters = std::max(1, std::min(clusters, atoi(eg)));
   const int grid = 2 * clusters;
   // programmatic dependent launch: the next GEMM in the stream may be scheduled while this one
   // drains; its CTAs run their prologue (barriers, TMEM, tensor-map prefetch) and then wait in
@@ -1031,14 +1036,15 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
       pp.num_units = pp.sk_first = pp.num_tiles;
       pp.sk_parts = 1;
       pp.nar_units = 0;
-      if (nsub == 2) {  // staggered start (opt-in, TK_STAGGER=1): half of the clusters begin
-        // with a half-width tile.  Measured: 16384^3 neutral, 8192^3 -6.5 % (the extra half
-        // tile lands on the critical cluster), so off by default.
+      if (nsub == 2) {  // staggered schedule (unit_at in tk_tc_gemm2.cuh): clusters [0, S)
+        // split one wide tile into a leading and a trailing half; balanced when T mod P >= S.
+        // Opt-in: bitwise equal, but measured 3-6 % slower (8192^3, 16384^3, 8192x16384x8192)
+        // -- under the power cap the overlapped drains raise average power and lower clocks.
         const char* e = getenv("TK_STAGGER");
-        const int nu = (pair_clusters() / 2) & ~1;
-        if (e && atoi(e) && pp.num_tiles >= nu) {
-          pp.nar_units = nu;
-          pp.num_units = pp.num_tiles + nu / 2;
+        const int P = pair_clusters(), S = P / 2;
+        if (e && atoi(e) && pp.num_tiles >= 2 * P) {
+          pp.nar_units = S;
+          pp.num_units = pp.num_tiles + S;  // (>= P: the grid is all P clusters)
         }
       }
       if (nsub == 1 && dense && w.splitk >= 0 && !getenv("TK_PAIR_GRID")) {

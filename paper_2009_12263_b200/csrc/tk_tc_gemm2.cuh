@@ -70,20 +70,38 @@ struct Tc2Plan {
 struct PairUnit {
   int tile, kb0, kb1, role, sk_tile, part, noff, narrow;
 };
-// NSUB 2 with a staggered start: units [0, nar_units) are the two 256-column halves of the
-// first nar_units/2 wide tiles; dealt round-robin, half of the clusters begin with a half-width
-// tile and run half a tile out of phase with the other half for the rest of the launch, so the
-// clusters' single-accumulator drains (C read + D write, HBM-bound when all clusters drain
-// together) alternate instead of coinciding.
 __device__ __forceinline__ PairUnit pair_unit(const TcParams& p, int u) {
-  if (p.nar_units > 0) {
-    if (u < p.nar_units) return PairUnit{u >> 1, 0, p.kb_total, 0, 0, 0, (u & 1) * 256, 1};
-    return PairUnit{(p.nar_units >> 1) + u - p.nar_units, 0, p.kb_total, 0, 0, 0, 0, 0};
-  }
   if (u < p.sk_first) return PairUnit{u, 0, p.kb_total, 0, 0, 0, 0, 0};
   const int v = u - p.sk_first, r = v / p.sk_parts, s = v - r * p.sk_parts;
   return PairUnit{p.sk_first + r, s * p.kb_total / p.sk_parts, (s + 1) * p.kb_total / p.sk_parts,
                   s == p.sk_parts - 1 ? 2 : 1, r, s, 0, 0};
+}
+// Per-cluster unit lists.  Default: units c, c+P, c+2P, ... (P clusters).  NSUB 2 staggered
+// (nar_units = S > 0): cluster c < S owns wide tile c and processes it as two half-width units,
+// the first at the start of its list and the second at its end; tiles S.. are dealt round-robin
+// starting at cluster S.  Half of the clusters thus run half a tile out of phase with the other
+// half, so the single-accumulator drains (C read + D write, HBM-bound when all clusters drain
+// together) alternate instead of coinciding, and every cluster still owns ceil(T/P) tiles'
+// worth of work when T mod P >= S.
+__device__ __forceinline__ int unit_count(const TcParams& p, int c, int P) {
+  if (p.nar_units > 0) {
+    const int S = p.nar_units, mid = p.num_tiles - S;
+    const int j0 = (c - S + P) % P;
+    return (j0 < mid ? (mid - 1 - j0) / P + 1 : 0) + (c < S ? 2 : 0);
+  }
+  return c < p.num_units ? (p.num_units - 1 - c) / P + 1 : 0;
+}
+__device__ __forceinline__ PairUnit unit_at(const TcParams& p, int c, int P, int idx, int count) {
+  if (p.nar_units > 0) {
+    const int S = p.nar_units;
+    if (c < S) {
+      if (idx == 0) return PairUnit{c, 0, p.kb_total, 0, 0, 0, 0, 1};
+      if (idx == count - 1) return PairUnit{c, 0, p.kb_total, 0, 0, 0, 256, 1};
+      --idx;
+    }
+    return PairUnit{S + (c - S + P) % P + idx * P, 0, p.kb_total, 0, 0, 0, 0, 0};
+  }
+  return pair_unit(p, c + idx * P);
 }
 
 template <bool DENSE_EPI, bool CSTREAM = false, int NSUB = 1, int BNI = 256, int CSL = TC2S_CSLOTS>
@@ -164,8 +182,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     // ------------------------------------------------------------ C loader (both CTAs)
     if (!p.c_zero && lane == 0) {
       uint32_t q = 0;
-      for (int u = cluster; u < p.num_units; u += nclusters) {
-        const PairUnit un = pair_unit(p, u);
+      const int nu = unit_count(p, cluster, nclusters);
+      for (int u = 0; u < nu; ++u) {
+        const PairUnit un = unit_at(p, cluster, nclusters, u, nu);
         if (un.role == 1) continue;  // partial K-parts never read C
         int mb, nb;
         tile_coords(p, un.tile, mb, nb);
@@ -190,8 +209,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int lu = 0;
-      for (int u = cluster; u < p.num_units; u += nclusters, ++lu) {
-        const PairUnit un = pair_unit(p, u);
+      const int nu = unit_count(p, cluster, nclusters);
+      for (int u = 0; u < nu; ++u, ++lu) {
+        const PairUnit un = unit_at(p, cluster, nclusters, u, nu);
         int mb, nb;
         tile_coords(p, un.tile, mb, nb);
         const int m0 = mb * 256 + int(rank) * 128;     // this CTA's rows of A
@@ -277,8 +297,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           tc_mma_f16_pair(d, a0, b0, idesc, (!first || kk > 0) ? 1u : 0u);
         }
       };
-      for (int u = cluster; u < p.num_units; u += nclusters, ++local) {
-        const PairUnit un = pair_unit(p, u);
+      const int nu = unit_count(p, cluster, nclusters);
+      for (int u = 0; u < nu; ++u, ++local) {
+        const PairUnit un = unit_at(p, cluster, nclusters, u, nu);
         if (NSUB == 1) {
           const int as = local & 1;
           const uint32_t aphase = (local >> 1) & 1;
@@ -353,8 +374,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     const int row_local = quarter * 32 + lane;
     int local = 0;
     uint32_t cq = 0;
-    for (int u = cluster; u < p.num_units; u += nclusters, ++local) {
-      const PairUnit un = pair_unit(p, u);
+    const int nu = unit_count(p, cluster, nclusters);
+    for (int u = 0; u < nu; ++u, ++local) {
+      const PairUnit un = unit_at(p, cluster, nclusters, u, nu);
       const int t = un.tile;
       int mb, nb;
       tile_coords(p, t, mb, nb);
@@ -416,7 +438,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         // (a half-width tile sits in TMEM columns [0,256): shift the base by its column offset)
         const uint32_t tb = tbase - uint32_t(un.noff);
         const int jbase = nb * BNP + un.noff + pass * BNI + half * PL::WCOLS;
-        if (blockIdx.x == p.dbg_cta && warp == 4 && lane == 0 && u + nclusters >= p.num_units) {
+        if (blockIdx.x == p.dbg_cta && warp == 4 && lane == 0 && u == nu - 1) {
           mbar_wait(tfull + as, aphase);
           TK_TS(4);
         }
