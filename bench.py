@@ -129,7 +129,7 @@ def run_reference(args):
     s0 = samples[0]
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong" if args.strong else "weak", "vs_baseline": None,
             "dtype": "f32 (fp16-valued inputs)", "data": "synthetic",
             "config": {"workload": f"dense GEMM D=A*B+C, M=N=K={n} column-major "
                                    "(bounded column-slab sample per step)", "n": n},
@@ -155,7 +155,11 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     m = k = args.n
-    n = args.n  # per-rank column slab (weak scaling)
+    # per-rank column slab: n x N columns (weak scaling, the default) or N/G of a fixed N x N x N
+    # problem (--strong: SURVEY 8e's "N=16384 over 2/4/8 GPUs")
+    n = args.n // world if args.strong else args.n
+    if n * (world if args.strong else 1) != args.n or n % 8:
+        raise SystemExit(f"--strong needs N divisible by 8 x world size (N={args.n}, G={world})")
     dt = tk.FLOAT16 if args.dtype == "fp16" else tk.BFLOAT16
     tdt = torch.float16 if args.dtype == "fp16" else torch.bfloat16
     g = torch.Generator(device=dev)
@@ -294,7 +298,7 @@ def run_ours(args):
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "higher_is_better": True, "scaling": "strong" if args.strong else "weak", "vs_baseline": None,
                 "dtype": args.dtype, "data": "synthetic",
                 "config": {"workload": f"dense GEMM D=A*B+C, fp16/bf16 A,B -> fp32 C,D, "
                                        f"column-major, M=K={m}, N={n} per GPU (column slab; "
@@ -398,6 +402,8 @@ def main():
     ap.add_argument("--dtype", choices=["fp16", "bf16"], default="fp16")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: the N x N x N problem split into G column slabs")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-library", action="store_true", help="skip the cuBLAS same-op context line")
     ap.add_argument("--fused-allgather", action="store_true",
