@@ -253,9 +253,19 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
   return r;
 }
+// Arrive on a (possibly remote) cluster barrier.  Default (.release.cta) semantics: the
+// arrivals only order TMEM reads (tcgen05.fence::before_thread_sync precedes them), never
+// global data.  An explicit .release.cluster arrive first makes every prior write visible
+// cluster-wide and stalls the issuing warp ~0.5 us (tools/mcast_probe.cu, PARRIVE=1).
+#ifndef TK_ARRIVE_CLUSTER_RELEASE
+#define TK_ARRIVE_CLUSTER_RELEASE 0
+#endif
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-               : "memory");
+  if (TK_ARRIVE_CLUSTER_RELEASE)
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+                 : "memory");
+  else
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // 2-SM TMA: data lands in this CTA's smem, transaction bytes are credited to `bar_cluster`
 // (the leader CTA's full barrier).
