@@ -1642,7 +1642,9 @@ int ex_pipelined(int tag, int ta, long long m, long long n, long long k, double 
   TK_CUDA(cudaMallocAsync(&db, sb, st.in));
   TK_CUDA(cudaMallocAsync(&dc, sc, st.in));
   TK_CUDA(cudaMemcpyAsync(da, a, sa, cudaMemcpyHostToDevice, st.in));
-  int slabs = int(std::max<long long>(1, std::min<long long>(8, n / 1024)));
+  int max_slabs = 8;
+  if (const char* e = getenv("TK_EX_SLABS")) max_slabs = std::max(1, atoi(e));
+  int slabs = int(std::max<long long>(1, std::min<long long>(max_slabs, n / 1024)));
   const long long w = ((n / slabs + 255) / 256) * 256;
   slabs = int((n + w - 1) / w);
   int rc = TK_OK;
