@@ -131,6 +131,29 @@ def test_split_k_last_wave(cuda, mnk, splitk, monkeypatch):
             assert O.rel_err(got, want) <= O.tolerance(k), O.rel_err(got, want)
 
 
+@pytest.mark.parametrize("mnk", [(8192, 8192, 8192), (4096, 8192 + 512, 8192)])
+def test_staggered_schedule_bitwise(cuda, mnk, monkeypatch):
+    """The opt-in staggered 256 x 512 schedule (half of the clusters split one tile into a
+    leading and a trailing half) covers every tile exactly once: bitwise equal to the default
+    schedule with serpentine K off (same k order per tile)."""
+    m, n, k = mnk
+    monkeypatch.setenv("TK_SERPENTINE", "0")
+    monkeypatch.setenv("TK_PAIR_NSUB", "2")
+    g = torch.Generator(device=cuda)
+    g.manual_seed(5)
+    a = torch.randn(m * k, generator=g, device=cuda).half()
+    b = torch.randn(k * n, generator=g, device=cuda).half()
+    c = torch.randn(m * n, generator=g, device=cuda)
+    cfg = tk.build_dense_config(m, n, k, np.float16)
+    outs = []
+    for stagger in ("0", "1"):
+        monkeypatch.setenv("TK_STAGGER", stagger)
+        d = torch.full((m * n,), float("nan"), device=cuda)
+        tk.matmul(cfg, a, b, c, d)
+        outs.append(d)
+    assert torch.equal(outs[0], outs[1])
+
+
 @pytest.mark.parametrize("trans", ["nn", "tt"])
 def test_full_size_c3_tile_shapes_agree(cuda, trans, monkeypatch):
     """The bench-size (8192^3) C3 epilogue (alpha/beta, bias, ReLU) on the default 256 x 512
