@@ -627,6 +627,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(const __grid_con
       const uint32_t b_step = p.b_mn ? 2048u : 32u;
       const uint32_t a_lbo = a_mn ? 8192u : 16u;
       const uint32_t b_lbo = p.b_mn ? 8192u : 16u;
+      // descriptors built once; per MMA only the start-address field advances (16-byte units,
+      // no carry: shared memory < 256 KB)
+      const uint64_t a0d = sdesc_sw128(smem_u32(a_tile(0, 0)), a_lbo, 1024);
+      const uint64_t b0d = sdesc_sw128(smem_u32(b_tile(0, 0)), b_lbo, 1024);
+      const uint64_t a1d = a0d + uint32_t(TC_A_TILE_BYTES >> 4);
+      const uint64_t b1d = b0d + uint32_t(S::B_TILE_BYTES >> 4);
+      const uint32_t a_kk = a_step >> 4, b_kk = b_step >> 4;
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
@@ -643,16 +650,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(const __grid_con
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
+          const uint32_t so = uint32_t(stage) * uint32_t(S::STAGE_BYTES >> 4);
 #pragma unroll
           for (int kk = 0; kk < TC_BK / 16; ++kk) {
             const uint32_t acc = (kb > kb0 || kk > 0) ? 1u : 0u;
-            const uint64_t a0 = sdesc_sw128(smem_u32(a_tile(stage, 0)) + kk * a_step, a_lbo, 1024);
-            const uint64_t b0 = sdesc_sw128(smem_u32(b_tile(stage, 0)) + kk * b_step, b_lbo, 1024);
+            const uint64_t a0 = a0d + so + kk * a_kk;
+            const uint64_t b0 = b0d + so + kk * b_kk;
             if (OP == OP_REAL) {
               tc_mma_f16(d0, a0, b0, idesc, acc);
             } else {
-              const uint64_t a1 = sdesc_sw128(smem_u32(a_tile(stage, 1)) + kk * a_step, a_lbo, 1024);
-              const uint64_t b1 = sdesc_sw128(smem_u32(b_tile(stage, 1)) + kk * b_step, b_lbo, 1024);
+              const uint64_t a1 = a1d + so + kk * a_kk;
+              const uint64_t b1 = b1d + so + kk * b_kk;
               if (OP == OP_COMPLEX) {
                 tc_mma_f16(d0, a0, b0, idesc, acc);      // Re += Ar*Br
                 tc_mma_f16(d0, a1, b1, idesc_neg, 1u);   // Re += (-Ai)*Bi

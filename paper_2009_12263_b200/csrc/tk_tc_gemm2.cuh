@@ -287,15 +287,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
+      // Descriptors are built once; per MMA only the start-address field (bits 0-13, in 16-byte
+      // units, never carrying: shared memory < 256 KB) advances.  The issuing thread's
+      // dependent-instruction chain, not the tensor core, bounds N=64/128 tiles (a diagnostic
+      // build measured ~64 clocks per MMA with the descriptors rebuilt each time).
+      const uint64_t a_desc0 = sdesc_sw128(smem_u32(a_tile(0)), a_lbo, 1024);
+      const uint64_t b_desc0 = sdesc_sw128(smem_u32(b_tile(0)), b_lbo, 1024);
+      const uint32_t a_kk = a_step >> 4, b_kk = b_step >> 4;
+      const bool no_mma = p.dbg_skip_epi & 4;  // diagnostic: operand traffic without MMAs
       auto issue = [&](int st, int sub, uint32_t d, bool first) {
+        if (no_mma) return;
+        const uint32_t so = uint32_t(st) * uint32_t(PL::STAGE_BYTES >> 4);
+        const uint64_t a0 = a_desc0 + so;
+        const uint64_t b0 = b_desc0 + so + uint32_t(sub * (PL::B_BYTES >> 4));
 #pragma unroll
-        for (int kk = 0; kk < TC_BK / 16; ++kk) {
-          if (p.dbg_skip_epi & 4) break;  // diagnostic: operand traffic without MMAs
-          const uint64_t a0 = sdesc_sw128(smem_u32(a_tile(st)) + kk * a_step, a_lbo, 1024);
-          const uint64_t b0 =
-              sdesc_sw128(smem_u32(b_tile(st) + sub * PL::B_BYTES) + kk * b_step, b_lbo, 1024);
-          tc_mma_f16_pair(d, a0, b0, idesc, (!first || kk > 0) ? 1u : 0u);
-        }
+        for (int kk = 0; kk < TC_BK / 16; ++kk)
+          tc_mma_f16_pair(d, a0 + kk * a_kk, b0 + kk * b_kk, idesc, (!first || kk > 0) ? 1u : 0u);
       };
       const int nu = unit_count(p, cluster, nclusters);
       for (int u = 0; u < nu; ++u, ++local) {
