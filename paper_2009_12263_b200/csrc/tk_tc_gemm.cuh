@@ -172,8 +172,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-#define TK_TS(i) do { if (blockIdx.x == p.dbg_cta) g_dbg_ts[i] = gtimer(); } while (0)
-#define TK_TS_EPI(i) do { if (blockIdx.x == p.dbg_cta && (threadIdx.x >> 5) == 4 && (threadIdx.x & 31) == 0) g_dbg_ts[i] = gtimer(); } while (0)
+#ifndef TK_STAMPS
+#define TK_STAMPS 0  // CTA timestamps for tools/ts_probe.py (build with -DTK_STAMPS=1): ~60 ns per K block on the MMA thread
+#endif
+#define TK_TS(i) do { if (TK_STAMPS && blockIdx.x == p.dbg_cta) g_dbg_ts[i] = gtimer(); } while (0)
+#define TK_TS_EPI(i) do { if (TK_STAMPS && blockIdx.x == p.dbg_cta && (threadIdx.x >> 5) == 4 && (threadIdx.x & 31) == 0) g_dbg_ts[i] = gtimer(); } while (0)
 
 // Split-K partials to fold into the accumulator before the epilogue: this thread's row of the
 // first partial block (column stride 128), n blocks `pstride` floats apart, summed in order.
