@@ -206,6 +206,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     // ------------------------------------------------------------ producer (both CTAs)
     if (lane == 0) {
       const uint64_t pol = policy_code(p.pol_a), pol_b = policy_code(p.pol_b);
+      // uniform per-launch decisions hoisted out of the K loop (the single producer thread's
+      // dependent-instruction chain is on the critical path for short tiles)
+      const bool no_load = p.dbg_skip_epi & 2;
+      const bool c_pf = CSTREAM && p.c_pf_kb > 0 && !p.c_zero;
+      const int a_mode = p.a_mn ? ((p.mn3d & 1) ? 0 : 1) : 2;  // 3-D MN box / two 2-D MN boxes / K-major
+      const int b_mode = p.b_mn ? ((p.mn3d & 2) ? 0 : 1) : 2;
       int stage = 0;
       uint32_t phase = 0;
       int lu = 0;
@@ -217,6 +223,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         const int m0 = mb * 256 + int(rank) * 128;     // this CTA's rows of A
         const int n0 = nb * BNP + un.noff + int(rank) * (BNI / 2);  // this CTA's columns of B (per MMA)
         const int nsub_u = un.narrow ? 1 : NSUB;
+        const uint32_t tx = 2 * (TC2_TILE_BYTES + nsub_u * PL::B_BYTES);
         // serpentine K: every other tile of a cluster walks K downwards, so the next
         // wave starts on the K-slices the previous one loaded last (still in L2)
         const bool rev = p.serp && (lu & 1);
@@ -224,12 +231,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           const int kb = rev ? un.kb1 - 1 - ki : un.kb0 + ki;
           const int k0 = kb * TC_BK;
           mbar_wait(&empty[stage], phase ^ 1);
-          if (p.dbg_skip_epi & 2) {  // diagnostic: MMA issue rate without operand traffic
+          if (no_load) {  // diagnostic: MMA issue rate without operand traffic
             if (leader) mbar_arrive(&full[stage]);
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
             continue;
           }
-          if (CSTREAM && p.c_pf_kb > 0 && !p.c_zero) {
+          if (c_pf) {
             // warm L2 with this CTA's C block so the (non-overlapped part of the) drain hits L2
             const int at = ki - (un.kb1 - un.kb0 - p.c_pf_kb);  // k-blocks into the prefetch span
             const int nbox = 4 * ((un.narrow ? 256 : BNP) / 32);
@@ -248,11 +255,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
                   tma_prefetch_l2_2d(&p.tcmap, mb * 256 + int(rank) * 128 + r * 32, nb * BNP + un.noff + c * 32);
             }
           }
-          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (TC2_TILE_BYTES + nsub_u * PL::B_BYTES));
+          if (leader) mbar_arrive_expect_tx(&full[stage], tx);
           const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
-          if (p.a_mn && (p.mn3d & 1)) {
+          if (a_mode == 0) {
             tma_load_3d_pair(a_tile(stage), &p.ta[0], fb, 0, k0, m0 >> 6, pol);
-          } else if (p.a_mn) {
+          } else if (a_mode == 1) {
             tma_load_2d_pair(a_tile(stage), &p.ta[0], fb, m0, k0, pol);
             tma_load_2d_pair(a_tile(stage) + 8192, &p.ta[0], fb, m0 + 64, k0, pol);
           } else {
@@ -263,9 +270,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
             if (sub >= nsub_u) break;
             uint8_t* bt = b_tile(stage) + sub * PL::B_BYTES;
             const int nn = n0 + sub * BNI;
-            if (p.b_mn && (p.mn3d & 2)) {
+            if (b_mode == 0) {
               tma_load_3d_pair(bt, &p.tb[0], fb, 0, k0, nn >> 6, pol_b);
-            } else if (p.b_mn) {  // 64-column atoms (BNI >= 128)
+            } else if (b_mode == 1) {  // 64-column atoms (BNI >= 128)
               for (int h = 0; h < BNI / 128; ++h)
                 tma_load_2d_pair(bt + h * 8192, &p.tb[0], fb, nn + 64 * h, k0, pol_b);
             } else {

@@ -1,4 +1,6 @@
-"""Where does a small pair-kernel launch spend its time: CTA-0 globaltimer stamps (us)."""
+"""Where does a small pair-kernel launch spend its time: CTA-0 globaltimer stamps (us).
+Needs a build with the stamps compiled in: tools/build_variants.sh stamps "-DTK_STAMPS=1" and
+TK_SM100_LIB=build/var_stamps/libtk_sm100.so."""
 import ctypes
 import os
 import sys
