@@ -475,6 +475,7 @@ int launch_tc_pair(const tk::TcParams& prm, cudaStream_t s) {
   if (run.sk_parts > 1 && max_clusters != pair_clusters()) {  // split parts must all be co-resident
     run.num_units = run.sk_first = run.num_tiles;
     run.sk_parts = 1;
+    run.sk_tma = 0;
   }
   const char* eg = getenv("TK_PAIR_GRID");
   if (run.nar_units > 0 && (max_clusters != pair_clusters() || eg)) {  // staggered lists assume P
@@ -516,7 +517,7 @@ int launch_tc_pair_bni(const tk::TcParams& prm, int bni, cudaStream_t s) {
   if (bni == 128) return launch_tc_pair<DENSE, CSTREAM, 1, 128>(prm, s);
   // single wave, 256-wide tiles: a 4-slot C ring holds each warp's whole C block
   const char* e = getenv("TK_PAIR_DEEPC");
-  if (CSTREAM && prm.num_units <= pair_clusters() && (!e || atoi(e)))
+  if (CSTREAM && prm.num_units <= pair_clusters() && !prm.sk_tma && (!e || atoi(e)))
     return launch_tc_pair<DENSE, CSTREAM, 1, 256, 4>(prm, s);
   return launch_tc_pair<DENSE, CSTREAM, 1, 256>(prm, s);
 }
@@ -1098,6 +1099,17 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
         pp.c_pf_spread = 0;
         if (const char* e = getenv("TK_C_PF_SPREAD")) pp.c_pf_spread = atoi(e);
         pp.c_pf_kb = std::min(pp.c_pf_kb, pp.kb_total);
+        // split-K partials as TMA boxes through the C ring (written from the ring by the K-parts,
+        // loaded into it by the last part's C loader) instead of per-thread stores and loads
+        pp.sk_tma = 0;
+        if (pp.sk_parts > 1 && !prm.c_zero && pp.d_tma) {
+          const char* e = getenv("TK_SK_TMA");
+          if (!e || atoi(e)) {
+            const int64_t cols = int64_t(pp.num_units - pp.sk_first) / pp.sk_parts * (pp.sk_parts - 1) * 2 * bni;
+            if ((rc = make_map_2d(&pp.tskmap, pp.sk_ws, TK_F32, 128, cols, 128, 32, 32))) return rc;
+            pp.sk_tma = 1;
+          }
+        }
         if (nsub == 2) {
           const char* e = getenv("TK_NSUB2_CSL");  // C-ring slots per warp (tuning)
           const int csl = e ? atoi(e) : 2;

@@ -106,10 +106,12 @@ struct TcParams {
   // leave raw FP32 partials in sk_ws and count down sk_flags[r], the last part reduces them.
   int32_t num_units, sk_first, sk_parts, dbg_cta;
   int32_t vec_ok, serp;          // diag_stream_kernel: 16-byte vector path legal; pair kernel: serpentine K
-  int32_t pdl, pad5;             // pair kernel launched with programmatic stream serialisation
+  int32_t pdl;                   // pair kernel launched with programmatic stream serialisation
+  int32_t sk_tma;                // split-K partials move as 32x32 TMA boxes through the C ring (tskmap)
   // fused all-gather of D over peer memory (NVLink): the streamed epilogue TMA-stores every D
   // box to the local slab and to the same slab position inside each peer's full-D buffer
   CUtensorMap tdpeer[7];
+  CUtensorMap tskmap;            // split-K workspace as {128 rows, blocks * BNP columns} fp32
   int32_t npeer, pad7;
   int32_t c_ident, r_ident, s_ident, nar_units;  // empty transform programs: skip the stage;
                                                  // pair NSUB 2: half-width first units (stagger)
@@ -403,6 +405,28 @@ __device__ __forceinline__ void epilogue_stream(const TcParams& p, uint64_t* tfu
     const int jl = j0 + lane;
     const float bcol = (p.bias_axis == 1 && jl < p.n) ? p.bias[jl] : 0.f;
     const float qcol = (p.affine && p.colsum_b && jl < p.n) ? p.aff_q * p.colsum_b[jl] : 0.f;
+    float pv[SK ? 32 : 1];
+    if constexpr (SK) {
+      if (p.sk_tma) {
+        // the other K-parts' partial boxes come through the ring ahead of this chunk's C box
+        // (summed in part order, as sk_gather does); each slot is handed back one use later
+        for (int s = 0; s < sk.n; ++s, ++cq) {
+          const uint32_t sl = cq % CSLOTS;
+          const uint32_t bs = smem_u32(ring + sl * (TC_CBOX_BYTES / 4));
+          mbar_wait(&cfull[sl], (cq / CSLOTS) & 1);
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) {
+            const float v = lds_f32(bs + uint32_t(jj * 32 + lane) * 4u);
+            pv[jj] = s ? pv[jj] + v : v;
+          }
+          __syncwarp();
+          if (lane == 0) {
+            bulk_wait_read<0>();
+            if (cq >= 1u) mbar_arrive(&cempty[(cq - 1) % CSLOTS]);
+          }
+        }
+      }
+    }
     const uint32_t slot = cq % CSLOTS;
     float* box = ring + slot * (TC_CBOX_BYTES / 4);
     const uint32_t box_s = smem_u32(box);  // explicit shared-space accesses (box is a generic pointer)
@@ -416,8 +440,9 @@ __device__ __forceinline__ void epilogue_stream(const TcParams& p, uint64_t* tfu
       if (lane == 0) bulk_wait_read<CSLOTS - 1>();  // slot's previous store has read it
       __syncwarp();
     }
-    float pv[SK ? 32 : 1];
-    if constexpr (SK) sk_gather(sk, j0 - jbase + (jbase % BN), pv);
+    if constexpr (SK) {
+      if (!p.sk_tma) sk_gather(sk, j0 - jbase + (jbase % BN), pv);
+    }
     tmem_ld_wait();
     if (ch == 0) TK_TS_EPI(8);
     float out[32];

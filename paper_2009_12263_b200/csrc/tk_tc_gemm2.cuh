@@ -183,12 +183,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     if (!p.c_zero && lane == 0) {
       uint32_t q = 0;
       const int nu = unit_count(p, cluster, nclusters);
+      // ring slot q (per epilogue warp): wait until the epilogue released its previous use
+      auto claim = [&](uint32_t qq, int w) -> int {
+        const int bi = w * CSL + int(qq % CSL);
+        mbar_wait_sleep(&cempty[bi], ((qq / CSL) & 1) ^ 1);
+        return bi;
+      };
       for (int u = 0; u < nu; ++u) {
         const PairUnit un = unit_at(p, cluster, nclusters, u, nu);
-        if (un.role == 1) continue;  // partial K-parts never read C
+        if (un.role == 1) {  // partial K-parts never read C
+          if (p.sk_tma) {    // ... but stage their outgoing partial boxes in the ring: claim slots
+            for (int ch = 0; ch < CH; ++ch, ++q)
+              for (int w = 0; w < TC_EPI_WARPS; ++w) mbar_arrive(&cfull[claim(q, w)]);
+          }
+          continue;
+        }
         int mb, nb;
         tile_coords(p, un.tile, mb, nb);
+        if (un.role == 2 && p.sk_tma) {
+          // last K-part: every other part's partial must be in memory before it is loaded
+          const int want = (p.sk_parts - 1) * 2 * TC_EPI_WARPS;
+          int got;
+          do {
+            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(got) : "l"(p.sk_flags + un.sk_tile) : "memory");
+            if (got < want) __nanosleep(128);
+          } while (got < want);
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
         for (int ch = 0; ch < (un.narrow ? 1 : NSUB) * CH; ++ch, ++q) {
+          if (un.role == 2 && p.sk_tma) {
+            // the other parts' partial boxes of this chunk, in part order, ahead of the C box
+            for (int s = 0; s < p.sk_parts - 1; ++s, ++q)
+              for (int w = 0; w < TC_EPI_WARPS; ++w) {
+                const int bi = claim(q, w);
+                const int blk = (un.sk_tile * (p.sk_parts - 1) + s) * 2 + int(rank);
+                mbar_arrive_expect_tx(&cfull[bi], TC_CBOX_BYTES);
+                tma_load_2d(smem + PL::CRING + bi * TC_CBOX_BYTES, &p.tskmap, &cfull[bi], (w & 3) * 32,
+                            blk * BNP + (w >> 2) * PL::WCOLS + ch * 32, policy_evict_first());
+              }
+          }
           const uint32_t slot = q % CSL, ph = (q / CSL) & 1;
           for (int w = 0; w < TC_EPI_WARPS; ++w) {
             const int bi = w * CSL + int(slot);
@@ -408,6 +441,47 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         mbar_wait_sleep(tfull + as, aphase);
         tc_fence_after();
         const uint32_t tbase = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(as * BNI);
+        if (CSTREAM && p.sk_tma) {
+          // stage each 32x32 box in a ring slot the C loader claimed for it, TMA-store it to
+          // the workspace, release slots like the D path (once the next store has been issued
+          // and this one has read its slot), then publish after the stores have completed
+          float* my_ring = cring + ew * CSL * (TC_CBOX_BYTES / 4);
+          uint64_t* wfull = cfull + ew * CSL;
+          uint64_t* wempty = cempty + ew * CSL;
+          const int blk_id = (un.sk_tile * (p.sk_parts - 1) + un.part) * 2 + int(rank);
+#pragma unroll 1
+          for (int ch = 0; ch < CH; ++ch, ++cq) {
+            const int col = half * PL::WCOLS + ch * 32;
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(tbase + uint32_t(col), r);
+            const uint32_t slot = cq % CSL;
+            float* box = my_ring + slot * (TC_CBOX_BYTES / 4);
+            const uint32_t box_s = smem_u32(box);
+            mbar_wait(&wfull[slot], (cq / CSL) & 1);
+            tmem_ld_wait();
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) sts_f32(box_s + uint32_t(jj * 32 + lane) * 4u, __uint_as_float(r[jj]));
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&p.tskmap, box, quarter * 32, blk_id * BNP + col);
+              bulk_commit();
+              bulk_wait_read<1>();
+              if (cq >= 1u) mbar_arrive(&wempty[(cq - 1) % CSL]);
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[as]), 0));
+            bulk_wait<0>();  // this warp's partial boxes are in memory
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            __threadfence();
+            atomicAdd(p.sk_flags + un.sk_tile, 1);
+          }
+          __syncwarp();
+          continue;
+        }
         float* out = sk_row + int64_t(un.part) * 2 * blk;
 #pragma unroll 1
         for (int ch = 0; ch < CH; ++ch) {
@@ -429,7 +503,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       SkIn sk{nullptr, 0, 0};
       if (NSUB == 1 && un.role == 2) {
         // last K-part: wait until every warp of every other part has published its partial
-        if (lane == 0) {
+        // (with sk_tma the C loader waits and the partials arrive through the ring)
+        if (lane == 0 && !(CSTREAM && p.sk_tma)) {
           const int want = (p.sk_parts - 1) * 2 * TC_EPI_WARPS;
           int got;
           do {

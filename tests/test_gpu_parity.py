@@ -131,6 +131,28 @@ def test_split_k_last_wave(cuda, mnk, splitk, monkeypatch):
             assert O.rel_err(got, want) <= O.tolerance(k), O.rel_err(got, want)
 
 
+@pytest.mark.parametrize("mnk,minkb", [((2560, 2560, 8192), "64"), ((1024, 1024, 1024), "4")])
+def test_split_k_ring_matches_direct(cuda, mnk, minkb, monkeypatch):
+    """Split-K partials moved as TMA boxes through the C ring (default) and by per-thread
+    stores/loads (TK_SK_TMA=0) sum in the same order: bitwise equal on random inputs."""
+    m, n, k = mnk
+    monkeypatch.setenv("TK_PAIR_BNI", "256")
+    monkeypatch.setenv("TK_SPLITK_MINKB", minkb)
+    g = torch.Generator(device=cuda)
+    g.manual_seed(9)
+    a = torch.randn(m * k, generator=g, device=cuda).half()
+    b = torch.randn(k * n, generator=g, device=cuda).half()
+    c = torch.randn(m * n, generator=g, device=cuda)
+    cfg = tk.build_dense_config(m, n, k, np.float16)
+    outs = []
+    for mode in ("1", "0"):
+        monkeypatch.setenv("TK_SK_TMA", mode)
+        d = torch.full((m * n,), float("nan"), device=cuda)
+        tk.matmul(cfg, a, b, c, d)
+        outs.append(d)
+    assert torch.equal(outs[0], outs[1])
+
+
 @pytest.mark.parametrize("mnk", [(8192, 8192, 8192), (4096, 8192 + 512, 8192)])
 def test_staggered_schedule_bitwise(cuda, mnk, monkeypatch):
     """The opt-in staggered 256 x 512 schedule (half of the clusters split one tile into a
