@@ -517,7 +517,7 @@ int launch_tc_pair_bni(const tk::TcParams& prm, int bni, cudaStream_t s) {
   if (bni == 128) return launch_tc_pair<DENSE, CSTREAM, 1, 128>(prm, s);
   // single wave, 256-wide tiles: a 4-slot C ring holds each warp's whole C block
   const char* e = getenv("TK_PAIR_DEEPC");
-  if (CSTREAM && prm.num_units <= pair_clusters() && !prm.sk_tma && (!e || atoi(e)))
+  if (CSTREAM && prm.num_units <= pair_clusters() && (!e || atoi(e)))
     return launch_tc_pair<DENSE, CSTREAM, 1, 256, 4>(prm, s);
   return launch_tc_pair<DENSE, CSTREAM, 1, 256>(prm, s);
 }

@@ -382,6 +382,23 @@ __device__ __forceinline__ void epilogue_dense(const TcParams& p, uint64_t* tful
 }
 
 
+// Release ring use cq - LAG once the stores committed after it no longer need their slots' data:
+// `smask` bit i says whether use cq - i committed a TMA store (split-K rings mix store uses with
+// partial-read uses, so the number of groups allowed in flight varies).  Lane 0 only.
+template <int CSLOTS>
+__device__ __forceinline__ void ring_release(uint64_t* cempty, uint32_t cq, uint32_t smask) {
+  static_assert(CSLOTS <= 4, "LAG <= 3");
+  constexpr int LAG = CSLOTS >= 4 ? CSLOTS - 1 : 1;
+  if (cq < uint32_t(LAG)) return;
+  switch (__popc(smask & ((1u << LAG) - 1u))) {
+    case 0: bulk_wait_read<0>(); break;
+    case 1: bulk_wait_read<1>(); break;
+    case 2: bulk_wait_read<2>(); break;
+    default: bulk_wait_read<3>(); break;
+  }
+  mbar_arrive(&cempty[(cq - LAG) % CSLOTS]);
+}
+
 // Dense column-major epilogue for HBM-bound shapes: C arrives in a per-warp ring of TMA boxes
 // filled by the loader warp; D is written back into the same slot and stored with one TMA
 // bulk store per 32x32 box (the slot is handed back to the loader once that store has read it).
@@ -389,7 +406,8 @@ template <int COLS, int BN, int CSLOTS = TC_CSLOTS, bool SK = false>
 __device__ __forceinline__ void epilogue_stream(const TcParams& p, uint64_t* tfull, uint32_t aphase,
                                                 uint32_t tbase, int i, int jbase, int lane,
                                                 float* ring, uint64_t* cfull, uint64_t* cempty,
-                                                uint32_t& cq, int row0, SkIn sk = SkIn{nullptr, 0, 0}) {
+                                                uint32_t& cq, int row0, SkIn sk = SkIn{nullptr, 0, 0},
+                                                uint32_t* smask = nullptr) {
   const bool row_ok = i < p.m;
   const bool has_c = !p.c_zero;
   float* dp = reinterpret_cast<float*>(p.d_ptr) + (row_ok ? i : 0);
@@ -420,10 +438,8 @@ __device__ __forceinline__ void epilogue_stream(const TcParams& p, uint64_t* tfu
             pv[jj] = s ? pv[jj] + v : v;
           }
           __syncwarp();
-          if (lane == 0) {
-            bulk_wait_read<0>();
-            if (cq >= 1u) mbar_arrive(&cempty[(cq - 1) % CSLOTS]);
-          }
+          *smask <<= 1;  // a read use: no store
+          if (lane == 0) ring_release<CSLOTS>(cempty, cq, *smask);
         }
       }
     }
@@ -463,8 +479,12 @@ __device__ __forceinline__ void epilogue_stream(const TcParams& p, uint64_t* tfu
           // chunk's slot (the loader runs one chunk ahead); a deep ring (>= 4 slots, used when
           // the whole C block is prefetched) lets CSLOTS-1 stores stay in flight instead
           constexpr int LAG = CSLOTS >= 4 ? CSLOTS - 1 : 1;
-          bulk_wait_read<LAG>();
-          if (cq >= uint32_t(LAG)) mbar_arrive(&cempty[(cq - LAG) % CSLOTS]);
+          if (SK && p.sk_tma) {
+            ring_release<CSLOTS>(cempty, cq, (*smask << 1) | 1u);
+          } else {
+            bulk_wait_read<LAG>();
+            if (cq >= uint32_t(LAG)) mbar_arrive(&cempty[(cq - LAG) % CSLOTS]);
+          }
         }
       }
     } else {
@@ -478,6 +498,7 @@ __device__ __forceinline__ void epilogue_stream(const TcParams& p, uint64_t* tfu
           if (j0 + jj < p.n) __stcs(dp + int64_t(j0 + jj) * p.ldd, out[jj]);
       }
     }
+    if (SK && p.sk_tma) *smask = (*smask << 1) | 1u;  // a store use
     ++cq;
   }
 }

@@ -421,6 +421,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     const int row_local = quarter * 32 + lane;
     int local = 0;
     uint32_t cq = 0;
+    // bit i: ring use cq - i committed a TMA store (every use before a split unit did; split
+    // units, always a cluster's last, mix in partial-read uses -- see ring_release)
+    uint32_t smask = 0xFFFFFFFFu;
     const int nu = unit_count(p, cluster, nclusters);
     for (int u = 0; u < nu; ++u, ++local) {
       const PairUnit un = unit_at(p, cluster, nclusters, u, nu);
@@ -463,11 +466,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
             for (int jj = 0; jj < 32; ++jj) sts_f32(box_s + uint32_t(jj * 32 + lane) * 4u, __uint_as_float(r[jj]));
             fence_proxy_async_smem();
             __syncwarp();
+            smask = (smask << 1) | 1u;
             if (lane == 0) {
               tma_store_2d(&p.tskmap, box, quarter * 32, blk_id * BNP + col);
               bulk_commit();
-              bulk_wait_read<1>();
-              if (cq >= 1u) mbar_arrive(&wempty[(cq - 1) % CSL]);
+              ring_release<CSL>(wempty, cq, smask);
             }
           }
           tc_fence_before();
@@ -535,7 +538,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           if (sk.p)
             epilogue_stream<PL::WCOLS, BNP, CSL, true>(p, tfull + as, aphase, tb, i, jbase, lane, my_ring,
                                                    cfull + ew * CSL, cempty + ew * CSL, cq,
-                                                   row0, sk);
+                                                   row0, sk, &smask);
           else
             epilogue_stream<PL::WCOLS, BNP, CSL>(p, tfull + as, aphase, tb, i, jbase, lane, my_ring,
                                                    cfull + ew * CSL, cempty + ew * CSL, cq, row0);
