@@ -1,13 +1,22 @@
 """Benchmark: FP16 -> FP32 GEMM TFLOPS on B200 (BASELINE.json metric), one JSON line.
 
-Workload (BASELINE.json configs[1], the north-star point): D = A*B + C, column-major,
-M = K = 8192, fp16 A/B, fp32 C/D, reference `build_dense_config` semantics.  Multi-GPU:
-one process per GPU, C sharded by column slabs of B with A replicated (no data-path
-collective): every rank owns an M x n slab, so the global problem is M x (n*G) x K and
-`scaling` is "weak".
+Workload (BASELINE.json configs[1]): D = A*B + C, column-major, fp16 A/B, fp32 C/D,
+reference `build_dense_config` semantics.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--n 8192] [--dtype fp16|bf16]
+* N = 1 GPU: the north-star point, M = N = K = 8192.
+* N > 1 GPUs (BASELINE configs[1]'s "N=16384 column-sharded at 2/4/8 GPUs", the default):
+  one process per GPU, the fixed 16384^3 problem split into G column slabs of B/C/D with A
+  replicated -- no data-path collective, `scaling` "strong".  `--weak` instead gives every
+  rank its own n-column slab of an M x (n*G) x K problem.  The NCCL all-gather of the D
+  slabs (the north star's optional collective) is timed separately, never in `value`.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--n N] [--dtype fp16|bf16] [--weak]
   python bench.py --impl reference ...   # the reference's own CPU implementation
+  python bench.py --gpus 2 --dry-run     # launcher/rank plumbing only (gloo, no GPU work)
+
+`--gpus N` without a torchrun environment re-launches this script under
+`torch.distributed.run` with N ranks (127.0.0.1 rendezvous); the line's `n_gpus` must equal
+`--gpus` or the run fails.
 
 Timing: W untimed steps, then K steps bracketed by barrier + cuda synchronize, CUDA events
 on the launching stream, max over ranks.  Inputs (768 MiB at n=8192) exceed the 126 MB L2.
@@ -18,6 +27,8 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
+import subprocess
 import sys
 import time
 
@@ -89,6 +100,8 @@ def cpu_sample(m, k, threads):
     """
     tilekit, kind = _reference_module()
     s = 1024 * max(1, min(8, -(-threads // 8)))  # one 1024-column block per 8 host threads
+    if m > 8192:  # keep a step's CPU work at the 8192^3 sample's size (a few seconds)
+        s = max(256, s * 8192 * 8192 // (m * k))
     a, b, c = _cpu_inputs(m, k, s)
     flops = 2.0 * m * s * k
     if tilekit is not None:
@@ -155,11 +168,11 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     m = k = args.n
-    # per-rank column slab: n x N columns (weak scaling, the default) or N/G of a fixed N x N x N
-    # problem (--strong: SURVEY 8e's "N=16384 over 2/4/8 GPUs")
+    # per-rank column slab: N/G columns of the fixed N x N x N problem (strong: the default at
+    # N > 1 GPUs, SURVEY 8e's "N=16384 over 2/4/8 GPUs") or n columns each (--weak)
     n = args.n // world if args.strong else args.n
     if n * (world if args.strong else 1) != args.n or n % 8:
-        raise SystemExit(f"--strong needs N divisible by 8 x world size (N={args.n}, G={world})")
+        raise SystemExit(f"strong scaling needs N divisible by 8 x world size (N={args.n}, G={world})")
     dt = tk.FLOAT16 if args.dtype == "fp16" else tk.BFLOAT16
     tdt = torch.float16 if args.dtype == "fp16" else torch.bfloat16
     g = torch.Generator(device=dev)
@@ -214,7 +227,7 @@ def run_ours(args):
     value = flops_rank * world / (ms * 1e-3) / 1e12
 
     # roofline of the dominant (only) kernel: one tcgen05 launch per step
-    burst, sustained, hbm, src = _peaks()
+    burst, sustained_peak, hbm, src = _peaks()
     kernel_ms = ms / launches_per_step
     achieved = flops_rank / (kernel_ms * 1e-3) / 1e12
     traffic = args.traffic
@@ -230,7 +243,7 @@ def run_ours(args):
                 "algorithmic_flops_per_launch": flops_rank,
                 "algorithmic_bytes_per_launch": 2 * (m * k + k * n) + 8 * m * n,
                 "peak_source": f"{src} bf16 burst (MEASURED_PEAKS.json)",
-                "frac_of_sustained": achieved / sustained if sustained else None,
+                "frac_of_sustained": achieved / sustained_peak if sustained_peak else None,
                 "frac_of_spec_2250": achieved / 2250.0}
 
     # optional collective, timed separately (north star: "an optional NCCL all-gather of C over
@@ -263,6 +276,33 @@ def run_ours(args):
             del full
         except Exception as exc:
             allgather = {"unavailable": str(exc)[:160]}
+
+    # sustained window (not `value`): the same step back to back for ~--sustain-s seconds with
+    # NVML sampling throughout, so clocks / power are observed under a long load and the
+    # sustained rate can be set beside MEASURED_PEAKS' bf16_tflops_sustained
+    sustained = None
+    if args.sustain_s > 0:
+        reps = max(1, int(args.sustain_s * 1e3 / ms))
+        long_sampler = ClockSampler(local)
+        barrier()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with long_sampler:
+            s0.record(stream)
+            for _ in range(reps):
+                step()
+            s1.record(stream)
+            torch.cuda.synchronize(dev)
+        barrier()
+        sms = torch.tensor([s0.elapsed_time(s1) / reps], device=dev)
+        if world > 1:
+            dist.all_reduce(sms, op=dist.ReduceOp.MAX)
+        sms = float(sms.item())
+        sus_tf = flops_rank * world / (sms * 1e-3) / 1e12
+        sustained = {"steps": reps, "seconds": sms * reps * 1e-3, "ms_per_step": sms,
+                     "value": sus_tf, "unit": UNIT,
+                     "per_gpu_vs_bf16_sustained_peak": (sus_tf / world) / sustained_peak
+                     if sustained_peak else None,
+                     "clocks": long_sampler.summary()}
 
     # e2e through the C ABI with host (pinned) buffers: H2D of A, B, C and D2H of C each step
     e2e = run_e2e(args, tk, api, torch, dev, m, n, k, world)
@@ -308,7 +348,10 @@ def run_ours(args):
                            "l2": "inputs (A+B+C+D) exceed the 126 MB L2; no flush",
                            "lane": tk.last_run()["lane"]},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "clocks": {**sampler.summary(), "sm_mhz_in_kernel": kernel_mhz},
+                # sm_mhz_in_kernel (clock64 / globaltimer inside the GEMM) is the clock the
+                # kernel ran at; NVML's sm_mhz over a short timed region can miss the load
+                "clocks": {"sm_mhz_in_kernel": kernel_mhz, **sampler.summary()},
+                "sustained": sustained,
                 "library_baseline": library,
                 "allgather_d": allgather,
                 "gpu_launches": launches_per_step * args.steps}
@@ -393,17 +436,64 @@ def run_e2e(args, tk, api, torch, dev, m, n, k, world):
             "path": "tk_gemm_ex_raw(TAG_F16F32) on pinned host buffers (C updated in place)"}
 
 
+def run_dry(args):
+    """--dry-run: the launcher and rank plumbing without GPU work (gloo process group; the
+    CPU test of `--gpus N`).  Prints the line rank 0 would print, minus the measurements."""
+    import torch
+    import torch.distributed as dist
+
+    world, rank, _ = _dist()
+    if world > 1:
+        dist.init_process_group("gloo")
+        t = torch.tensor([float(rank)])
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        seen = int(t.item()) + 1
+        dist.destroy_process_group()
+    else:
+        seen = 1
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world,
+                          "ranks_seen": seen, "dry_run": True,
+                          "scaling": "strong" if args.strong else "weak",
+                          "config": {"n": args.n, "n_per_gpu": args.n // world if args.strong else args.n}}),
+              flush=True)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _self_launch(args):
+    """`--gpus N` outside torchrun: re-run this script as N ranks (one process per GPU)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--n", type=int, default=8192)
+    ap.add_argument("--n", type=int, default=None,
+                    help="problem size (default 8192 on 1 GPU, 16384 strong-sharded on N > 1)")
     ap.add_argument("--dtype", choices=["fp16", "bf16"], default="fp16")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--sustain-s", type=float, default=3.0,
+                    help="seconds of back-to-back steps for the sustained clocks/TFLOPS figure")
     ap.add_argument("--strong", action="store_true",
-                    help="strong scaling: the N x N x N problem split into G column slabs")
+                    help="strong scaling: the N x N x N problem split into G column slabs "
+                         "(the default when N > 1 GPUs)")
+    ap.add_argument("--weak", action="store_true",
+                    help="weak scaling: every rank owns an n-column slab (n = --n, default 8192)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher / rank plumbing only: gloo process group, no GPU work")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-library", action="store_true", help="skip the cuBLAS same-op context line")
     ap.add_argument("--fused-allgather", action="store_true",
@@ -413,7 +503,22 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    if args.impl == "reference":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_self_launch(args))
+    world = _dist()[0]
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but {world} rank(s) launched (WORLD_SIZE)")
+    if args.strong and args.weak:
+        raise SystemExit("--strong and --weak are exclusive")
+    args.strong = args.strong or (world > 1 and not args.weak)
+    if args.n is None:
+        args.n = 16384 if args.strong and world > 1 else 8192
+    if world > 1:  # let the driver see NCCL's own report of the ranks / transports
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    if args.dry_run:
+        run_dry(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

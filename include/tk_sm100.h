@@ -157,6 +157,45 @@ int tk_last_launch_count(void);
 /* Message of the last failure in this thread ("" if none). */
 const char* tk_last_error(void);
 
+/* ---- introspection and tuning (no reference counterpart) --------------------------------- */
+
+/* What the last tk_gemm / tk_gemm_ex_raw call on this thread launched: the main kernel's
+ * on-chip plan (the reference's allocation audit, kernel.py:74-95, logs its per-worker scratch;
+ * here the per-CTA shared-memory stages, C ring and TMEM accumulator columns are the analogue).
+ * Sizes in bytes unless noted. */
+typedef struct TkPlanInfo {
+  char kernel[32];          /* "pair", "pair_ops", "single", "stream", "quad", "diag_stream", "simt" */
+  int32_t lane;             /* TkLane of the launch, -1 before any */
+  int32_t op;               /* TkOperator */
+  int32_t tile_m, tile_n;   /* output tile per cluster (or CTA) */
+  int32_t tile_k;           /* K per pipeline stage */
+  int32_t mma_n, nsub;      /* instruction N, MMAs sharing one A stage */
+  int32_t mmas_per_k16;     /* tcgen05.mma per K=16 step (real 1, complex 4, dual 3, split-precision 3) */
+  int32_t cluster;          /* CTAs per cluster */
+  int32_t stages, stage_bytes;
+  int32_t cring_bytes;      /* streamed-C ring (per CTA) */
+  int32_t smem_bytes;       /* dynamic shared memory per CTA */
+  int32_t tmem_cols;        /* TMEM columns allocated per CTA (x 128 lanes x 4 bytes) */
+  int32_t grid_ctas;
+  int32_t tiles, units;     /* output tiles; schedule units (tiles + split-K parts) */
+  int32_t sk_parts, sk_tiles, sk_tma;
+  int32_t serpentine, group_m, pdl, c_stream, d_tma;
+  int32_t launches;         /* device kernels of the call (prep passes included) */
+  int32_t reserved;
+  int64_t workspace_bytes;
+} TkPlanInfo;
+
+/* Copy the plan of the last call on this thread into *out. */
+int tk_last_plan_info(TkPlanInfo* out);
+
+/* Tuning knobs (the TK_* names of DESIGN.md), read from the environment once when the library
+ * is first used.  tk_tune_set overrides one (value NULL or "" restores its default); it returns
+ * TK_ERR_CONFIG for an unknown name or malformed value.  tk_tune_reset re-reads the environment.
+ * tk_tune_get returns the current value or INT32_MIN when unset. */
+int tk_tune_set(const char* name, const char* value);
+int tk_tune_reset(void);
+int tk_tune_get(const char* name);
+
 /* ---- diagnostics (no reference counterpart; used by bench.py and tools/) ---------------- */
 
 /* Effective SM clock (MHz) of CTA 0 over the last CTA-pair GEMM launch: clock64 ticks over

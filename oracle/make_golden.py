@@ -96,6 +96,24 @@ def dense_cases():
          d=d.reshape((m, n), order="F"))
 
 
+def c1_cases():
+    """BASELINE configs[0] (C1): fp16-valued 256^3 column-major at the reference's DEFAULT
+    tiling (build_dense_config resolves block (256, 256, 8), op (8, 8, 8)), f32 k-ascending."""
+    rng = np.random.default_rng(256)
+    m = n = k = 256
+    a = rng.standard_normal((m, k)).astype(np.float16).astype(np.float32)
+    b = rng.standard_normal((k, n)).astype(np.float16).astype(np.float32)
+    c = rng.standard_normal((m, n)).astype(np.float32)
+    cfg = tk.build_dense_config(m, n, k, np.float32)
+    d = np.zeros(m * n, np.float32)
+    cnt = tk.matmul(cfg, a.ravel(order="F"), b.ravel(order="F"), c.ravel(order="F"), d)
+    res = tk.kernel.resolve_config(cfg)
+    save("c1_dense_256", {"m": m, "n": n, "k": k, "counters": counters_dict(cnt),
+                          "block_tile": list(res.params.block_tile),
+                          "operator_shape": list(res.params.operator_shape)},
+         a=a, b=b, c=c, d=d.reshape((m, n), order="F"))
+
+
 def fused_cases():
     rng = np.random.default_rng(12)
     m, n, k = 128, 96, 64
@@ -275,7 +293,7 @@ def host_logic_cases():
 
 if __name__ == "__main__":
     print("reference lane:", tk.active_lane())
-    which = sys.argv[1:] or ["dense", "fused", "pair", "variant", "gett", "host_logic"]
+    which = sys.argv[1:] or ["dense", "c1", "fused", "pair", "variant", "gett", "host_logic"]
     for name in which:
         globals()[f"{name}_cases"]()
     print("wrote", sorted(os.listdir(OUT)))

@@ -54,6 +54,14 @@ class TkGemmPlan(ctypes.Structure):
     ]
 
 
+class TkPlanInfo(ctypes.Structure):
+    _fields_ = [("kernel", ctypes.c_char * 32)] + [(f, c_int32) for f in (
+        "lane", "op", "tile_m", "tile_n", "tile_k", "mma_n", "nsub", "mmas_per_k16", "cluster",
+        "stages", "stage_bytes", "cring_bytes", "smem_bytes", "tmem_cols", "grid_ctas", "tiles",
+        "units", "sk_parts", "sk_tiles", "sk_tma", "serpentine", "group_m", "pdl", "c_stream",
+        "d_tma", "launches", "reserved")] + [("workspace_bytes", c_int64)]
+
+
 GEMM_EX_ARGTYPES = [c_int, c_int, c_int, c_longlong, c_longlong, c_longlong, c_double,
                     c_double, c_void_p, c_void_p, c_double, c_double, c_void_p]
 
@@ -61,7 +69,8 @@ GEMM_EX_ARGTYPES = [c_int, c_int, c_int, c_longlong, c_longlong, c_longlong, c_d
 EXPORTED = ("tk_abi_version", "tk_plan_lane", "tk_workspace_bytes", "tk_gemm", "tk_gemm_ex_raw",
             "tk_gemm_ex_raw_async", "tk_last_launch_count", "tk_last_error", "tk_debug_pair_mhz",
             "tk_debug_pair_ts", "tk_debug_clock_probe", "tk_debug_clock_probe_mhz",
-            "tk_gemm_peers", "tk_last_peer_mode", "tk_ipc_handle", "tk_ipc_open", "tk_ipc_close")
+            "tk_gemm_peers", "tk_last_peer_mode", "tk_ipc_handle", "tk_ipc_open", "tk_ipc_close",
+            "tk_last_plan_info", "tk_tune_set", "tk_tune_reset", "tk_tune_get")
 
 _lib = None
 _load_error = None
@@ -104,6 +113,13 @@ def load():
     lib.tk_gemm_ex_raw_async.restype = c_int
     lib.tk_last_launch_count.restype = c_int
     lib.tk_last_error.restype = ctypes.c_char_p
+    lib.tk_last_plan_info.argtypes = [ctypes.POINTER(TkPlanInfo)]
+    lib.tk_last_plan_info.restype = c_int
+    lib.tk_tune_set.argtypes = [ctypes.c_char_p, ctypes.c_char_p]
+    lib.tk_tune_set.restype = c_int
+    lib.tk_tune_reset.restype = c_int
+    lib.tk_tune_get.argtypes = [ctypes.c_char_p]
+    lib.tk_tune_get.restype = c_int
     if lib.tk_abi_version() != ABI_VERSION:
         _load_error = f"libtk_sm100.so ABI {lib.tk_abi_version()} != expected {ABI_VERSION}"
         raise RuntimeError(_load_error)
@@ -113,3 +129,35 @@ def load():
 
 def last_error() -> str:
     return load().tk_last_error().decode(errors="replace")
+
+
+def plan_info() -> dict:
+    """The on-chip plan of the last GEMM on this thread (tk_last_plan_info) as a dict."""
+    info = TkPlanInfo()
+    load().tk_last_plan_info(ctypes.byref(info))
+    out = {f: getattr(info, f) for f, _ in TkPlanInfo._fields_ if f != "reserved"}
+    out["kernel"] = info.kernel.decode()
+    return out
+
+
+KNOB_UNSET = -(2 ** 31)
+
+
+def tune(name: str, value=None) -> None:
+    """Override one tuning knob (TK_* name); None restores its default.
+
+    Knobs are read from the environment once, when the library loads; this is the only way to
+    change one afterwards (the launch path never reads the environment)."""
+    rc = load().tk_tune_set(name.encode(), None if value is None else str(value).encode())
+    if rc != TK_OK:
+        raise ValueError(last_error())
+
+
+def tune_reset() -> None:
+    """Drop every override: knobs return to the values the environment gives."""
+    load().tk_tune_reset()
+
+
+def tune_get(name: str):
+    v = load().tk_tune_get(name.encode())
+    return None if v == KNOB_UNSET else v

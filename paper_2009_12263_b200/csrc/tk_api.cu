@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <atomic>
+#include <climits>
 #include <cmath>
 #include <complex>
 #include <cstdarg>
@@ -49,6 +51,88 @@ int fail(int code, const char* fmt, ...) {
     if (e_ != cudaSuccess)                                                            \
       return fail(TK_ERR_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_));       \
   } while (0)
+
+// ------------------------------------------------------------------ tuning knobs
+// Every dispatch choice with a tunable default reads this table.  It is filled once from the
+// TK_* environment when the library is first used and changes only through tk_tune_set /
+// tk_tune_reset (tests, tools/): no launch path calls getenv.  Knobs that change results
+// (skipping loads, MMAs, C or the epilogue) exist only in diagnostic builds (-DTK_DIAG).
+enum Knob {
+  K_TC_KERNEL, K_PAIR_BNI, K_PAIR_NSUB, K_SERPENTINE, K_GROUP_M, K_SPLITK, K_SPLITK_MINKB,
+  K_SPLITK_S, K_SK_TMA, K_PDL, K_MN3D, K_PAIR_CSTREAM, K_PAIR_DTMA, K_C_PF, K_C_PF_SPREAD,
+  K_NSUB2_CSL, K_STAGGER, K_PAIR_GRID, K_PAIR_DEEPC, K_PAIROPS_BN, K_DIAG_STREAM, K_D_TMA,
+  K_L2_PROMO, K_POLICY_AB, K_POL_A, K_POL_B, K_PAIR_CLUSTERS, K_EX_SLABS, K_VERBOSE,
+  K_DBG_C_ZERO, K_DBG_SKIP_EPI, K_DBG_NO_LOAD, K_DBG_NO_MMA, K_DBG_CTA, K_COUNT
+};
+constexpr int K_FIRST_DIAG = K_DBG_C_ZERO;
+const char* const kKnobNames[K_COUNT] = {
+  "TK_TC_KERNEL", "TK_PAIR_BNI", "TK_PAIR_NSUB", "TK_SERPENTINE", "TK_GROUP_M", "TK_SPLITK",
+  "TK_SPLITK_MINKB", "TK_SPLITK_S", "TK_SK_TMA", "TK_PDL", "TK_MN3D", "TK_PAIR_CSTREAM",
+  "TK_PAIR_DTMA", "TK_C_PF", "TK_C_PF_SPREAD", "TK_NSUB2_CSL", "TK_STAGGER", "TK_PAIR_GRID",
+  "TK_PAIR_DEEPC", "TK_PAIROPS_BN", "TK_DIAG_STREAM", "TK_D_TMA", "TK_L2_PROMO", "TK_POLICY_AB",
+  "TK_POL_A", "TK_POL_B", "TK_PAIR_CLUSTERS", "TK_EX_SLABS", "TK_VERBOSE",
+  "TK_DBG_C_ZERO", "TK_DBG_SKIP_EPI", "TK_DBG_NO_LOAD", "TK_DBG_NO_MMA", "TK_DBG_CTA"};
+#ifdef TK_DIAG
+constexpr int K_ENABLED = K_COUNT;
+#else
+constexpr int K_ENABLED = K_FIRST_DIAG;
+#endif
+constexpr int KNOB_UNSET = INT32_MIN;
+
+struct KnobTable {
+  std::atomic<int> v[K_COUNT];
+};
+
+// TK_TC_KERNEL takes a kernel name; every other knob an integer
+int parse_knob(int id, const char* s, int* out) {
+  if (!s || !*s) { *out = KNOB_UNSET; return TK_OK; }
+  if (id == K_TC_KERNEL) {
+    static const char* names[] = {"auto", "single", "pair", "stream", "quad", "diagstream"};
+    for (int i = 0; i < 6; ++i)
+      if (!strcmp(s, names[i])) { *out = i; return TK_OK; }
+    return fail(TK_ERR_CONFIG, "TK_TC_KERNEL: unknown kernel '%s'", s);
+  }
+  char* end = nullptr;
+  const long v = strtol(s, &end, 10);
+  if (end == s || *end) return fail(TK_ERR_CONFIG, "%s: integer expected, got '%s'", kKnobNames[id], s);
+  *out = int(v);
+  return TK_OK;
+}
+
+void knobs_from_env(KnobTable& t) {
+  for (int i = 0; i < K_COUNT; ++i) {
+    int v = KNOB_UNSET;
+    if (i < K_ENABLED && parse_knob(i, getenv(kKnobNames[i]), &v) != TK_OK) v = KNOB_UNSET;
+    t.v[i].store(v, std::memory_order_relaxed);
+  }
+  g_err.clear();
+}
+
+KnobTable& knob_table() {
+  static KnobTable t;
+  static std::once_flag once;
+  std::call_once(once, [] { knobs_from_env(t); });
+  return t;
+}
+
+// value of a knob, or `def` when it is not set
+inline int knob(Knob id, int def) {
+  const int v = knob_table().v[id].load(std::memory_order_relaxed);
+  return v == KNOB_UNSET ? def : v;
+}
+inline bool knob_set(Knob id) { return knob_table().v[id].load(std::memory_order_relaxed) != KNOB_UNSET; }
+
+// what the last launch ran (tk_last_plan_info)
+thread_local TkPlanInfo g_info;
+
+void info_reset() {
+  memset(&g_info, 0, sizeof(g_info));
+  g_info.lane = -1;
+}
+void info_kernel(const char* name) {
+  snprintf(g_info.kernel, sizeof(g_info.kernel), "%s", name);
+  g_info.tile_k = strcmp(name, "simt") && strcmp(name, "diag_stream") ? 64 : 0;  // tk::TC_BK
+}
 
 // ------------------------------------------------------------------ plan checks
 int64_t scalar_bytes(int s) { return s == TK_F16 || s == TK_BF16 ? 2 : s == TK_F32 ? 4 : 8; }
@@ -333,8 +417,7 @@ Workspace plan_workspace(const TkGemmPlan* p0, int lane) {
 // ------------------------------------------------------------------ TMA
 // TK_L2_PROMO=0|64|128|256 (tuning knob; default 256B L2 sector promotion for TMA loads)
 CUtensorMapL2promotion l2_promo() {
-  const char* e = getenv("TK_L2_PROMO");
-  const int v = e ? atoi(e) : 256;
+  const int v = knob(K_L2_PROMO, 256);
   return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
        : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
        : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
@@ -417,13 +500,23 @@ tk::EpiProg to_prog(const TkTransform& t) {
   return g;
 }
 
+// Per-device caches (SM count, raised shared-memory limits, co-resident cluster counts) are
+// indexed by the current device: a process may drive several GPUs.
+constexpr int TK_MAX_DEV = 64;
+int cur_dev() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev >= 0 && dev < TK_MAX_DEV ? dev : 0;
+}
+
 int sm_count() {
-  static int n = 0;
+  static int cache[TK_MAX_DEV] = {};
+  const int dev = cur_dev();
+  int n = cache[dev];
   if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     if (n <= 0) n = 148;
+    cache[dev] = n;
   }
   return n;
 }
@@ -431,15 +524,34 @@ int sm_count() {
 template <int OP, bool DENSE, int CSTREAM = 0>
 int launch_tc_variant(const tk::TcParams& prm, cudaStream_t s) {
   using S = tk::TcSmem<OP, CSTREAM>;
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[TK_MAX_DEV] = {};
+  const int dev = cur_dev();
+  if (!attr[dev]) {
     TK_CUDA(cudaFuncSetAttribute(tk::tc_gemm_kernel<OP, DENSE, CSTREAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL));
-    attr = true;
+    attr[dev] = true;
   }
   const int grid = std::min(prm.num_tiles, sm_count());
   tk::tc_gemm_kernel<OP, DENSE, CSTREAM><<<grid, tk::TC_THREADS, S::TOTAL, s>>>(prm);
   TK_CUDA(cudaGetLastError());
   ++g_launches;
+  info_kernel(CSTREAM ? "stream" : "single");
+  g_info.tile_m = tk::TC_BM;
+  g_info.tile_n = tk::TcCfg<OP>::BN;
+  g_info.mma_n = tk::TcCfg<OP>::BN;
+  g_info.nsub = 1;
+  g_info.mmas_per_k16 = OP == tk::OP_REAL ? 1 : OP == tk::OP_COMPLEX ? 4 : 3;
+  g_info.cluster = 1;
+  g_info.stages = S::STAGES;
+  g_info.stage_bytes = S::STAGE_BYTES;
+  g_info.cring_bytes = S::CRING_BYTES;
+  g_info.smem_bytes = S::TOTAL;
+  g_info.tmem_cols = tk::TcCfg<OP>::TMEM_COLS;
+  g_info.grid_ctas = grid;
+  g_info.tiles = g_info.units = prm.num_tiles;
+  g_info.sk_parts = 1;
+  g_info.group_m = prm.group_m;
+  g_info.c_stream = CSTREAM ? 1 : 0;
+  g_info.d_tma = prm.d_tma;
   return TK_OK;
 }
 
@@ -447,12 +559,14 @@ template <bool DENSE, bool CSTREAM = false, int NSUB = 1, int BNI = 256, int CSL
 int launch_tc_pair(const tk::TcParams& prm, cudaStream_t s) {
   constexpr int SMEM = tk::Tc2Plan<NSUB, CSTREAM, BNI, CSL>::SMEM;
   auto kern = tk::tc_gemm_pair_kernel<DENSE, CSTREAM, NSUB, BNI, CSL>;
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[TK_MAX_DEV] = {};
+  static int max_clusters_dev[TK_MAX_DEV] = {};
+  const int dev = cur_dev();
+  if (!attr[dev]) {
     TK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-    attr = true;
+    attr[dev] = true;
   }
-  static int max_clusters = 0;
+  int& max_clusters = max_clusters_dev[dev];
   if (!max_clusters) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * (sm_count() / 2));
@@ -469,7 +583,7 @@ int launch_tc_pair(const tk::TcParams& prm, cudaStream_t s) {
       cudaGetLastError();
       max_clusters = sm_count() / 2;
     }
-    if (getenv("TK_VERBOSE")) fprintf(stderr, "tk: pair kernel max active clusters %d\n", max_clusters);
+    if (knob(K_VERBOSE, 0)) fprintf(stderr, "tk: pair kernel max active clusters %d\n", max_clusters);
   }
   tk::TcParams run = prm;
   if (run.sk_parts > 1 && max_clusters != pair_clusters()) {  // split parts must all be co-resident
@@ -477,21 +591,27 @@ int launch_tc_pair(const tk::TcParams& prm, cudaStream_t s) {
     run.sk_parts = 1;
     run.sk_tma = 0;
   }
-  const char* eg = getenv("TK_PAIR_GRID");
+  const bool eg = knob_set(K_PAIR_GRID);
   if (run.nar_units > 0 && (max_clusters != pair_clusters() || eg)) {  // staggered lists assume P
     run.num_units = run.num_tiles;
     run.nar_units = 0;
   }
   int clusters = std::min(run.num_units, max_clusters);
-  if (eg) clusters = std::max(1, std::min(clusters, atoi(eg)));
+  if (eg) clusters = std::max(1, std::min(clusters, knob(K_PAIR_GRID, clusters)));
+  // every split unit must be the LAST unit of its cluster (units c, c+P, ...: sk_first a
+  // multiple of the cluster count, at most one split unit per cluster) -- the epilogue's C-ring
+  // bookkeeping (smask in tc_gemm_pair_kernel) relies on it; any other schedule runs unsplit
+  if (run.sk_parts > 1 && (run.sk_first % clusters != 0 || run.num_units - run.sk_first > clusters)) {
+    run.num_units = run.sk_first = run.num_tiles;
+    run.sk_parts = 1;
+    run.sk_tma = 0;
+    clusters = std::min(run.num_units, clusters);
+  }
   const int grid = 2 * clusters;
   // programmatic dependent launch: the next GEMM in the stream may be scheduled while this one
   // drains; its CTAs run their prologue (barriers, TMEM, tensor-map prefetch) and then wait in
   // griddepcontrol.wait until this grid has completed and its writes are visible
-  static const bool pdl = [] {
-    const char* e = getenv("TK_PDL");
-    return !e || atoi(e);
-  }();
+  const bool pdl = knob(K_PDL, 1) != 0;
   // not after the split-K flag memset: a programmatic launch may start before a preceding
   // memset node completes, and the flags must be zero before any part counts in
   run.pdl = (pdl && run.sk_parts == 1) ? 1 : 0;
@@ -507,6 +627,30 @@ int launch_tc_pair(const tk::TcParams& prm, cudaStream_t s) {
   cfg.numAttrs = run.pdl ? 1 : 0;
   TK_CUDA(cudaLaunchKernelEx(&cfg, kern, run));
   ++g_launches;
+  using PL = tk::Tc2Plan<NSUB, CSTREAM, BNI, CSL>;
+  info_kernel("pair");
+  g_info.tile_m = 256;
+  g_info.tile_n = PL::BNP;
+  g_info.mma_n = BNI;
+  g_info.nsub = NSUB;
+  g_info.mmas_per_k16 = NSUB;
+  g_info.cluster = 2;
+  g_info.stages = PL::STAGES;
+  g_info.stage_bytes = PL::STAGE_BYTES;
+  g_info.cring_bytes = PL::CRING_BYTES;
+  g_info.smem_bytes = SMEM;
+  g_info.tmem_cols = PL::TMEM_COLS;
+  g_info.grid_ctas = grid;
+  g_info.tiles = run.num_tiles;
+  g_info.units = run.num_units;
+  g_info.sk_parts = run.sk_parts;
+  g_info.sk_tiles = run.sk_parts > 1 ? (run.num_units - run.sk_first) / run.sk_parts : 0;
+  g_info.sk_tma = run.sk_tma;
+  g_info.serpentine = run.serp;
+  g_info.group_m = run.group_m;
+  g_info.pdl = run.pdl;
+  g_info.c_stream = CSTREAM ? 1 : 0;
+  g_info.d_tma = run.d_tma;
   return TK_OK;
 }
 
@@ -516,8 +660,7 @@ int launch_tc_pair_bni(const tk::TcParams& prm, int bni, cudaStream_t s) {
   if (bni == 64) return launch_tc_pair<DENSE, CSTREAM, 1, 64>(prm, s);
   if (bni == 128) return launch_tc_pair<DENSE, CSTREAM, 1, 128>(prm, s);
   // single wave, 256-wide tiles: a 4-slot C ring holds each warp's whole C block
-  const char* e = getenv("TK_PAIR_DEEPC");
-  if (CSTREAM && prm.num_units <= pair_clusters() && (!e || atoi(e)))
+  if (CSTREAM && prm.num_units <= pair_clusters() && knob(K_PAIR_DEEPC, 1))
     return launch_tc_pair<DENSE, CSTREAM, 1, 256, 4>(prm, s);
   return launch_tc_pair<DENSE, CSTREAM, 1, 256>(prm, s);
 }
@@ -532,16 +675,14 @@ struct SplitPlan {
 SplitPlan split_plan(int64_t tiles, int clusters, int kb_total, int bnp) {
   SplitPlan sp;
   sp.first = int(tiles);
-  if (const char* e = getenv("TK_SPLITK"))
-    if (!atoi(e)) return sp;
+  if (!knob(K_SPLITK, 1)) return sp;
   const int64_t r = tiles % clusters;
   if (r == 0 || r > clusters / 2) return sp;
   // >= 64 block-K steps per part: below that the partial hand-off costs what the wave gains
   // (measured: 4096^3 -2 %, 4096x4096x16384 +6.5 %, 1536x4096x16384 +13 %)
-  int min_kb = 64;
-  if (const char* e = getenv("TK_SPLITK_MINKB")) min_kb = std::max(1, atoi(e));
+  const int min_kb = std::max(1, knob(K_SPLITK_MINKB, 64));
   int parts = int(std::min<int64_t>(std::min<int64_t>(4, clusters / r), kb_total / min_kb));
-  if (const char* e = getenv("TK_SPLITK_S")) parts = std::max(1, std::min(parts, atoi(e)));
+  if (knob_set(K_SPLITK_S)) parts = std::max(1, std::min(parts, knob(K_SPLITK_S, parts)));
   if (parts < 2) return sp;
   sp.first = int(tiles - r);
   sp.parts = parts;
@@ -563,8 +704,8 @@ int64_t split_ws_bytes(int64_t m, int64_t n, int64_t k, const TkLayout& b) {
 // waves x per-tile time (per k-block, per SM: MMA 2*BNI clocks vs operand ingest of
 // (16 KB + 64*BNI B) at ~60 B/clock); 64 needs K-major B (64-column MN-major atoms).
 int choose_pair_bni(int64_t m, int64_t n, bool b_mn_major, int clusters) {
-  if (const char* e = getenv("TK_PAIR_BNI")) {
-    const int v = atoi(e);
+  if (knob_set(K_PAIR_BNI)) {
+    const int v = knob(K_PAIR_BNI, 256);
     if (v == 64 || v == 128 || v == 256) return (v == 64 && b_mn_major) ? 128 : v;
   }
   int best = 256;
@@ -581,23 +722,21 @@ int choose_pair_bni(int64_t m, int64_t n, bool b_mn_major, int clusters) {
 }
 
 int pair_clusters() {
-  static int c = 0;
-  if (!c) {
-    c = sm_count() / 2;
-    if (const char* e = getenv("TK_PAIR_CLUSTERS")) c = std::max(1, atoi(e));
-  }
-  return c;
+  const int c = sm_count() / 2;
+  return knob_set(K_PAIR_CLUSTERS) ? std::max(1, knob(K_PAIR_CLUSTERS, c)) : c;
 }
 
 template <bool DENSE>
 int launch_tc_quad(const tk::TcParams& prm, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[TK_MAX_DEV] = {};
+  static int max_clusters_dev[TK_MAX_DEV] = {};
+  const int dev = cur_dev();
+  if (!attr[dev]) {
     TK_CUDA(cudaFuncSetAttribute(tk::tc_gemm_quad_kernel<DENSE>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, tk::TC2_SMEM));
-    attr = true;
+    attr[dev] = true;
   }
-  static int max_clusters = 0;
+  int& max_clusters = max_clusters_dev[dev];
   if (!max_clusters) {  // 4-CTA clusters do not tile every GPC: ask how many are co-resident
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(4 * (sm_count() / 4));
@@ -615,25 +754,33 @@ int launch_tc_quad(const tk::TcParams& prm, cudaStream_t s) {
       cudaGetLastError();
       max_clusters = sm_count() / 4;
     }
-    if (getenv("TK_VERBOSE")) fprintf(stderr, "tk: quad kernel max active clusters %d\n", max_clusters);
+    if (knob(K_VERBOSE, 0)) fprintf(stderr, "tk: quad kernel max active clusters %d\n", max_clusters);
   }
   const int grid = 4 * std::min(prm.num_tiles, max_clusters);
   tk::tc_gemm_quad_kernel<DENSE><<<grid, tk::TC_THREADS, tk::TC2_SMEM, s>>>(prm);
   TK_CUDA(cudaGetLastError());
   ++g_launches;
+  info_kernel("quad");
+  g_info.tile_m = 512;
+  g_info.tile_n = tk::TC2_BN;
+  g_info.mma_n = tk::TC2_BN;
+  g_info.nsub = 1;
+  g_info.mmas_per_k16 = 1;
+  g_info.cluster = 4;
+  g_info.stages = tk::TC2_STAGES;
+  g_info.stage_bytes = tk::TC2_STAGE_BYTES;
+  g_info.smem_bytes = tk::TC2_SMEM;
+  g_info.tmem_cols = 512;
+  g_info.grid_ctas = grid;
+  g_info.tiles = g_info.units = prm.num_tiles;
+  g_info.sk_parts = 1;
+  g_info.group_m = prm.group_m;
   return TK_OK;
 }
 
 // TK_TC_KERNEL=quad|pair|single forces the CTA-pair / single-CTA tcgen05 kernel (tests, tuning)
 int tc_kernel_override() {
-  const char* e = getenv("TK_TC_KERNEL");
-  if (!e) return 0;
-  if (!strcmp(e, "pair")) return 2;
-  if (!strcmp(e, "quad")) return 4;
-  if (!strcmp(e, "stream")) return 3;
-  if (!strcmp(e, "single")) return 1;
-  if (!strcmp(e, "diagstream")) return 5;
-  return 0;
+  return knob(K_TC_KERNEL, 0);  // parse_knob: auto 0, single 1, pair 2, stream 3, quad 4, diagstream 5
 }
 
 template <int OP>
@@ -898,7 +1045,7 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
   }
   // ---- epilogue
   prm.c_zero = p->c.kind == TK_LAYOUT_ZERO;
-  if (const char* g = getenv("TK_DBG_C_ZERO")) prm.c_zero |= atoi(g);  // diagnostic: skip C
+  prm.c_zero |= knob(K_DBG_C_ZERO, 0) ? 1 : 0;  // diagnostic builds only: skip C
   prm.c_pair = p->c.pair;
   prm.d_pair = p->d.pair;
   prm.c_ptr = c;
@@ -923,20 +1070,19 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
   // grouped raster: 16 M-blocks per group keeps the group's A panel L2-resident while B
   // streams (8192^3: DRAM reads 1.18 -> 1.12 GB, +2 %; 4 / 32 are worse)
   prm.group_m = 16;
-  if (const char* g = getenv("TK_GROUP_M")) prm.group_m = std::max(1, atoi(g));
-  if (const char* g = getenv("TK_DBG_SKIP_EPI")) prm.dbg_skip_epi = atoi(g);
-  if (const char* g = getenv("TK_DBG_NO_LOAD")) prm.dbg_skip_epi |= atoi(g) ? 2 : 0;
+  prm.group_m = std::max(1, knob(K_GROUP_M, prm.group_m));
+  // result-changing diagnostics (TK_DIAG builds only; the table never holds them otherwise)
+  prm.dbg_skip_epi = knob(K_DBG_SKIP_EPI, 0) | (knob(K_DBG_NO_LOAD, 0) ? 2 : 0) | (knob(K_DBG_NO_MMA, 0) ? 4 : 0);
   prm.dbg_cta = -1;  // timestamp probes off unless a CTA is selected (tools/ts_probe.py)
-  if (const char* g = getenv("TK_DBG_CTA")) prm.dbg_cta = atoi(g);
+  prm.dbg_cta = knob(K_DBG_CTA, -1);
   // serpentine K order on the pair kernel: DRAM reads 1.43 -> 1.29 GB at 8192^3, ~+1 %
   prm.serp = 1;
-  if (const char* g = getenv("TK_SERPENTINE")) prm.serp = atoi(g);
-  if (const char* g = getenv("TK_DBG_NO_MMA")) prm.dbg_skip_epi |= atoi(g) ? 4 : 0;
+  prm.serp = knob(K_SERPENTINE, prm.serp);
   prm.pol_ab = 1;  // A/B panels are re-read by neighbouring tiles: keep them in L2
-  if (const char* g = getenv("TK_POLICY_AB")) prm.pol_ab = atoi(g);
+  prm.pol_ab = knob(K_POLICY_AB, prm.pol_ab);
   prm.pol_a = prm.pol_b = prm.pol_ab ? 1 : 0;
-  if (const char* g = getenv("TK_POL_A")) prm.pol_a = atoi(g);
-  if (const char* g = getenv("TK_POL_B")) prm.pol_b = atoi(g);
+  prm.pol_a = knob(K_POL_A, prm.pol_a);
+  prm.pol_b = knob(K_POL_B, prm.pol_b);
   const bool pair = op != TK_OP_REAL;
   // real operator: C/D rows may follow any digit map (GETT outputs whose M indices are not
   // one contiguous run) as long as columns are one strided digit -- the register epilogue
@@ -968,8 +1114,7 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
   // diagonal A: an HBM stream, run as one (vectorised) elementwise pass, not on the tensor cores
   if (op == TK_OP_REAL && prm.diag_a && dense && !rmapped && !prm.affine && prm.b_mn == 0 &&
       (ov == 0 || ov == 5)) {
-    const char* e = getenv("TK_DIAG_STREAM");
-    if (!e || atoi(e)) {
+    if (knob(K_DIAG_STREAM, 1)) {
       int mnk;
       int64_t ldb;
       tma_operand(p->b, mnk, ldb);
@@ -986,6 +1131,8 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
         tk::diag_stream_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(ps, static_cast<const __nv_bfloat16*>(b), ldb);
       TK_CUDA(cudaGetLastError());
       ++g_launches;
+      info_kernel("diag_stream");
+      g_info.grid_ctas = int(grid.x * grid.y);
       return TK_OK;
     }
   }
@@ -997,7 +1144,7 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
       int rc;
       if (!prm.c_zero && (rc = make_map_2d(&ps.tcmap, c, TK_F32, p->m, p->n, prm.ldc, 32, 32))) return rc;
       ps.d_tma = (prm.ldd * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(d) & 15) == 0;
-      if (const char* e = getenv("TK_D_TMA")) ps.d_tma = ps.d_tma && atoi(e);
+      ps.d_tma = ps.d_tma && knob(K_D_TMA, 1);
       if (ps.d_tma && (rc = make_map_2d(&ps.tdmap, d, TK_F32, p->m, p->n, prm.ldd, 32, 32))) return rc;
       const bool hbm = prm.diag_a || prm.kb_total <= 4;
       return hbm ? launch_tc_variant<tk::OP_REAL, true, 1>(ps, s) : launch_tc_variant<tk::OP_REAL, true, 2>(ps, s);
@@ -1025,7 +1172,7 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
       // 8192^3 +1 %, 16384^3 +13 % (burst) / +22 % (sustained), 6144^3 -3 % (so not there)
       const int64_t tiles2 = ((p->m + 255) / 256) * ((p->n + 511) / 512);
       int nsub = (p->k >= 8192 && tiles2 >= 4 * int64_t(pair_clusters())) ? 2 : 1;
-      if (const char* e = getenv("TK_PAIR_NSUB")) nsub = atoi(e) == 2 ? 2 : 1;
+      if (knob_set(K_PAIR_NSUB)) nsub = knob(K_PAIR_NSUB, 1) == 2 ? 2 : 1;
       int mn;
       int64_t pitch;
       int rc;
@@ -1041,14 +1188,13 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
         // split one wide tile into a leading and a trailing half; balanced when T mod P >= S.
         // Opt-in: bitwise equal, but measured 3-6 % slower (8192^3, 16384^3, 8192x16384x8192)
         // -- under the power cap the overlapped drains raise average power and lower clocks.
-        const char* e = getenv("TK_STAGGER");
         const int P = pair_clusters(), S = P / 2;
-        if (e && atoi(e) && pp.num_tiles >= 2 * P) {
+        if (knob(K_STAGGER, 0) && pp.num_tiles >= 2 * P) {
           pp.nar_units = S;
           pp.num_units = pp.num_tiles + S;  // (>= P: the grid is all P clusters)
         }
       }
-      if (nsub == 1 && dense && w.splitk >= 0 && !getenv("TK_PAIR_GRID")) {
+      if (nsub == 1 && dense && w.splitk >= 0 && !knob_set(K_PAIR_GRID)) {
         const SplitPlan sp = split_plan(pp.num_tiles, pair_clusters(), pp.kb_total, bni);
         if (sp.parts > 1 && sp.ws_bytes <= split_ws_bytes(p->m, p->n, p->k, p->b)) {
           pp.sk_first = sp.first;
@@ -1062,8 +1208,7 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
       // per-CTA halves: A box 128 rows / B box bni/2 columns
       tma_operand(p->a, mn, pitch);
       pp.mn3d = 0;
-      const char* e3 = getenv("TK_MN3D");
-      const bool use3d = !e3 || atoi(e3);
+      const bool use3d = knob(K_MN3D, 1) != 0;
       // MN-major A (M % 64 == 0 so atoms never straddle the M edge): one 3-D box per stage
       if (mn && use3d && p->m % 64 == 0) {
         if ((rc = make_map_mn3d(&pp.ta[0], a_plane0, p->a.scalar, p->m, p->k, pitch, 2))) return rc;
@@ -1076,11 +1221,11 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
         if ((rc = make_map_mn3d(&pp.tb[0], b_plane0, p->b.scalar, p->n, p->k, pitch, bni / 128))) return rc;
         pp.mn3d |= 2;
       }
-      if (getenv("TK_VERBOSE")) fprintf(stderr, "tk: pair kernel bni %d nsub %d tiles %d\n", bni, nsub, pp.num_tiles);
+      if (knob(K_VERBOSE, 0)) fprintf(stderr, "tk: pair kernel bni %d nsub %d tiles %d\n", bni, nsub, pp.num_tiles);
       // streamed C/D epilogue (TMA ring + bulk stores) when C/D are TMA-compatible
       bool cs = dense && !rmapped && (prm.c_zero || ((prm.ldc * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(c) & 15) == 0)) &&
                 (prm.ldd * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(d) & 15) == 0;
-      if (const char* e = getenv("TK_PAIR_CSTREAM")) cs = cs && atoi(e);
+      cs = cs && knob(K_PAIR_CSTREAM, 1);
       if (cs) {
         if (!prm.c_zero && (rc = make_map_2d(&pp.tcmap, c, TK_F32, p->m, p->n, prm.ldc, 32, 32))) return rc;
         if ((rc = make_map_2d(&pp.tdmap, d, TK_F32, p->m, p->n, prm.ldd, 32, 32))) return rc;
@@ -1092,27 +1237,22 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
           pp.npeer = g_npeer;
           g_peer_mode = 1;
         }
-        if (const char* e = getenv("TK_PAIR_DTMA"))
-          if (!pp.npeer) pp.d_tma = atoi(e);
-        pp.c_pf_kb = 0;  // L2 prefetch of the next drain's C: measured neutral-to-negative
-        if (const char* e = getenv("TK_C_PF")) pp.c_pf_kb = atoi(e);
-        pp.c_pf_spread = 0;
-        if (const char* e = getenv("TK_C_PF_SPREAD")) pp.c_pf_spread = atoi(e);
+        if (!pp.npeer) pp.d_tma = knob(K_PAIR_DTMA, 1);
+        pp.c_pf_kb = knob(K_C_PF, 0);  // L2 prefetch of the next drain's C: measured neutral-to-negative
+        pp.c_pf_spread = knob(K_C_PF_SPREAD, 0);
         pp.c_pf_kb = std::min(pp.c_pf_kb, pp.kb_total);
         // split-K partials as TMA boxes through the C ring (written from the ring by the K-parts,
         // loaded into it by the last part's C loader) instead of per-thread stores and loads
         pp.sk_tma = 0;
         if (pp.sk_parts > 1 && !prm.c_zero && pp.d_tma) {
-          const char* e = getenv("TK_SK_TMA");
-          if (!e || atoi(e)) {
+          if (knob(K_SK_TMA, 1)) {
             const int64_t cols = int64_t(pp.num_units - pp.sk_first) / pp.sk_parts * (pp.sk_parts - 1) * 2 * bni;
             if ((rc = make_map_2d(&pp.tskmap, pp.sk_ws, TK_F32, 128, cols, 128, 32, 32))) return rc;
             pp.sk_tma = 1;
           }
         }
         if (nsub == 2) {
-          const char* e = getenv("TK_NSUB2_CSL");  // C-ring slots per warp (tuning)
-          const int csl = e ? atoi(e) : 2;
+          const int csl = knob(K_NSUB2_CSL, 2);  // C-ring slots per warp (tuning)
           if (csl == 3) return launch_tc_pair<true, true, 2, 256, 3>(pp, s);
           if (csl == 4) return launch_tc_pair<true, true, 2, 256, 4>(pp, s);
           return launch_tc_pair<true, true, 2>(pp, s);
@@ -1129,12 +1269,12 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
     if (ov == 2 || (ov == 0 && pair_tiles >= sm_count() / 2 && prm.kb_total > 4)) {
       tk::TcParams pp = prm;
       // two A planes per tile: 8 M-blocks per group keep the panel L2-resident (16: -4 %)
-      if (!getenv("TK_GROUP_M")) pp.group_m = 8;
+      pp.group_m = std::max(1, knob(K_GROUP_M, 8));
       // 256-wide pair tiles (N=256 MMAs: 96 instead of 128 B/clk of shared-memory operand
       // reads) when there are >= 4 waves of them to amortise the single accumulator's drain
       const int64_t tiles256 = ((p->m + 255) / 256) * ((p->n + 255) / 256);
       int bn = tiles256 >= 4 * int64_t(pair_clusters()) ? 256 : 128;
-      if (const char* e = getenv("TK_PAIROPS_BN")) bn = atoi(e) == 256 ? 256 : 128;
+      if (knob_set(K_PAIROPS_BN)) bn = knob(K_PAIROPS_BN, 128) == 256 ? 256 : 128;
       pp.num_mb = int((p->m + 255) / 256);
       pp.num_nb = int((p->n + bn - 1) / bn);
       pp.num_tiles = pp.num_mb * pp.num_nb;
@@ -1154,7 +1294,8 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
       if (mn)  // K-major B: this CTA's bn/2-column half per box
         for (int pl = 0; pl < 2; ++pl)
           if ((rc = make_map_2d(&pp.tb[pl], planes_b[pl], p->b.scalar, p->k, p->n, pitch, 64, bn / 2))) return rc;
-      static bool attr[2][2][2] = {};
+      static bool attr_dev[TK_MAX_DEV][2][2][2] = {};
+      auto& attr = attr_dev[cur_dev()];
       const int oi = op == TK_OP_COMPLEX ? 0 : 1;
       const int smem_bytes = bn == 256 ? tk::Tc2cPlan<256>::SMEM : tk::Tc2cPlan<128>::SMEM;
       auto launch = [&](auto kern) -> int {
@@ -1163,9 +1304,8 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
           attr[oi][dense][bn == 256] = true;
         }
         const int grid = 2 * std::min(pp.num_tiles, sm_count() / 2);
-        const char* e = getenv("TK_PDL");
         tk::TcParams run = pp;
-        run.pdl = (!e || atoi(e)) ? 1 : 0;
+        run.pdl = knob(K_PDL, 1) ? 1 : 0;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(grid);
         cfg.blockDim = dim3(tk::TC_THREADS);
@@ -1178,6 +1318,23 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
         cfg.numAttrs = run.pdl ? 1 : 0;
         TK_CUDA(cudaLaunchKernelEx(&cfg, kern, run));
         ++g_launches;
+        info_kernel("pair_ops");
+        g_info.tile_m = 256;
+        g_info.tile_n = bn;
+        g_info.mma_n = bn;
+        g_info.nsub = 1;
+        g_info.mmas_per_k16 = op == TK_OP_COMPLEX ? 4 : 3;
+        g_info.cluster = 2;
+        g_info.stages = bn == 256 ? tk::Tc2cPlan<256>::STAGES : tk::Tc2cPlan<128>::STAGES;
+        g_info.stage_bytes = bn == 256 ? tk::Tc2cPlan<256>::STAGE_BYTES : tk::Tc2cPlan<128>::STAGE_BYTES;
+        g_info.smem_bytes = smem_bytes;
+        g_info.tmem_cols = 512;
+        g_info.grid_ctas = grid;
+        g_info.tiles = g_info.units = run.num_tiles;
+        g_info.sk_parts = 1;
+        g_info.serpentine = run.serp;
+        g_info.group_m = run.group_m;
+        g_info.pdl = run.pdl;
         return TK_OK;
       };
       if (bn == 256) {
@@ -1219,6 +1376,9 @@ int launch_simt(const tk::SimtParams& sp, cudaStream_t s) {
   tk::simt_gemm_kernel<OP, T, Acc><<<int((total + threads - 1) / threads), threads, 0, s>>>(sp);
   TK_CUDA(cudaGetLastError());
   ++g_launches;
+  info_kernel("simt");
+  g_info.tile_m = g_info.tile_n = 1;
+  g_info.grid_ctas = int((total + threads - 1) / threads);
   return TK_OK;
 }
 
@@ -1386,6 +1546,7 @@ int tk_gemm(const TkGemmPlan* plan0, const void* a, const void* b, const void* c
             const uint8_t* kmask, void* workspace, int64_t workspace_bytes, void* stream) {
   g_err.clear();
   g_launches = 0;
+  info_reset();
   int rc = check_plan(plan0);
   if (rc) return rc;
   TkGemmPlan norm;
@@ -1407,9 +1568,45 @@ int tk_gemm(const TkGemmPlan* plan0, const void* a, const void* b, const void* c
     Workspace w = plan_workspace(plan, lane);
     if (w.total > 0 && (!workspace || workspace_bytes < w.total))
       return fail(TK_ERR_CONFIG, "workspace of %lld bytes required", (long long)w.total);
-    return run_tc(plan, a, b, c, d, bias, static_cast<uint8_t*>(workspace), w, s);
+    rc = run_tc(plan, a, b, c, d, bias, static_cast<uint8_t*>(workspace), w, s);
+    g_info.workspace_bytes = w.total;
+  } else {
+    rc = run_simt(plan, a, b, c, d, bias, kmask, s);
   }
-  return run_simt(plan, a, b, c, d, bias, kmask, s);
+  g_info.lane = lane;
+  g_info.op = plan->op;
+  g_info.launches = g_launches;
+  return rc;
+}
+
+int tk_last_plan_info(TkPlanInfo* out) {
+  if (!out) return fail(TK_ERR_CONFIG, "null output");
+  *out = g_info;
+  return TK_OK;
+}
+
+int tk_tune_set(const char* name, const char* value) {
+  if (!name) return fail(TK_ERR_CONFIG, "null knob name");
+  for (int i = 0; i < K_ENABLED; ++i)
+    if (!strcmp(name, kKnobNames[i])) {
+      int v;
+      if (int rc = parse_knob(i, value, &v)) return rc;
+      knob_table().v[i].store(v, std::memory_order_relaxed);
+      return TK_OK;
+    }
+  return fail(TK_ERR_CONFIG, "unknown tuning knob '%s'%s", name,
+              strncmp(name, "TK_DBG_", 7) ? "" : " (diagnostic knobs need a -DTK_DIAG build)");
+}
+
+int tk_tune_reset(void) {
+  knobs_from_env(knob_table());
+  return TK_OK;
+}
+
+int tk_tune_get(const char* name) {
+  for (int i = 0; name && i < K_ENABLED; ++i)
+    if (!strcmp(name, kKnobNames[i])) return knob_table().v[i].load(std::memory_order_relaxed);
+  return KNOB_UNSET;
 }
 
 int tk_gemm_peers(const TkGemmPlan* plan, const void* a, const void* b, const void* c, void* d,
@@ -1619,22 +1816,30 @@ namespace {
 
 struct ExStreams {
   cudaStream_t in = nullptr, comp = nullptr, out = nullptr;
+  cudaMemPool_t pool = nullptr;  // private: staging memory stays cached between calls
   bool ok = false;
 };
 
+// Per device: three streams and a private stream-ordered pool for the staging buffers (the
+// device's default pool, which the host application may use too, is left untouched).
 ExStreams& ex_streams() {
-  static ExStreams st;
-  static std::once_flag once;
-  std::call_once(once, [] {
+  static ExStreams st_dev[TK_MAX_DEV];
+  static std::once_flag once[TK_MAX_DEV];
+  const int dev = cur_dev();
+  ExStreams& st = st_dev[dev];
+  std::call_once(once[dev], [&st, dev] {
     st.ok = cudaStreamCreateWithFlags(&st.in, cudaStreamNonBlocking) == cudaSuccess &&
             cudaStreamCreateWithFlags(&st.comp, cudaStreamNonBlocking) == cudaSuccess &&
             cudaStreamCreateWithFlags(&st.out, cudaStreamNonBlocking) == cudaSuccess;
-    // keep freed staging memory in the stream-ordered pool between calls
-    int dev = 0;
-    cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    if (st.ok && cudaMemPoolCreate(&st.pool, &props) == cudaSuccess) {
       uint64_t thr = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      cudaMemPoolSetAttribute(st.pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    } else {
+      st.ok = false;
     }
   });
   return st;
@@ -1650,12 +1855,11 @@ int ex_pipelined(int tag, int ta, long long m, long long n, long long k, double 
   if (!st.ok) return fail(TK_ERR_CUDA, "stream creation failed");
   const int64_t sa = m * k * esz_ab * pairf, sb = k * n * esz_ab * pairf, sc = m * n * esz_c * pairf;
   void *da = nullptr, *db = nullptr, *dc = nullptr;
-  TK_CUDA(cudaMallocAsync(&da, sa, st.in));
-  TK_CUDA(cudaMallocAsync(&db, sb, st.in));
-  TK_CUDA(cudaMallocAsync(&dc, sc, st.in));
+  TK_CUDA(cudaMallocFromPoolAsync(&da, sa, st.pool, st.in));
+  TK_CUDA(cudaMallocFromPoolAsync(&db, sb, st.pool, st.in));
+  TK_CUDA(cudaMallocFromPoolAsync(&dc, sc, st.pool, st.in));
   TK_CUDA(cudaMemcpyAsync(da, a, sa, cudaMemcpyHostToDevice, st.in));
-  int max_slabs = 8;
-  if (const char* e = getenv("TK_EX_SLABS")) max_slabs = std::max(1, atoi(e));
+  const int max_slabs = std::max(1, knob(K_EX_SLABS, 8));
   int slabs = int(std::max<long long>(1, std::min<long long>(max_slabs, n / 1024)));
   const long long w = ((n / slabs + 255) / 256) * 256;
   slabs = int((n + w - 1) / w);
@@ -1700,6 +1904,7 @@ int ex_pipelined(int tag, int ta, long long m, long long n, long long k, double 
     cudaEventDestroy(ev_done[i]);
   }
   g_launches = launches;
+  g_info.launches = launches;
   if (rc == TK_OK) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(TK_ERR_CUDA, "pipelined gemm_ex: %s", cudaGetErrorString(e));

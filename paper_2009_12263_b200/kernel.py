@@ -547,7 +547,6 @@ def gemm_execute(config: KernelConfig, a, b, c, d, *, stream=None, synchronize: 
         if prep.ws_bytes:
             ws = torch.empty(prep.ws_bytes, dtype=torch.uint8, device=device)
             _note("workspace", prep.ws_bytes)
-        _note_onchip(prep.plan, prep.lane_id)
         s = stream if stream is not None else torch.cuda.current_stream(device)
         args = (prep.plan_ref, A.ptr(), B.ptr(), C.ptr(), D.ptr(),
                 bias_dev.ptr() if bias_dev else None,
@@ -565,6 +564,8 @@ def gemm_execute(config: KernelConfig, a, b, c, d, *, stream=None, synchronize: 
             raise RuntimeError(f"libtk_sm100: {_lib.last_error()}")
         _LAST["lane"] = _lib.LANE_NAMES[prep.lane_id]
         _LAST["launches"] = lib.tk_last_launch_count()
+        _LAST["plan"] = _lib.plan_info()
+        _note_onchip(_LAST["plan"])
         if D.host is not None:
             s.synchronize()
             D.copy_back()
@@ -577,16 +578,15 @@ def gemm_execute(config: KernelConfig, a, b, c, d, *, stream=None, synchronize: 
     return dataclasses.replace(prep.counters)
 
 
-def _note_onchip(plan, lane_id):
-    if _audit.get() is None:
+def _note_onchip(info):
+    """Log what the launched kernel holds on chip, from the library's own record of the launch
+    (tk_last_plan_info): per CTA, each operand stage of the shared-memory ring, the streamed-C
+    ring and the TMEM accumulator columns (128 lanes x 4 bytes each)."""
+    if _audit.get() is None or info.get("lane") != _lib.LANE_TCGEN05 or not info.get("stages"):
         return
-    if lane_id == _lib.LANE_TCGEN05:
-        pair = plan.op != 0
-        bn = 128 if pair else 256
-        stages = 3 if pair else 4
-        planes = 2 if pair else 1
-        for s in range(stages):
-            _note(f"smem:stage_a[{s}]", planes * 128 * 64)
-            _note(f"smem:stage_b[{s}]", planes * bn * 64)
-        for s in range(2):
-            _note(f"tmem:accumulator[{s}]", 128 * 256)
+    for s in range(info["stages"]):
+        _note(f"smem:stage[{s}] ({info['kernel']}, {info['tile_m']}x{info['tile_n']} tile)",
+              info["stage_bytes"])
+    if info["cring_bytes"]:
+        _note("smem:c_ring", info["cring_bytes"])
+    _note("tmem:accumulator_columns", info["tmem_cols"])

@@ -121,8 +121,18 @@ def sharded_gemm(config, a, b, c, d, *, rank: int, world: int, group=None,
     ``torch.distributed.all_gather_into_tensor`` on ``group``.  With ``fused=True`` and
     ``peers`` (a ``PeerBuffers`` over each rank's ``allgather_into``) the slab is instead
     written by the GEMM itself into the local and every peer's full D (peer-memory stores from
-    the epilogue, overlapping the remaining tiles); the ranks are then synchronised with a
-    stream sync and a barrier.  Returns the slab counters.
+    the epilogue, overlapping the remaining tiles).
+
+    Ordering of the fused path (both sides are needed because peers write into memory this
+    rank reads):
+
+    * write side -- before the GEMM, every rank drains its device (so all work already queued
+      that reads its ``allgather_into``, e.g. from the previous call, has finished) and the
+      ranks meet at a barrier; only then may any rank's epilogue store into a peer's buffer;
+    * read side -- after the GEMM, a device sync and a second barrier publish the gathered D:
+      every rank's slab has landed in every buffer when ``sharded_gemm`` returns.
+
+    Returns the slab counters.
     """
     slab, off, _ = shard_config(config, rank, world)
     sb = slab.global_b_layout.physical_size()
@@ -135,6 +145,8 @@ def sharded_gemm(config, a, b, c, d, *, rank: int, world: int, group=None,
         import torch.distributed as dist
 
         dst = _view(allgather_into, off["D"], sd)
+        torch.cuda.synchronize(dst.device)  # write side: no reader of the buffers is in flight
+        dist.barrier(group=group)
         counters = kernel.gemm_execute(slab, a, _view(b, off["B"], sb), _view(c, off["C"], sc),
                                        dst, peers=peers.peer_slabs(off["D"] * dst.element_size()),
                                        **run_kwargs)

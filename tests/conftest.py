@@ -20,3 +20,13 @@ def cuda():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return torch.device("cuda:0")
+
+
+@pytest.fixture
+def knob():
+    """Set libtk_sm100 tuning knobs for one test (tk_tune_set); every override is dropped at
+    teardown.  The library reads TK_* from the environment only once, at load."""
+    from paper_2009_12263_b200 import _lib
+
+    yield _lib.tune
+    _lib.tune_reset()

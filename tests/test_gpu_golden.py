@@ -58,6 +58,25 @@ def test_f16_valued_on_both_lanes(cuda):
     assert np.array_equal(d2.reshape((m, n), order="F"), z["d"])
 
 
+def test_c1_default_tiling_both_lanes(cuda):
+    """BASELINE C1 (256^3, default tiling (256, 256, 8), reference-generated golden): the
+    tcgen05 lane on fp16 storage within 4 * 2^-24 * sqrt(K); the exact lane bitwise."""
+    meta, z = load("c1_dense_256")
+    m, n, k = meta["m"], meta["n"], meta["k"]
+    a16, b16 = z["a"].astype(np.float16), z["b"].astype(np.float16)
+    cfg = tk.build_dense_config(m, n, k, np.float16)
+    assert list(tk.kernel.resolve_config(cfg).params.block_tile) == meta["block_tile"]
+    d = np.zeros(m * n, np.float32)
+    cnt = tk.matmul(cfg, F(a16), F(b16), F(z["c"]), d)
+    assert tk.last_run()["lane"] == "tcgen05"
+    assert O.rel_err(d.reshape((m, n), order="F"), z["d"]) <= O.tolerance(k)
+    assert dataclasses.asdict(cnt) == meta["counters"]
+    with tk.force_lane("simt"):
+        d2 = np.zeros(m * n, np.float32)
+        tk.matmul(cfg, F(a16), F(b16), F(z["c"]), d2)
+    assert np.array_equal(d2.reshape((m, n), order="F"), z["d"])
+
+
 def test_f64_and_wide_bitwise(cuda):
     meta, z = load("dense_f64_int")
     m, n, k = meta["m"], meta["n"], meta["k"]

@@ -42,18 +42,18 @@ def _f32(x):
 
 
 @pytest.fixture(params=["single", "pair", "pair128", "pair64", "pair512", "quad", "stream"])
-def tc_kernel(request, monkeypatch):
+def tc_kernel(request, knob):
     """Pin the single-CTA (128x256), CTA-pair (256 x 256/128/64 tiles, or 256 x 512 with two
     MMAs per K step), 4-CTA multicast or C-streaming tcgen05 kernel."""
     name = request.param
     if name.startswith("pair") and name != "pair":
-        monkeypatch.setenv("TK_TC_KERNEL", "pair")
+        knob("TK_TC_KERNEL", "pair")
         if name == "pair512":
-            monkeypatch.setenv("TK_PAIR_NSUB", "2")
+            knob("TK_PAIR_NSUB", "2")
         else:
-            monkeypatch.setenv("TK_PAIR_BNI", name[4:])
+            knob("TK_PAIR_BNI", name[4:])
     else:
-        monkeypatch.setenv("TK_TC_KERNEL", name)
+        knob("TK_TC_KERNEL", name)
     return name
 
 
@@ -103,12 +103,12 @@ _SPLITK_WANT = {}
 
 @pytest.mark.parametrize("mnk", [(2560, 2560, 8192), (1536, 4096, 8192), (1280, 1280, 16384)])
 @pytest.mark.parametrize("splitk", ["0", "1"])
-def test_split_k_last_wave(cuda, mnk, splitk, monkeypatch):
+def test_split_k_last_wave(cuda, mnk, splitk, knob):
     """Pair kernel with the poorly filled last wave cut into K-parts (FP32 partials in the
     workspace, reduced in a fixed order by the last part): integer inputs stay bitwise exact,
     random inputs within tolerance, with or without the split."""
-    monkeypatch.setenv("TK_SPLITK", splitk)
-    monkeypatch.setenv("TK_PAIR_BNI", "256")  # 256-wide tiles: the last wave is R = T % 74 tiles
+    knob("TK_SPLITK", splitk)
+    knob("TK_PAIR_BNI", "256")  # 256-wide tiles: the last wave is R = T % 74 tiles
     m, n, k = mnk
     rng = np.random.default_rng(17)
     for integer in (True, False):
@@ -132,12 +132,12 @@ def test_split_k_last_wave(cuda, mnk, splitk, monkeypatch):
 
 
 @pytest.mark.parametrize("mnk,minkb", [((2560, 2560, 8192), "64"), ((1024, 1024, 1024), "4")])
-def test_split_k_ring_matches_direct(cuda, mnk, minkb, monkeypatch):
+def test_split_k_ring_matches_direct(cuda, mnk, minkb, knob):
     """Split-K partials moved as TMA boxes through the C ring (default) and by per-thread
     stores/loads (TK_SK_TMA=0) sum in the same order: bitwise equal on random inputs."""
     m, n, k = mnk
-    monkeypatch.setenv("TK_PAIR_BNI", "256")
-    monkeypatch.setenv("TK_SPLITK_MINKB", minkb)
+    knob("TK_PAIR_BNI", "256")
+    knob("TK_SPLITK_MINKB", minkb)
     g = torch.Generator(device=cuda)
     g.manual_seed(9)
     a = torch.randn(m * k, generator=g, device=cuda).half()
@@ -146,21 +146,25 @@ def test_split_k_ring_matches_direct(cuda, mnk, minkb, monkeypatch):
     cfg = tk.build_dense_config(m, n, k, np.float16)
     outs = []
     for mode in ("1", "0"):
-        monkeypatch.setenv("TK_SK_TMA", mode)
+        knob("TK_SK_TMA", mode)
         d = torch.full((m * n,), float("nan"), device=cuda)
         tk.matmul(cfg, a, b, c, d)
+        plan = tk.last_run()["plan"]
+        # the split really ran, with the requested hand-off (not a silently unsplit launch)
+        assert plan["kernel"] == "pair" and plan["sk_parts"] > 1, plan
+        assert plan["sk_tma"] == int(mode), plan
         outs.append(d)
     assert torch.equal(outs[0], outs[1])
 
 
 @pytest.mark.parametrize("mnk", [(8192, 8192, 8192), (4096, 8192 + 512, 8192)])
-def test_staggered_schedule_bitwise(cuda, mnk, monkeypatch):
+def test_staggered_schedule_bitwise(cuda, mnk, knob):
     """The opt-in staggered 256 x 512 schedule (half of the clusters split one tile into a
     leading and a trailing half) covers every tile exactly once: bitwise equal to the default
     schedule with serpentine K off (same k order per tile)."""
     m, n, k = mnk
-    monkeypatch.setenv("TK_SERPENTINE", "0")
-    monkeypatch.setenv("TK_PAIR_NSUB", "2")
+    knob("TK_SERPENTINE", "0")
+    knob("TK_PAIR_NSUB", "2")
     g = torch.Generator(device=cuda)
     g.manual_seed(5)
     a = torch.randn(m * k, generator=g, device=cuda).half()
@@ -169,7 +173,7 @@ def test_staggered_schedule_bitwise(cuda, mnk, monkeypatch):
     cfg = tk.build_dense_config(m, n, k, np.float16)
     outs = []
     for stagger in ("0", "1"):
-        monkeypatch.setenv("TK_STAGGER", stagger)
+        knob("TK_STAGGER", stagger)
         d = torch.full((m * n,), float("nan"), device=cuda)
         tk.matmul(cfg, a, b, c, d)
         outs.append(d)
@@ -177,7 +181,7 @@ def test_staggered_schedule_bitwise(cuda, mnk, monkeypatch):
 
 
 @pytest.mark.parametrize("trans", ["nn", "tt"])
-def test_full_size_c3_tile_shapes_agree(cuda, trans, monkeypatch):
+def test_full_size_c3_tile_shapes_agree(cuda, trans, knob):
     """The bench-size (8192^3) C3 epilogue (alpha/beta, bias, ReLU) on the default 256 x 512
     pair tiles against 256 x 256 tiles (same k order with serpentine off: bitwise equal), and
     sampled rows against the float64 product (size-independent checks at full size)."""
@@ -194,10 +198,10 @@ def test_full_size_c3_tile_shapes_agree(cuda, trans, monkeypatch):
         tk.build_dense_config(m, n, k, np.float16, trans_a=ta, trans_b=tb),
         transform_g2s_c=tk.components.scale(be / al), transform_r2s_d=tk.components.scale(al),
         epilogue=tk.components.BiasEpilogue(bias), transform_s2g_d=tk.components.relu)
-    monkeypatch.setenv("TK_SERPENTINE", "0")
+    knob("TK_SERPENTINE", "0")
     outs = []
     for nsub in ("2", "1"):
-        monkeypatch.setenv("TK_PAIR_NSUB", nsub)
+        knob("TK_PAIR_NSUB", nsub)
         d = torch.empty(m * n, device=cuda)
         tk.matmul(cfg, a, b, c, d)
         outs.append(d)
@@ -235,12 +239,12 @@ def test_fused_affine_bias_relu(cuda):
 @pytest.mark.parametrize("kernel", ["auto", "single", "pair", "pair256"])
 @pytest.mark.parametrize("split", [False, True])
 @pytest.mark.parametrize("kind", ["complex", "dual"])
-def test_pair_operators(cuda, split, kind, kernel, monkeypatch):
+def test_pair_operators(cuda, split, kind, kernel, knob):
     if kernel == "pair256":  # 256-wide pair tiles, one accumulator pair
-        monkeypatch.setenv("TK_TC_KERNEL", "pair")
-        monkeypatch.setenv("TK_PAIROPS_BN", "256")
+        knob("TK_TC_KERNEL", "pair")
+        knob("TK_PAIROPS_BN", "256")
     elif kernel != "auto":
-        monkeypatch.setenv("TK_TC_KERNEL", kernel)
+        knob("TK_TC_KERNEL", kernel)
     m, n, k = 512, 384, 320
     rng = np.random.default_rng(3)
     h16 = lambda s: rng.standard_normal(s).astype(np.float16)
@@ -281,11 +285,11 @@ def test_pair_operators(cuda, split, kind, kernel, monkeypatch):
 @pytest.mark.parametrize("bn", ["128", "256"])
 @pytest.mark.parametrize("split", [False, True])
 @pytest.mark.parametrize("kind", ["complex", "dual"])
-def test_pair_operators_bf16_integer_exact(cuda, kind, split, bn, monkeypatch):
+def test_pair_operators_bf16_integer_exact(cuda, kind, split, bn, knob):
     """bf16 pair storage (COMPLEXBF16 / DUALBF16) on both pair-tile widths: small-integer
     inputs make every product and sum exact, so the result is bitwise the oracle's."""
-    monkeypatch.setenv("TK_TC_KERNEL", "pair")
-    monkeypatch.setenv("TK_PAIROPS_BN", bn)
+    knob("TK_TC_KERNEL", "pair")
+    knob("TK_PAIROPS_BN", bn)
     m, n, k = 512, 512, 320
     rng = np.random.default_rng(8)
     ints = lambda s: rng.integers(-4, 5, s).astype(np.float32)
@@ -336,13 +340,13 @@ def _unpack_pair(t, shape, split):
 
 @pytest.mark.parametrize("kernel", ["auto", "single", "tensor"])
 @pytest.mark.parametrize("n", [256, 1024, 640])
-def test_diagonal_variant(cuda, n, kernel, monkeypatch):
+def test_diagonal_variant(cuda, n, kernel, knob):
     """auto: the vectorised HBM stream; single / tensor: the tcgen05 kernel with the diagonal
     tile fabricated in shared memory -- all bitwise equal to the oracle."""
     if kernel == "single":
-        monkeypatch.setenv("TK_TC_KERNEL", kernel)
+        knob("TK_TC_KERNEL", kernel)
     elif kernel == "tensor":
-        monkeypatch.setenv("TK_DIAG_STREAM", "0")
+        knob("TK_DIAG_STREAM", "0")
     rng = np.random.default_rng(4)
     diag = rng.standard_normal(n).astype(np.float16)
     b = rng.standard_normal((n, n)).astype(np.float16)
@@ -359,10 +363,10 @@ def test_diagonal_variant(cuda, n, kernel, monkeypatch):
 
 
 @pytest.mark.parametrize("stream", ["1", "0", "misaligned"])
-def test_diagonal_epilogue_rectangular(cuda, stream, monkeypatch):
+def test_diagonal_epilogue_rectangular(cuda, stream, knob):
     """Diagonal A with alpha/beta scaling, a row bias and ReLU, N != M; 'misaligned' offsets
     the buffers by one element so the stream kernel takes its scalar path."""
-    monkeypatch.setenv("TK_DIAG_STREAM", "0" if stream == "0" else "1")
+    knob("TK_DIAG_STREAM", "0" if stream == "0" else "1")
     m, n, k = 520, 384, 520
     rng = np.random.default_rng(6)
     diag = rng.integers(-4, 5, min(m, k)).astype(np.float16)

@@ -30,6 +30,13 @@ def test_dense_f16valued_bitwise():
     assert np.array_equal(O.gemm_real(z["a"], z["b"], z["c"]), z["d"])
 
 
+def test_c1_default_tiling_bitwise():
+    """BASELINE C1: 256^3 fp16-valued at the reference's default tiling (256, 256, 8)."""
+    meta, z = load("c1_dense_256")
+    assert meta["block_tile"] == [256, 256, 8]
+    assert np.array_equal(O.gemm_real(z["a"], z["b"], z["c"]), z["d"])
+
+
 def test_dense_f64_integer_bitwise():
     _, z = load("dense_f64_int")
     assert np.array_equal(O.gemm_real(z["a"], z["b"], z["c"]), z["d"])

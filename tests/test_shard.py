@@ -87,12 +87,12 @@ def test_gloo_world2_allgather_equals_unsharded():
 
 
 @pytest.mark.gpu
-def test_device_slabs_match_single_gpu_columns(monkeypatch):
+def test_device_slabs_match_single_gpu_columns(knob):
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    monkeypatch.setenv("TK_TC_KERNEL", "pair")
-    monkeypatch.setenv("TK_SERPENTINE", "0")  # same k order in every tile of every slab
+    knob("TK_TC_KERNEL", "pair")
+    knob("TK_SERPENTINE", "0")  # same k order in every tile of every slab
     m, n, k = 1024, 2048, 512
     rng = np.random.default_rng(3)
     dev = lambda x: torch.from_numpy(np.ascontiguousarray(np.asarray(x).ravel(order="F"))).cuda()
