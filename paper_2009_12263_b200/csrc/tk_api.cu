@@ -230,13 +230,15 @@ int check_plan(const TkGemmPlan* p) {
 }
 
 // ------------------------------------------------------------------ lane selection
-bool affine_of(const TkTransform& t, double& alpha, double& beta) {
-  alpha = 1.0;
-  beta = 0.0;
+// A load transform whose result is always representable in the operand's own half type
+// (relu, scale by +-1, add 0): the transform pass writes one plane and the ordinary real
+// kernels run on it.  Any other program needs the hi + lo split (OP_SPLIT kernels).
+bool half_exact(const TkTransform& t) {
   for (int i = 0; i < t.n; ++i) {
-    if (t.op[i] == TK_T_SCALE) { alpha *= t.re[i]; beta *= t.re[i]; }
-    else if (t.op[i] == TK_T_ADD) beta += t.re[i];
-    else return false;
+    if (t.op[i] == TK_T_RELU) continue;
+    if (t.op[i] == TK_T_SCALE && (t.re[i] == 1.0 || t.re[i] == -1.0)) continue;
+    if (t.op[i] == TK_T_ADD && t.re[i] == 0.0) continue;
+    return false;
   }
   return true;
 }
@@ -338,9 +340,11 @@ bool tc_lane_ok(const TkGemmPlan* p, std::string& why) {
   if (p->c.kind != TK_LAYOUT_ZERO && p->c.scalar != TK_F32) return no("C must be f32");
   if (p->d.scalar != TK_F32) return no("D must be f32");
   if (p->c.kind == TK_LAYOUT_DIAGONAL) return no("Diagonal C unsupported on tcgen05 lane");
-  double al, be;
-  if (!affine_of(p->t_a, al, be) || !affine_of(p->t_b, al, be)) return no("non-affine A/B transform");
   if (p->op != TK_OP_REAL && (p->t_a.n || p->t_b.n)) return no("pair operands need identity g2s");
+  // transformed operands go through the transform pass: fp16 splits into hi + lo planes; bf16
+  // would need three planes for the reference's f32 transform result, so only exact programs
+  if (p->a.scalar == TK_BF16 && !(half_exact(p->t_a) && half_exact(p->t_b)))
+    return no("bf16 operand transforms beyond relu / scale(+-1) run on the exact lane");
   if (p->predicate == TK_PRED_MASK) return no("arbitrary predicates run on the exact lane");
   if (p->predicate == TK_PRED_DIAGONAL && p->a.kind != TK_LAYOUT_DIAGONAL)
     return no("diagonal predicate over a dense A runs on the exact lane");
@@ -360,8 +364,9 @@ int choose_lane(const TkGemmPlan* p, std::string* why_out = nullptr) {
 
 // ------------------------------------------------------------------ workspace plan
 struct Workspace {
-  int64_t a_planes = -1, b_planes = -1, rowsum = -1, colsum = -1, a_perm = -1, a_pack = -1, b_pack = -1,
-          splitk = -1, total = 0;
+  int64_t a_planes = -1, b_planes = -1, a_perm = -1, a_pack = -1, b_pack = -1, splitk = -1,
+          a_tx = -1, b_tx = -1, tx_flags = -1, total = 0;
+  bool tx_split = false;  // transformed operands carry hi + lo planes (OP_SPLIT)
 };
 
 int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
@@ -402,15 +407,19 @@ Workspace plan_workspace(const TkGemmPlan* p0, int lane) {
     w.b_planes = w.total;
     w.total += align256(p->k * p->n * 2 * 2);
   }
-  double aa, ba, ab, bb;
-  affine_of(p->t_a, aa, ba);
-  affine_of(p->t_b, ab, bb);
-  if (p->op == TK_OP_REAL && p->a.kind != TK_LAYOUT_DIAGONAL) {  // split-K partials (pair kernel)
+  // load transforms (g2s_a / g2s_b): transformed operand planes, hi (+ lo), and the lo flags
+  if (p->op == TK_OP_REAL && (p->t_a.n || p->t_b.n)) {
+    w.tx_split = !(half_exact(p->t_a) && half_exact(p->t_b));
+    const int planes = w.tx_split ? 2 : 1;
+    if (p->t_a.n) { w.a_tx = w.total; w.total += align256(p->m * p->k * 2 * planes); }
+    if (p->t_b.n) { w.b_tx = w.total; w.total += align256(p->k * p->n * 2 * planes); }
+    w.tx_flags = w.total;
+    w.total += 256;
+  }
+  if (p->op == TK_OP_REAL && !w.tx_split && p->a.kind != TK_LAYOUT_DIAGONAL) {  // split-K partials (pair kernel)
     const int64_t sb = split_ws_bytes(p->m, p->n, p->k, p->b);
     if (sb > 0) { w.splitk = w.total; w.total += align256(sb); }
   }
-  if (p->op == TK_OP_REAL && bb != 0.0) { w.rowsum = w.total; w.total += align256(p->m * 4); }
-  if (p->op == TK_OP_REAL && ba != 0.0) { w.colsum = w.total; w.total += align256(p->n * 4); }
   return w;
 }
 
@@ -924,9 +933,56 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
     }
     p = &packed;
   }
+  // ---- load transforms (g2s_a / g2s_b, reference kernel.py:406-418): one pass per transformed
+  // operand writes t(x) as an fp16 hi plane (+ lo plane: OP_SPLIT) in the operand's orientation
+  TkGemmPlan txp;
+  if (w.tx_flags >= 0) {
+    txp = *p;
+    int32_t* flags = reinterpret_cast<int32_t*>(ws + w.tx_flags);
+    TK_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int32_t), s));
+    auto run_tx = [&](const TkLayout& L, const TkTransform& t, const void*& ptr, TkLayout& out,
+                      int64_t rows, int64_t cols, int64_t off, int32_t* flag) -> int {
+      int mn;  // 1: dim 0 contiguous
+      int64_t pitch;
+      tma_operand(L, mn, pitch);
+      const int64_t fast = mn ? rows : cols, slow = mn ? cols : rows, vol = rows * cols;
+      __half* hi = reinterpret_cast<__half*>(ws + off);
+      const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>((vol / 8 + 255) / 256, 8 * sm_count())));
+      if (w.tx_split)
+        tk::transform_split_kernel<true><<<grid, 256, 0, s>>>(static_cast<const __half*>(ptr), hi, hi + vol,
+                                                              fast, slow, pitch, to_prog(t), flag);
+      else
+        tk::transform_split_kernel<false><<<grid, 256, 0, s>>>(static_cast<const __half*>(ptr), hi, hi + vol,
+                                                               fast, slow, pitch, to_prog(t), flag);
+      TK_CUDA(cudaGetLastError());
+      ++g_launches;
+      dense_operand(out, rows, cols);
+      if (!mn) {  // keep the source orientation (K-major A / N-major B stay so)
+        out.stride[0][0] = cols;
+        out.stride[1][0] = 1;
+      }
+      out.pair = w.tx_split ? TK_PAIR_SPLIT : TK_PAIR_NONE;
+      out.plane_stride = w.tx_split ? vol : 0;
+      out.size = vol * (w.tx_split ? 2 : 1);
+      ptr = hi;
+      return TK_OK;
+    };
+    int rc;
+    if (p->t_a.n && (rc = run_tx(p->a, p->t_a, a, txp.a, p->m, p->k, w.a_tx, flags))) return rc;
+    if (p->t_b.n && (rc = run_tx(p->b, p->t_b, b, txp.b, p->k, p->n, w.b_tx, flags + 1))) return rc;
+    if (w.tx_split) {  // an untransformed operand: its "lo plane" is never read (flag stays 0)
+      if (!p->t_a.n) { txp.a.pair = TK_PAIR_SPLIT; txp.a.plane_stride = 0; }
+      if (!p->t_b.n) { txp.b.pair = TK_PAIR_SPLIT; txp.b.plane_stride = 0; }
+    }
+    txp.t_a.n = txp.t_b.n = 0;
+    p = &txp;
+  }
   tk::TcParams prm;
   memset(&prm, 0, sizeof(prm));
-  const int op = p->op;
+  // kernel operator: the plan's, or OP_SPLIT for hi + lo transformed operands (a real GEMM)
+  const int kop = w.tx_split ? int(tk::OP_SPLIT) : p->op;
+  const int op = kop;
+  if (w.tx_flags >= 0) prm.split_flags = reinterpret_cast<const int32_t*>(ws + w.tx_flags);
   const int planes = op == TK_OP_REAL ? 1 : 2;
   const int BN = op == TK_OP_REAL ? tk::TcCfg<tk::OP_REAL>::BN : tk::TcCfg<tk::OP_COMPLEX>::BN;
   prm.m = int(p->m);
@@ -998,51 +1054,6 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
       if (rc) return rc;
     }
   }
-  // ---- affine operand transforms -> epilogue terms
-  double aa, ba, ab, bb;
-  affine_of(p->t_a, aa, ba);
-  affine_of(p->t_b, ab, bb);
-  if (op == TK_OP_REAL && (aa != 1.0 || ba != 0.0 || ab != 1.0 || bb != 0.0)) {
-    prm.affine = 1;
-    prm.aff_s = float(aa * ab);
-    prm.aff_r = float(aa * bb);
-    prm.aff_q = float(ba * ab);
-    prm.aff_k = float(double(p->k) * ba * bb);
-    auto row_sums = [&](const TkLayout& L, const void* x, float* out, int64_t count, int64_t len,
-                        int dim_count) -> int {
-      // sums over the other dimension for each index of dim `dim_count`
-      const int64_t s_count = L.stride[dim_count][0], s_len = L.stride[1 - dim_count][0];
-      if (s_count == 1) {
-        TK_CUDA(cudaMemsetAsync(out, 0, count * sizeof(float), s));
-        const int bx = int((count + 255) / 256);
-        const int by = int(std::max<int64_t>(1, std::min<int64_t>(len / 32, (8 * sm_count() + bx - 1) / bx)));
-        const dim3 grid(bx, by);
-        if (L.scalar == TK_F16)
-          tk::strided_sum_unit_kernel<__half><<<grid, 256, 0, s>>>(static_cast<const __half*>(x), out, count, len, s_len);
-        else
-          tk::strided_sum_unit_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x), out, count, len, s_len);
-      } else {
-        const int blocks = int((count * 32 + 255) / 256);
-        if (L.scalar == TK_F16)
-          tk::strided_sum_kernel<__half><<<blocks, 256, 0, s>>>(static_cast<const __half*>(x), out, count, len, s_count, s_len);
-        else
-          tk::strided_sum_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x), out, count, len, s_count, s_len);
-      }
-      TK_CUDA(cudaGetLastError());
-      ++g_launches;
-      return TK_OK;
-    };
-    if (w.rowsum >= 0) {
-      prm.rowsum_a = reinterpret_cast<float*>(ws + w.rowsum);
-      int rc = row_sums(p->a, a, reinterpret_cast<float*>(ws + w.rowsum), p->m, p->k, 0);
-      if (rc) return rc;
-    }
-    if (w.colsum >= 0) {
-      prm.colsum_b = reinterpret_cast<float*>(ws + w.colsum);
-      int rc = row_sums(p->b, b, reinterpret_cast<float*>(ws + w.colsum), p->n, p->k, 1);
-      if (rc) return rc;
-    }
-  }
   // ---- epilogue
   prm.c_zero = p->c.kind == TK_LAYOUT_ZERO;
   prm.c_zero |= knob(K_DBG_C_ZERO, 0) ? 1 : 0;  // diagnostic builds only: skip C
@@ -1083,13 +1094,13 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
   prm.pol_a = prm.pol_b = prm.pol_ab ? 1 : 0;
   prm.pol_a = knob(K_POL_A, prm.pol_a);
   prm.pol_b = knob(K_POL_B, prm.pol_b);
-  const bool pair = op != TK_OP_REAL;
+  const bool pair = op == TK_OP_COMPLEX || op == TK_OP_DUAL;  // pair-valued epilogue
   // real operator: C/D rows may follow any digit map (GETT outputs whose M indices are not
   // one contiguous run) as long as columns are one strided digit -- the register epilogue
   // then adds a per-thread row offset instead of i (rows stay coalesced inside a run)
   auto rowmapped = [&](const TkLayout& L, int64_t& ld, int32_t& flag) {
     if (colmajor_dense(L, ld)) return true;
-    if (op != TK_OP_REAL || L.kind != TK_LAYOUT_STRIDED || L.ndigits[1] != 1) return false;
+    if (pair || L.kind != TK_LAYOUT_STRIDED || L.ndigits[1] != 1) return false;
     ld = L.stride[1][0];
     flag = 1;
     return true;
@@ -1112,7 +1123,7 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
   const bool single_wave = prm.num_tiles <= sm_count();
   const bool rmapped = prm.c_rmap || prm.d_rmap;
   // diagonal A: an HBM stream, run as one (vectorised) elementwise pass, not on the tensor cores
-  if (op == TK_OP_REAL && prm.diag_a && dense && !rmapped && !prm.affine && prm.b_mn == 0 &&
+  if (op == TK_OP_REAL && prm.diag_a && dense && !rmapped && prm.b_mn == 0 &&
       (ov == 0 || ov == 5)) {
     if (knob(K_DIAG_STREAM, 1)) {
       int mnk;
@@ -1294,9 +1305,9 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
       if (mn)  // K-major B: this CTA's bn/2-column half per box
         for (int pl = 0; pl < 2; ++pl)
           if ((rc = make_map_2d(&pp.tb[pl], planes_b[pl], p->b.scalar, p->k, p->n, pitch, 64, bn / 2))) return rc;
-      static bool attr_dev[TK_MAX_DEV][2][2][2] = {};
+      static bool attr_dev[TK_MAX_DEV][3][2][2] = {};  // [device][complex, dual, split][dense][bn 256]
       auto& attr = attr_dev[cur_dev()];
-      const int oi = op == TK_OP_COMPLEX ? 0 : 1;
+      const int oi = op == TK_OP_COMPLEX ? 0 : op == TK_OP_DUAL ? 1 : 2;
       const int smem_bytes = bn == 256 ? tk::Tc2cPlan<256>::SMEM : tk::Tc2cPlan<128>::SMEM;
       auto launch = [&](auto kern) -> int {
         if (!attr[oi][dense][bn == 256]) {
@@ -1323,7 +1334,7 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
         g_info.tile_n = bn;
         g_info.mma_n = bn;
         g_info.nsub = 1;
-        g_info.mmas_per_k16 = op == TK_OP_COMPLEX ? 4 : 3;
+        g_info.mmas_per_k16 = op == TK_OP_COMPLEX ? 4 : 3;  // dual / split: 3 (split: at most)
         g_info.cluster = 2;
         g_info.stages = bn == 256 ? tk::Tc2cPlan<256>::STAGES : tk::Tc2cPlan<128>::STAGES;
         g_info.stage_bytes = bn == 256 ? tk::Tc2cPlan<256>::STAGE_BYTES : tk::Tc2cPlan<128>::STAGE_BYTES;
@@ -1341,12 +1352,18 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
         if (op == TK_OP_COMPLEX)
           return dense ? launch(tk::tc_gemm_pair_ops_kernel<tk::OP_COMPLEX, true, 256>)
                        : launch(tk::tc_gemm_pair_ops_kernel<tk::OP_COMPLEX, false, 256>);
+        if (op == tk::OP_SPLIT)
+          return dense ? launch(tk::tc_gemm_pair_ops_kernel<tk::OP_SPLIT, true, 256>)
+                       : launch(tk::tc_gemm_pair_ops_kernel<tk::OP_SPLIT, false, 256>);
         return dense ? launch(tk::tc_gemm_pair_ops_kernel<tk::OP_DUAL, true, 256>)
                      : launch(tk::tc_gemm_pair_ops_kernel<tk::OP_DUAL, false, 256>);
       }
       if (op == TK_OP_COMPLEX)
         return dense ? launch(tk::tc_gemm_pair_ops_kernel<tk::OP_COMPLEX, true>)
                      : launch(tk::tc_gemm_pair_ops_kernel<tk::OP_COMPLEX, false>);
+      if (op == tk::OP_SPLIT)
+        return dense ? launch(tk::tc_gemm_pair_ops_kernel<tk::OP_SPLIT, true>)
+                     : launch(tk::tc_gemm_pair_ops_kernel<tk::OP_SPLIT, false>);
       return dense ? launch(tk::tc_gemm_pair_ops_kernel<tk::OP_DUAL, true>)
                    : launch(tk::tc_gemm_pair_ops_kernel<tk::OP_DUAL, false>);
     }
@@ -1354,6 +1371,7 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
   switch (op) {
     case TK_OP_REAL: return launch_tc<tk::OP_REAL>(prm, dense, s);
     case TK_OP_COMPLEX: return launch_tc<tk::OP_COMPLEX>(prm, dense, s);
+    case tk::OP_SPLIT: return launch_tc<tk::OP_SPLIT>(prm, dense, s);
     default: return launch_tc<tk::OP_DUAL>(prm, dense, s);
   }
 }

@@ -3,10 +3,9 @@
 //     reaches the tensor cores through plain 2-D TMA maps (the paper's "interleaved global,
 //     split shared" composition, reference api.py:243-250).  TMA cannot stride dimension 0,
 //     so the de-interleave cannot be folded into the tensor map itself.
-//   * sum_rows / sum_cols: row sums of A and column sums of B; with them an affine operand
-//     transform T(x) = alpha*x + beta on the A/B streams (add_constant / scale,
-//     components.py:60-78) is applied exactly in the epilogue:
-//       sum_k Ta(A_ik) Tb(B_kj) = aa*ab*S_ij + aa*bb*R_i + ba*ab*Q_j + K*ba*bb
+//   * transform_split: the g2s_a / g2s_b load transforms (reference kernel.py:406-418,
+//     components.py:52-94) applied once per operand element in FP32, written as fp16 hi + lo
+//     planes for the tensor cores (see the kernel).
 #pragma once
 #include "tk_types.cuh"
 
@@ -43,34 +42,55 @@ __device__ __forceinline__ float h2f<__half>(__half v) { return __half2float(v);
 template <>
 __device__ __forceinline__ float h2f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
 
-// out[i] = sum_t X[i*s_outer + t*s_inner], t < len; one warp per output, lanes stride t.
-template <typename H>
-__global__ void strided_sum_kernel(const H* __restrict__ x, float* __restrict__ out, int64_t count,
-                                   int64_t len, int64_t s_outer, int64_t s_inner) {
-  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (warp >= count) return;
-  const H* row = x + warp * s_outer;
-  float acc = 0.f;
-  for (int64_t t = lane; t < len; t += 32) acc += h2f(row[t * s_inner]);
+// Operand load transform, the faithful form of the reference's per-element g2s transform:
+// s = t(x) is evaluated in FP32 with the reference's operation order (run_prog_real: numpy's
+// f32 arithmetic on the f32-widened operand), then split into hi = fp16(s) and
+// lo = fp16(s - hi), so hi + lo carries s to ~2^-22 relative and the tensor cores form
+// s_a * s_b as hi*hi + hi*lo + lo*hi in FP32 accumulators (lo*lo, < 2^-22, is dropped).
+// With SPLIT = false only hi is written (transforms exact in fp16: relu, scale by +-1).
+// The operand is a rows x cols matrix with the `fast` dimension contiguous (pitch = the
+// stride of the other one); the planes are written dense in the same orientation.
+// flag |= 1 when some lo is non-zero: the GEMM skips the lo loads and MMAs otherwise.
+template <bool SPLIT>
+__global__ void __launch_bounds__(256) transform_split_kernel(const __half* __restrict__ src, __half* __restrict__ hi,
+                                                              __half* __restrict__ lo, int64_t fast, int64_t slow,
+                                                              int64_t pitch, const __grid_constant__ EpiProg g,
+                                                              int32_t* __restrict__ flag) {
+  const int64_t total = fast * slow;
+  const bool vec = (fast % 8) == 0 && (pitch % 8) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+  bool nz = false;
+  auto one = [&](float x, __half& h, __half& l) {
+    const float v = run_prog_real(g, x);
+    h = __float2half_rn(v);
+    if (SPLIT) {
+      l = __float2half_rn(v - __half2float(h));
+      nz |= __half2float(l) != 0.f;
+    }
+  };
+  const int64_t step = int64_t(gridDim.x) * blockDim.x;
+  if (vec) {
+    for (int64_t e8 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e8 < total / 8; e8 += step) {
+      const int64_t e = e8 * 8, r = e % fast, c = e / fast;
+      const uint4 v = __ldcs(reinterpret_cast<const uint4*>(src + c * pitch + r));
+      const __half* x = reinterpret_cast<const __half*>(&v);
+      uint4 vh, vl;
+      __half* h = reinterpret_cast<__half*>(&vh);
+      __half* l = reinterpret_cast<__half*>(&vl);
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) out[warp] = acc;
-}
-
-// out[i] += sum_{t in slice} X[i + t*s_inner] for unit-stride outputs: threads along i
-// (coalesced), blockIdx.y splits t so the grid covers the GPU; out must be zeroed first.
-template <typename H>
-__global__ void strided_sum_unit_kernel(const H* __restrict__ x, float* __restrict__ out,
-                                        int64_t count, int64_t len, int64_t s_inner) {
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= count) return;
-  const int64_t per = (len + gridDim.y - 1) / gridDim.y;
-  const int64_t t0 = int64_t(blockIdx.y) * per, t1 = min(len, t0 + per);
-  float acc = 0.f;
-#pragma unroll 8
-  for (int64_t t = t0; t < t1; ++t) acc += h2f(x[i + t * s_inner]);
-  atomicAdd(out + i, acc);
+      for (int q = 0; q < 8; ++q) one(__half2float(x[q]), h[q], l[q]);
+      *reinterpret_cast<uint4*>(hi + e) = vh;
+      if (SPLIT) *reinterpret_cast<uint4*>(lo + e) = vl;
+    }
+  } else {
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += step) {
+      const int64_t r = e % fast, c = e / fast;
+      __half h, l;
+      one(__half2float(src[c * pitch + r]), h, l);
+      hi[e] = h;
+      if (SPLIT) lo[e] = l;
+    }
+  }
+  if (SPLIT && __syncthreads_or(nz) && threadIdx.x == 0) atomicOr(flag, 1);
 }
 
 }  // namespace tk

@@ -42,6 +42,8 @@ template <>
 struct TcCfg<OP_DUAL> {
   static constexpr int PLANES = 2, BN = 128, STAGES = 3, ACC_COLS = 256, TMEM_COLS = 512;
 };
+template <>
+struct TcCfg<OP_SPLIT> : TcCfg<OP_DUAL> {};
 
 // C-streaming variants: a per-epilogue-warp ring of TMA-loaded C boxes (32 rows x 32 columns
 // fp32), refilled by the loader warp.  CS = 1 (HBM-bound shapes: diagonal A, K <= 256):
@@ -85,10 +87,9 @@ struct TcParams {
   const float* bias;
   DigitMap c_map, d_map;
   int64_t c_plane, d_plane;
-  int32_t affine, pad0;
-  float aff_s, aff_r, aff_q, aff_k;
-  const float* rowsum_a;
-  const float* colsum_b;
+  // OP_SPLIT: split_flags[0] / [1] != 0 when A / B has a non-zero lo plane (written by the
+  // transform pass); a zero lo plane is neither loaded nor multiplied
+  const int32_t* split_flags;
   EpiProg t_c, t_r2s, t_s2g;
   // dense column-major epilogue: transforms pre-decoded to relu?(x*mul + add) (complex mul/add
   // for pair operators); see decode_affine() in tk_api.cu
@@ -205,24 +206,19 @@ __device__ __forceinline__ void sk_gather(const SkIn& sk, int col, float (&pv)[3
 __device__ __forceinline__ float relu_if(float v, int on) { return on ? np_relu(v) : v; }
 
 // The fused real epilogue on one 32-column chunk (row = lane), in the reference's order
-// (components.py:110-157): v = acc [+ split-K partials]; affine operand terms; + t_c(C);
-// r2s; + bias; s2g.  Uniform decisions are taken once per chunk (a branch around every
-// element's shuffle costs ~1 us per chunk), the per-element arithmetic is unchanged.
+// (components.py:110-157): v = acc [+ split-K partials]; + t_c(C); r2s; + bias; s2g.
+// Uniform decisions are taken once per chunk (a branch around every element's shuffle costs
+// ~1 us per chunk), the per-element arithmetic is unchanged.
 template <bool SK>
 __device__ __forceinline__ void epi_math_real(const TcParams& p, const uint32_t (&r)[32],
                                               const float (&cv)[32], const float (&pv)[SK ? 32 : 1],
-                                              bool has_c, float rterm, float bias_m, float bcol,
-                                              float qcol, float (&out)[32]) {
+                                              bool has_c, float bias_m, float bcol, float (&out)[32]) {
   float v[32];
 #pragma unroll
   for (int jj = 0; jj < 32; ++jj) v[jj] = __uint_as_float(r[jj]);
   if constexpr (SK) {
 #pragma unroll
     for (int jj = 0; jj < 32; ++jj) v[jj] = pv[jj] + v[jj];
-  }
-  if (p.affine) {
-#pragma unroll
-    for (int jj = 0; jj < 32; ++jj) v[jj] = p.aff_s * v[jj] + (rterm + __shfl_sync(0xffffffffu, qcol, jj));
   }
   if (has_c) {
     if (p.c_ident) {  // identity g2s_c (the reference's default): acc starts from C itself
@@ -265,18 +261,31 @@ __device__ __forceinline__ void epi_math_real(const TcParams& p, const uint32_t 
 // per lane, TMEM lane quarter) x COLS columns in chunks of 32; C for the next chunk is in
 // flight while the current chunk computes and stores (streaming cache hints: C and D are
 // touched once and must not evict the A/B panels from L2).
+// OP_SPLIT: the second accumulator (BN columns on) is added to the first when `eps` is set.
+template <int OP, int BN>
+__device__ __forceinline__ void split_sum(uint32_t (&r)[32], uint32_t taddr, bool eps) {
+  if constexpr (OP == OP_SPLIT) {
+    if (eps) {
+      uint32_t r1[32];
+      tmem_ld_32x32b_x32(taddr + uint32_t(BN), r1);
+      tmem_ld_wait();
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) r[jj] = __float_as_uint(__uint_as_float(r[jj]) + __uint_as_float(r1[jj]));
+    }
+  }
+}
+
 template <int OP, int COLS, int BN, bool SK = false>
 __device__ __forceinline__ void epilogue_dense(const TcParams& p, uint64_t* tfull, uint32_t aphase,
                                                uint32_t tbase, int i, int jbase, int lane,
-                                               SkIn sk = SkIn{nullptr, 0, 0}) {
+                                               SkIn sk = SkIn{nullptr, 0, 0}, bool eps = false) {
   const bool row_ok = i < p.m;
   const bool has_c = !p.c_zero;
-  if (OP == OP_REAL) {
+  if (OP == OP_REAL || OP == OP_SPLIT) {
     const int64_t crow = !row_ok ? 0 : p.c_rmap ? map_dim(p.c_map, 0, i) : i;
     const int64_t drow = !row_ok ? 0 : p.d_rmap ? map_dim(p.d_map, 0, i) : i;
     const float* cp = reinterpret_cast<const float*>(p.c_ptr) + crow;
     float* dp = reinterpret_cast<float*>(p.d_ptr) + drow;
-    const float rterm = p.affine && row_ok ? (p.aff_r * (p.rowsum_a ? p.rowsum_a[i] : 0.f) + p.aff_k) : 0.f;
     const float bias_m = (p.bias_axis == 2 && row_ok) ? p.bias[i] : 0.f;
     float cv[32];
     auto load_c = [&](int j0) {
@@ -293,16 +302,17 @@ __device__ __forceinline__ void epilogue_dense(const TcParams& p, uint64_t* tful
     for (int ch = 0; ch < COLS / 32; ++ch) {
       const int j0 = jbase + ch * 32;
       uint32_t r[32];
-      tmem_ld_32x32b_x32(tbase + uint32_t(j0 - jbase + (jbase % BN)), r);
-      // lane-distributed column vectors (bias[j], colsum_b[j]) broadcast with shuffles
+      const uint32_t taddr = tbase + uint32_t(j0 - jbase + (jbase % BN));
+      tmem_ld_32x32b_x32(taddr, r);
+      // lane-distributed bias[j] broadcast with shuffles
       const int jl = j0 + lane;
       const float bcol = (p.bias_axis == 1 && jl < p.n) ? p.bias[jl] : 0.f;
-      const float qcol = (p.affine && p.colsum_b && jl < p.n) ? p.aff_q * p.colsum_b[jl] : 0.f;
       float pv[SK ? 32 : 1];
       if constexpr (SK) sk_gather(sk, j0 - jbase + (jbase % BN), pv);
       tmem_ld_wait();
+      split_sum<OP, BN>(r, taddr, eps);
       float out[32];
-      epi_math_real<SK>(p, r, cv, pv, has_c, rterm, bias_m, bcol, qcol, out);
+      epi_math_real<SK>(p, r, cv, pv, has_c, bias_m, bcol, out);
       if (ch + 1 < COLS / 32) load_c(j0 + 32);
       if (row_ok) {
 #pragma unroll
@@ -411,7 +421,6 @@ __device__ __forceinline__ void epilogue_stream(const TcParams& p, uint64_t* tfu
   const bool row_ok = i < p.m;
   const bool has_c = !p.c_zero;
   float* dp = reinterpret_cast<float*>(p.d_ptr) + (row_ok ? i : 0);
-  const float rterm = p.affine && row_ok ? (p.aff_r * (p.rowsum_a ? p.rowsum_a[i] : 0.f) + p.aff_k) : 0.f;
   const float bias_m = (p.bias_axis == 2 && row_ok) ? p.bias[i] : 0.f;
   mbar_wait_sleep(tfull, aphase);
   tc_fence_after();
@@ -422,7 +431,6 @@ __device__ __forceinline__ void epilogue_stream(const TcParams& p, uint64_t* tfu
     tmem_ld_32x32b_x32(tbase + uint32_t(j0 - jbase + (jbase % BN)), r);
     const int jl = j0 + lane;
     const float bcol = (p.bias_axis == 1 && jl < p.n) ? p.bias[jl] : 0.f;
-    const float qcol = (p.affine && p.colsum_b && jl < p.n) ? p.aff_q * p.colsum_b[jl] : 0.f;
     float pv[SK ? 32 : 1];
     if constexpr (SK) {
       if (p.sk_tma) {
@@ -462,7 +470,7 @@ __device__ __forceinline__ void epilogue_stream(const TcParams& p, uint64_t* tfu
     tmem_ld_wait();
     if (ch == 0) TK_TS_EPI(8);
     float out[32];
-    epi_math_real<SK>(p, r, cv, pv, has_c, rterm, bias_m, bcol, qcol, out);
+    epi_math_real<SK>(p, r, cv, pv, has_c, bias_m, bcol, out);
     if (ch == 0) TK_TS_EPI(9);
     if (p.d_tma) {
 #pragma unroll
@@ -506,11 +514,10 @@ __device__ __forceinline__ void epilogue_stream(const TcParams& p, uint64_t* tfu
 // Any digit-mapped C/D layout and any transform program (the rare path).
 template <int OP, int COLS, int BN>
 __device__ __noinline__ void epilogue_generic(const TcParams& p, uint64_t* tfull, uint32_t aphase,
-                                              uint32_t tbase, int i, int jbase) {
+                                              uint32_t tbase, int i, int jbase, bool eps = false) {
   const bool row_ok = i < p.m;
   const int64_t c_row = row_ok ? map_dim(p.c_map, 0, i) : 0;
   const int64_t d_row = row_ok ? map_dim(p.d_map, 0, i) : 0;
-  const float rsum = (p.affine && row_ok && p.rowsum_a) ? p.rowsum_a[i] : 0.f;
   const float bias_m = (p.bias_axis == 2 && row_ok) ? p.bias[i] : 0.f;
   mbar_wait_sleep(tfull, aphase);
   tc_fence_after();
@@ -520,16 +527,15 @@ __device__ __noinline__ void epilogue_generic(const TcParams& p, uint64_t* tfull
     const uint32_t col = uint32_t(j0 - jbase + (jbase % BN));
     uint32_t r0[32], r1[32];
     tmem_ld_32x32b_x32(tbase + col, r0);
-    if (OP != OP_REAL) tmem_ld_32x32b_x32(tbase + uint32_t(BN) + col, r1);
+    if (OP == OP_COMPLEX || OP == OP_DUAL) tmem_ld_32x32b_x32(tbase + uint32_t(BN) + col, r1);
     tmem_ld_wait();
+    split_sum<OP, BN>(r0, tbase + col, eps);
 #pragma unroll 1
     for (int jj = 0; jj < 32; ++jj) {
       const int j = j0 + jj;
       if (!row_ok || j >= p.n) continue;
-      if (OP == OP_REAL) {
+      if (OP == OP_REAL || OP == OP_SPLIT) {
         float v = __uint_as_float(r0[jj]);
-        if (p.affine)
-          v = p.aff_s * v + p.aff_r * rsum + (p.colsum_b ? p.aff_q * p.colsum_b[j] : 0.f) + p.aff_k;
         if (!p.c_zero) v = run_prog_real(p.t_c, load_scalar_f32(p.c_ptr, c_row + map_dim(p.c_map, 1, j))) + v;
         v = run_prog_real(p.t_r2s, v);
         if (p.bias_axis == 1) v = v + p.bias[j];
@@ -605,6 +611,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(const __grid_con
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // OP_SPLIT: which lo planes are non-zero (the others are neither loaded nor multiplied)
+  const bool lo_a = OP != OP_SPLIT || p.split_flags[0] != 0;
+  const bool lo_b = OP != OP_SPLIT || p.split_flags[1] != 0;
 
   auto a_tile = [&](int s, int plane) -> uint8_t* {
     return smem + s * S::STAGE_BYTES + plane * TC_A_TILE_BYTES;
@@ -617,8 +626,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(const __grid_con
     // ------------------------------------------------------------ producer
     const uint64_t pol_a = p.pol_ab ? policy_evict_last() : policy_evict_normal();
     const uint64_t pol_b = pol_a;
-    const uint32_t a_bytes = p.diag_a ? 0u : uint32_t(TC_A_TILE_BYTES * C::PLANES);
-    const uint32_t tx_bytes = a_bytes + uint32_t(S::B_TILE_BYTES * C::PLANES);
+    const uint32_t a_bytes = p.diag_a ? 0u : uint32_t(TC_A_TILE_BYTES * (C::PLANES == 1 ? 1 : 1 + lo_a));
+    const uint32_t tx_bytes = a_bytes + uint32_t(S::B_TILE_BYTES * (C::PLANES == 1 ? 1 : 1 + lo_b));
     int stage = 0;
     uint32_t phase = 0;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
@@ -643,7 +652,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(const __grid_con
           mbar_arrive_expect_tx(&full[stage], tx_bytes);
 #pragma unroll
           for (int pl = 0; pl < C::PLANES; ++pl) {
-            if (!p.diag_a) {
+            if (!p.diag_a && (pl == 0 || lo_a)) {
               if (p.a_mn) {  // column-major A: two 64-row boxes (M inner)
                 tma_load_2d(a_tile(stage, pl), &p.ta[pl], &full[stage], m0, k0, pol_a);
                 tma_load_2d(a_tile(stage, pl) + 8192, &p.ta[pl], &full[stage], m0 + 64, k0, pol_a);
@@ -651,7 +660,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(const __grid_con
                 tma_load_2d(a_tile(stage, pl), &p.ta[pl], &full[stage], k0, m0, pol_a);
               }
             }
-            if (p.b_mn) {    // row-major B: BN/64 boxes, N inner
+            if (pl == 1 && !lo_b) {
+              // (OP_SPLIT) zero lo plane of B: not loaded
+            } else if (p.b_mn) {    // row-major B: BN/64 boxes, N inner
 #pragma unroll
               for (int h = 0; h < BN / 64; ++h)
                 tma_load_2d(b_tile(stage, pl) + h * 8192, &p.tb[pl], &full[stage], n0 + 64 * h, k0,
@@ -715,10 +726,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(const __grid_con
                 tc_mma_f16(d0, a1, b1, idesc_neg, 1u);   // Re += (-Ai)*Bi
                 tc_mma_f16(d1, a0, b1, idesc, acc);      // Im += Ar*Bi
                 tc_mma_f16(d1, a1, b0, idesc, 1u);       // Im += Ai*Br
-              } else {
+              } else if (OP == OP_DUAL) {
                 tc_mma_f16(d0, a0, b0, idesc, acc);      // v   += Av*Bv
                 tc_mma_f16(d1, a0, b1, idesc, acc);      // eps += Av*Beps
                 tc_mma_f16(d1, a1, b0, idesc, 1u);       // eps += Aeps*Bv
+              } else {                                   // OP_SPLIT
+                tc_mma_f16(d0, a0, b0, idesc, acc);      // hi*hi
+                if (lo_b) tc_mma_f16(d1, a0, b1, idesc, acc);            // hi*lo
+                if (lo_a) tc_mma_f16(d1, a1, b0, idesc, lo_b ? 1u : acc);  // lo*hi
               }
             }
           }
@@ -773,9 +788,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(const __grid_con
                                            cfull + ew * S::CSLOTS, cempty + ew * S::CSLOTS, cq,
                                            mb * TC_BM + quarter * 32);
       else if (DENSE_EPI)
-        epilogue_dense<OP, COLS_PER_WARP, BN>(p, tfull + as, aphase, tbase, i, jbase, lane);
+        epilogue_dense<OP, COLS_PER_WARP, BN>(p, tfull + as, aphase, tbase, i, jbase, lane,
+                                              SkIn{nullptr, 0, 0}, lo_a || lo_b);
       else
-        epilogue_generic<OP, COLS_PER_WARP, BN>(p, tfull + as, aphase, tbase, i, jbase);
+        epilogue_generic<OP, COLS_PER_WARP, BN>(p, tfull + as, aphase, tbase, i, jbase, lo_a || lo_b);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[as]);

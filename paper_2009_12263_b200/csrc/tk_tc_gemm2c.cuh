@@ -89,6 +89,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
   }
+  // OP_SPLIT: which lo planes are non-zero (read after the wait: the transform pass wrote them)
+  const bool lo_a = OP != OP_SPLIT || p.split_flags[0] != 0;
+  const bool lo_b = OP != OP_SPLIT || p.split_flags[1] != 0;
 
   auto a_tile = [&](int s, int pl) -> uint8_t* { return smem + s * PL::STAGE_BYTES + pl * TC2C_A_BYTES; };
   auto b_tile = [&](int s, int pl) -> uint8_t* {
@@ -111,11 +114,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           const int kb = rev ? p.kb_total - 1 - ki : ki;
           const int k0 = kb * TC_BK;
           mbar_wait(&empty[stage], phase ^ 1);
-          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * PL::STAGE_BYTES);
+          if (leader)
+            mbar_arrive_expect_tx(&full[stage], 2 * ((1 + lo_a) * TC2C_A_BYTES + (1 + lo_b) * PL::B_BYTES));
           const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
 #pragma unroll
           for (int pl = 0; pl < 2; ++pl) {
-            if (p.a_mn && (p.mn3d & 1)) {
+            if (pl == 1 && !lo_a) {
+              // (OP_SPLIT) zero lo plane of A: not loaded
+            } else if (p.a_mn && (p.mn3d & 1)) {
               tma_load_3d_pair(a_tile(stage, pl), &p.ta[pl], fb, 0, k0, m0 >> 6, pol);
             } else if (p.a_mn) {
               tma_load_2d_pair(a_tile(stage, pl), &p.ta[pl], fb, m0, k0, pol);
@@ -123,7 +129,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
             } else {
               tma_load_2d_pair(a_tile(stage, pl), &p.ta[pl], fb, k0, m0, pol);
             }
-            if (p.b_mn) {  // 64-column MN-major atoms
+            if (pl == 1 && !lo_b) {
+              // (OP_SPLIT) zero lo plane of B: not loaded
+            } else if (p.b_mn) {  // 64-column MN-major atoms
               for (int h = 0; h < BN / 128; ++h)
                 tma_load_2d_pair(b_tile(stage, pl) + h * 8192, &p.tb[pl], fb, n0 + 64 * h, k0, pol);
             } else {
@@ -167,10 +175,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
               tc_mma_f16_pair(d0, a1, b1, idesc_neg, 1u);
               tc_mma_f16_pair(d1, a0, b1, idesc, acc);
               tc_mma_f16_pair(d1, a1, b0, idesc, 1u);
-            } else {
+            } else if (OP == OP_DUAL) {
               tc_mma_f16_pair(d0, a0, b0, idesc, acc);
               tc_mma_f16_pair(d1, a0, b1, idesc, acc);
               tc_mma_f16_pair(d1, a1, b0, idesc, 1u);
+            } else {  // OP_SPLIT: hi*hi, hi*lo, lo*hi
+              tc_mma_f16_pair(d0, a0, b0, idesc, acc);
+              if (lo_b) tc_mma_f16_pair(d1, a0, b1, idesc, acc);
+              if (lo_a) tc_mma_f16_pair(d1, a1, b0, idesc, lo_b ? 1u : acc);
             }
           }
           tc_commit_pair(&empty[stage], 0x3);
@@ -197,9 +209,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         mbar_wait_sleep(tfull + as, aphase);
         tc_fence_after();
       } else if (DENSE_EPI)
-        epilogue_dense<OP, BN / 2, BN>(p, tfull + as, aphase, tbase, i, jbase, lane);
+        epilogue_dense<OP, BN / 2, BN>(p, tfull + as, aphase, tbase, i, jbase, lane, SkIn{nullptr, 0, 0},
+                                       lo_a || lo_b);
       else
-        epilogue_generic<OP, BN / 2, BN>(p, tfull + as, aphase, tbase, i, jbase);
+        epilogue_generic<OP, BN / 2, BN>(p, tfull + as, aphase, tbase, i, jbase, lo_a || lo_b);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[as]), 0));

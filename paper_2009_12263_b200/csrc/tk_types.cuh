@@ -7,7 +7,10 @@
 
 namespace tk {
 
-enum { OP_REAL = 0, OP_COMPLEX = 1, OP_DUAL = 2 };
+// OP_SPLIT (internal): a real GEMM whose transformed fp16 operands arrive as hi + lo planes
+// (x = hi + lo, see transform_split_kernel); 3 MMAs per step (hi*hi, hi*lo, lo*hi) into two
+// FP32 accumulators that the real epilogue sums.
+enum { OP_REAL = 0, OP_COMPLEX = 1, OP_DUAL = 2, OP_SPLIT = 3 };
 enum { S_F16 = 0, S_BF16 = 1, S_F32 = 2, S_F64 = 3 };
 enum { L_STRIDED = 0, L_DIAGONAL = 1, L_ZERO = 2 };
 enum { P_NONE = 0, P_INTERLEAVED = 1, P_SPLIT = 2 };

@@ -431,10 +431,17 @@ def test_lane_selection_variants():
     assert lanes == {"complex16": "tcgen05", "complex16_split": "tcgen05", "dual16": "tcgen05",
                      "diag16": "tcgen05", "fused16": "tcgen05", "complex64": "simt",
                      "tc16": "tcgen05"}
-    # a relu on the A stream is not affine: the exact lane runs it
-    cfg = dataclasses.replace(tk.build_dense_config(256, 256, 64, np.float16),
-                              transform_g2s_a=components.relu)
-    assert kernel.plan_lane(kernel.lower(kernel.resolve_config(cfg))[0]) == "simt"
+    # any A/B load transform runs on the tensor cores through the transform pass (fp16: hi +
+    # lo planes when the result is not exact in fp16) ...
+    prog = components.compose(components.scale(0.3), components.relu, components.add_constant(0.1))
+    for t in (components.relu, prog):
+        cfg = dataclasses.replace(tk.build_dense_config(256, 256, 64, np.float16),
+                                  transform_g2s_a=t, transform_g2s_b=components.relu)
+        assert kernel.plan_lane(kernel.lower(kernel.resolve_config(cfg))[0]) == "tcgen05"
+    # ... bf16 only when the result is exact in bf16 (else it would need three planes)
+    for t, lane in ((components.relu, "tcgen05"), (prog, "simt")):
+        cfg = dataclasses.replace(tk.build_dense_config(256, 256, 64, tk.BFLOAT16), transform_g2s_b=t)
+        assert kernel.plan_lane(kernel.lower(kernel.resolve_config(cfg))[0]) == lane
     with tk.force_lane("simt"):
         plan, _, _ = kernel.lower(kernel.resolve_config(tk.build_dense_config(256, 256, 64,
                                                                               np.float16)))
