@@ -106,8 +106,8 @@ int tk_abi_version(void);
 int tk_plan_lane(const TkGemmPlan* plan);
 
 /* Device workspace (bytes) tk_gemm needs for this plan (de-interleave planes, gathered
- * GETT operands, row/column sums of affine operand transforms, split-K partials and their
- * counters).  Caller allocates it. */
+ * GETT operands, transformed operand planes of g2s_a / g2s_b programs, split-K partials and
+ * their counters).  Caller allocates it. */
 int64_t tk_workspace_bytes(const TkGemmPlan* plan);
 
 /* Execute one GEMM (replaces kernel.gemm_execute, kernel.py:253-330).
@@ -181,7 +181,7 @@ typedef struct TkPlanInfo {
   int32_t sk_parts, sk_tiles, sk_tma;
   int32_t serpentine, group_m, pdl, c_stream, d_tma;
   int32_t launches;         /* device kernels of the call (prep passes included) */
-  int32_t reserved;
+  int32_t overlap_kb;       /* pair kernel, 256 x 512 tiles: lo-only / hi-only k-blocks per tile end */
   int64_t workspace_bytes;
 } TkPlanInfo;
 

@@ -114,6 +114,43 @@ def c1_cases():
          a=a, b=b, c=c, d=d.reshape((m, n), order="F"))
 
 
+def padded_cases():
+    """Padded layouts (reference layouts.py:132-188, builder 414-418): padded SHARED staging
+    (build_dense_config(shared_pad=...): the heuristic sees the padded footprint) and padded
+    GLOBAL A / B / C / D buffers (physical size (rows + pad) * cols, padding never observed)."""
+    from tilekit import layouts as L
+
+    rng = np.random.default_rng(414)
+    m, n, k = 128, 192, 96
+    a = rng.standard_normal((m, k)).astype(np.float16).astype(np.float32)
+    b = rng.standard_normal((k, n)).astype(np.float16).astype(np.float32)
+    c = rng.standard_normal((m, n)).astype(np.float32)
+    cfg = tk.build_dense_config(m, n, k, np.float32, shared_pad=4)
+    d = np.zeros(m * n, np.float32)
+    cnt = tk.matmul(cfg, a.ravel(order="F"), b.ravel(order="F"), c.ravel(order="F"), d)
+    res = tk.kernel.resolve_config(cfg)
+    save("padded_shared", {"m": m, "n": n, "k": k, "pad": 4, "counters": counters_dict(cnt),
+                           "block_tile": list(res.params.block_tile)},
+         a=a, b=b, c=c, d=d.reshape((m, n), order="F"))
+    pads = {"A": 8, "B": 3, "C": 4, "D": 5}
+    cfg = dataclasses.replace(
+        tk.build_dense_config(m, n, k, np.float32),
+        global_a_layout=L.Padded(L.ColMajor(np.float32, ("M", "K"), (m, k)), pads["A"]),
+        global_b_layout=L.Padded(L.ColMajor(np.float32, ("K", "N"), (k, n)), pads["B"]),
+        global_c_layout=L.Padded(L.ColMajor(np.float32, ("M", "N"), (m, n)), pads["C"]),
+        global_d_layout=L.Padded(L.ColMajor(np.float32, ("M", "N"), (m, n)), pads["D"]))
+
+    def pad_buf(x, p):
+        buf = np.full((x.shape[0] + p, x.shape[1]), -7.0, np.float32)
+        buf[:x.shape[0]] = x
+        return buf.ravel(order="F")
+
+    dbuf = np.full((m + pads["D"]) * n, 123.0, np.float32)
+    cnt = tk.matmul(cfg, pad_buf(a, pads["A"]), pad_buf(b, pads["B"]), pad_buf(c, pads["C"]), dbuf)
+    save("padded_global", {"m": m, "n": n, "k": k, "pads": pads, "counters": counters_dict(cnt)},
+         a=a, b=b, c=c, d_buf=dbuf)
+
+
 def fused_cases():
     rng = np.random.default_rng(12)
     m, n, k = 128, 96, 64
@@ -293,7 +330,7 @@ def host_logic_cases():
 
 if __name__ == "__main__":
     print("reference lane:", tk.active_lane())
-    which = sys.argv[1:] or ["dense", "c1", "fused", "pair", "variant", "gett", "host_logic"]
+    which = sys.argv[1:] or ["dense", "c1", "padded", "fused", "pair", "variant", "gett", "host_logic"]
     for name in which:
         globals()[f"{name}_cases"]()
     print("wrote", sorted(os.listdir(OUT)))

@@ -59,7 +59,7 @@ class TkPlanInfo(ctypes.Structure):
         "lane", "op", "tile_m", "tile_n", "tile_k", "mma_n", "nsub", "mmas_per_k16", "cluster",
         "stages", "stage_bytes", "cring_bytes", "smem_bytes", "tmem_cols", "grid_ctas", "tiles",
         "units", "sk_parts", "sk_tiles", "sk_tma", "serpentine", "group_m", "pdl", "c_stream",
-        "d_tma", "launches", "reserved")] + [("workspace_bytes", c_int64)]
+        "d_tma", "launches", "overlap_kb")] + [("workspace_bytes", c_int64)]
 
 
 GEMM_EX_ARGTYPES = [c_int, c_int, c_int, c_longlong, c_longlong, c_longlong, c_double,
@@ -135,7 +135,7 @@ def plan_info() -> dict:
     """The on-chip plan of the last GEMM on this thread (tk_last_plan_info) as a dict."""
     info = TkPlanInfo()
     load().tk_last_plan_info(ctypes.byref(info))
-    out = {f: getattr(info, f) for f, _ in TkPlanInfo._fields_ if f != "reserved"}
+    out = {f: getattr(info, f) for f, _ in TkPlanInfo._fields_}
     out["kernel"] = info.kernel.decode()
     return out
 

@@ -62,6 +62,7 @@ enum Knob {
   K_SPLITK_S, K_SK_TMA, K_PDL, K_MN3D, K_PAIR_CSTREAM, K_PAIR_DTMA, K_C_PF, K_C_PF_SPREAD,
   K_NSUB2_CSL, K_STAGGER, K_PAIR_GRID, K_PAIR_DEEPC, K_PAIROPS_BN, K_DIAG_STREAM, K_D_TMA,
   K_L2_PROMO, K_POLICY_AB, K_POL_A, K_POL_B, K_PAIR_CLUSTERS, K_EX_SLABS, K_VERBOSE,
+  K_NSUB2_OVERLAP,
   K_DBG_C_ZERO, K_DBG_SKIP_EPI, K_DBG_NO_LOAD, K_DBG_NO_MMA, K_DBG_CTA, K_COUNT
 };
 constexpr int K_FIRST_DIAG = K_DBG_C_ZERO;
@@ -70,7 +71,7 @@ const char* const kKnobNames[K_COUNT] = {
   "TK_SPLITK_MINKB", "TK_SPLITK_S", "TK_SK_TMA", "TK_PDL", "TK_MN3D", "TK_PAIR_CSTREAM",
   "TK_PAIR_DTMA", "TK_C_PF", "TK_C_PF_SPREAD", "TK_NSUB2_CSL", "TK_STAGGER", "TK_PAIR_GRID",
   "TK_PAIR_DEEPC", "TK_PAIROPS_BN", "TK_DIAG_STREAM", "TK_D_TMA", "TK_L2_PROMO", "TK_POLICY_AB",
-  "TK_POL_A", "TK_POL_B", "TK_PAIR_CLUSTERS", "TK_EX_SLABS", "TK_VERBOSE",
+  "TK_POL_A", "TK_POL_B", "TK_PAIR_CLUSTERS", "TK_EX_SLABS", "TK_VERBOSE", "TK_NSUB2_OVERLAP",
   "TK_DBG_C_ZERO", "TK_DBG_SKIP_EPI", "TK_DBG_NO_LOAD", "TK_DBG_NO_MMA", "TK_DBG_CTA"};
 #ifdef TK_DIAG
 constexpr int K_ENABLED = K_COUNT;
@@ -321,6 +322,29 @@ bool permuted_plan(const TkGemmPlan* p, TkGemmPlan* out) {
   return true;
 }
 
+// A block predicate the tensor-core lane evaluates itself: a host-evaluated mask, or the diagonal
+// rule over a dense A (a Diagonal A layout instead restricts the k range in its own kernels).
+bool pred_on_tc(const TkGemmPlan* p) {
+  return p->predicate == TK_PRED_MASK || (p->predicate == TK_PRED_DIAGONAL && p->a.kind != TK_LAYOUT_DIAGONAL);
+}
+
+// Instruction N of the CTA-pair kernel for a predicated plan: every 256 x BNI tile must lie in one
+// reference block (bm % 256, bn % BNI) and each K=16 MMA step in one block-K chunk (bk % 16);
+// 0 when no tile shape fits (the exact lane then runs the predicate).
+int pred_bni(const TkGemmPlan* p, std::string* why = nullptr) {
+  auto no = [&](const char* w) { if (why) *why = w; return 0; };
+  if (p->op != TK_OP_REAL || p->t_a.n || p->t_b.n) return no("block predicates on the tensor cores: real operator, no A/B transforms");
+  if (p->block[2] % 16) return no("block predicate with bk % 16 != 0 (an MMA step would straddle two block-K chunks)");
+  if (p->block[0] % 256) return no("block predicate with bm % 256 != 0 (a 256-row pair tile would straddle blocks)");
+  if (p->m <= 128 || (p->k + 63) / 64 <= 4) return no("block predicate on a shape below the CTA-pair kernel");
+  int mn = 1;
+  int64_t pitch;
+  const bool b_mn = tma_operand(p->b, mn, pitch) ? !mn : false;  // a gathered B is K-major
+  for (int bni : {256, 128, 64})
+    if (p->block[1] % bni == 0 && !(bni == 64 && b_mn)) return bni;
+  return no("block predicate with bn not a multiple of the pair tile width");
+}
+
 bool tc_lane_ok(const TkGemmPlan* p, std::string& why) {
   TkGemmPlan rewritten;
   if (permuted_plan(p, &rewritten)) return tc_lane_ok(&rewritten, why);
@@ -345,9 +369,7 @@ bool tc_lane_ok(const TkGemmPlan* p, std::string& why) {
   // would need three planes for the reference's f32 transform result, so only exact programs
   if (p->a.scalar == TK_BF16 && !(half_exact(p->t_a) && half_exact(p->t_b)))
     return no("bf16 operand transforms beyond relu / scale(+-1) run on the exact lane");
-  if (p->predicate == TK_PRED_MASK) return no("arbitrary predicates run on the exact lane");
-  if (p->predicate == TK_PRED_DIAGONAL && p->a.kind != TK_LAYOUT_DIAGONAL)
-    return no("diagonal predicate over a dense A runs on the exact lane");
+  if (pred_on_tc(p) && !pred_bni(p, &why)) return false;
   if (p->bias_axis && p->bias_scalar != TK_F32) return no("bias must be f32");
   if (p->m >= (1ll << 31) || p->n >= (1ll << 31) || p->k >= (1ll << 31)) return no("extent >= 2^31");
   return true;
@@ -365,7 +387,7 @@ int choose_lane(const TkGemmPlan* p, std::string* why_out = nullptr) {
 // ------------------------------------------------------------------ workspace plan
 struct Workspace {
   int64_t a_planes = -1, b_planes = -1, a_perm = -1, a_pack = -1, b_pack = -1, splitk = -1,
-          a_tx = -1, b_tx = -1, tx_flags = -1, total = 0;
+          a_tx = -1, b_tx = -1, tx_flags = -1, kbits = -1, total = 0;
   bool tx_split = false;  // transformed operands carry hi + lo planes (OP_SPLIT)
 };
 
@@ -416,7 +438,12 @@ Workspace plan_workspace(const TkGemmPlan* p0, int lane) {
     w.tx_flags = w.total;
     w.total += 256;
   }
-  if (p->op == TK_OP_REAL && !w.tx_split && p->a.kind != TK_LAYOUT_DIAGONAL) {  // split-K partials (pair kernel)
+  if (pred_on_tc(p)) {  // per-tile MMA-step bits of the block predicate (expand_kbits_kernel)
+    const int bni = pred_bni(p);
+    const int64_t tiles = ((p->m + 255) / 256) * ((p->n + bni - 1) / bni);
+    w.kbits = w.total;
+    w.total += align256(tiles * (((p->k + 15) / 16 + 31) / 32) * 4);
+  } else if (p->op == TK_OP_REAL && !w.tx_split && p->a.kind != TK_LAYOUT_DIAGONAL) {  // split-K partials (pair kernel)
     const int64_t sb = split_ws_bytes(p->m, p->n, p->k, p->b);
     if (sb > 0) { w.splitk = w.total; w.total += align256(sb); }
   }
@@ -660,6 +687,7 @@ int launch_tc_pair(const tk::TcParams& prm, cudaStream_t s) {
   g_info.pdl = run.pdl;
   g_info.c_stream = CSTREAM ? 1 : 0;
   g_info.d_tma = run.d_tma;
+  g_info.overlap_kb = NSUB == 2 ? run.ovl_kb : 0;
   return TK_OK;
 }
 
@@ -901,7 +929,7 @@ int launch_pack(const TkLayout& L, const void* src, uint16_t* dst, int64_t rows,
 }
 
 int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, void* d, const void* bias,
-           uint8_t* ws, const Workspace& w, cudaStream_t s) {
+           const uint8_t* kmask, uint8_t* ws, const Workspace& w, cudaStream_t s) {
   TkGemmPlan rewritten;
   const TkGemmPlan* p = p0;
   if (w.a_perm >= 0 && permuted_plan(p0, &rewritten)) {
@@ -1147,7 +1175,8 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
       return TK_OK;
     }
   }
-  if (op == TK_OP_REAL && dense && !rmapped &&
+  const bool pred_tc = w.kbits >= 0;  // block predicate: the CTA-pair kernel evaluates it
+  if (op == TK_OP_REAL && dense && !rmapped && !pred_tc &&
       (ov == 3 || (ov == 0 && (prm.diag_a || prm.kb_total <= 4 || (single_wave && !pair_ok))))) {
     const bool cs = prm.c_zero || ((prm.ldc * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(c) & 15) == 0);
     if (cs) {
@@ -1163,7 +1192,7 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
   }
   if (op == TK_OP_REAL && !prm.diag_a) {
     // CTA pair (256x256 tiles) once there are enough pair tiles to cover the SMs
-    if (ov == 4) {
+    if (ov == 4 && !pred_tc) {
       tk::TcParams pp = prm;
       pp.num_mb = int((p->m + 511) / 512);
       pp.num_nb = int((p->n + tk::TC2_BN - 1) / tk::TC2_BN);
@@ -1175,7 +1204,7 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
       if (mn && (rc = make_map_2d(&pp.tb[0], b_plane0, p->b.scalar, p->k, p->n, pitch, 64, 64))) return rc;
       return dense ? launch_tc_quad<true>(pp, s) : launch_tc_quad<false>(pp, s);
     }
-    if (ov == 2 || (ov == 0 && pair_ok)) {
+    if (ov == 2 || (ov == 0 && pair_ok) || pred_tc) {
       tk::TcParams pp = prm;
       // 256 x 512 pair tiles (two MMAs share each A tile: 25 % fewer L2->SM bytes per flop, so
       // more flops per joule under the power cap) once K is long enough to amortise their
@@ -1184,17 +1213,28 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
       const int64_t tiles2 = ((p->m + 255) / 256) * ((p->n + 511) / 512);
       int nsub = (p->k >= 8192 && tiles2 >= 4 * int64_t(pair_clusters())) ? 2 : 1;
       if (knob_set(K_PAIR_NSUB)) nsub = knob(K_PAIR_NSUB, 1) == 2 ? 2 : 1;
+      if (pred_tc) nsub = 1;
       int mn;
       int64_t pitch;
       int rc;
       tma_operand(p->b, mn, pitch);
-      const int bni = nsub == 2 ? 256 : choose_pair_bni(p->m, p->n, /*b_mn_major=*/!mn, pair_clusters());
+      const int bni = pred_tc ? pred_bni(p) : nsub == 2 ? 256 : choose_pair_bni(p->m, p->n, /*b_mn_major=*/!mn, pair_clusters());
       pp.num_mb = int((p->m + 255) / 256);
       pp.num_nb = int((p->n + bni * nsub - 1) / (bni * nsub));
       pp.num_tiles = pp.num_mb * pp.num_nb;
       pp.num_units = pp.sk_first = pp.num_tiles;
       pp.sk_parts = 1;
       pp.nar_units = 0;
+      if (pred_tc) {  // block predicate -> per-tile MMA-step bits, before the GEMM on the stream
+        pp.kwords = int(((p->k + 15) / 16 + 31) / 32);
+        pp.kbits = reinterpret_cast<const uint32_t*>(ws + w.kbits);
+        const int64_t words = int64_t(pp.num_tiles) * pp.kwords;
+        tk::expand_kbits_kernel<<<unsigned((words + 255) / 256), 256, 0, s>>>(
+            const_cast<uint32_t*>(pp.kbits), pp.num_tiles, pp.kwords, pp.num_mb, pp.num_nb, pp.group_m, bni,
+            p->m, p->k, p->block[0], p->block[1], p->block[2], kmask, p->predicate == TK_PRED_DIAGONAL ? 1 : 2);
+        TK_CUDA(cudaGetLastError());
+        ++g_launches;
+      }
       if (nsub == 2) {  // staggered schedule (unit_at in tk_tc_gemm2.cuh): clusters [0, S)
         // split one wide tile into a leading and a trailing half; balanced when T mod P >= S.
         // Opt-in: bitwise equal, but measured 3-6 % slower (8192^3, 16384^3, 8192x16384x8192)
@@ -1204,6 +1244,9 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
           pp.nar_units = S;
           pp.num_units = pp.num_tiles + S;  // (>= P: the grid is all P clusters)
         }
+        // drain overlap (nsub2_step in tk_tc_gemm2.cuh): 16 lo-only + 16 hi-only k-block steps
+        // at each tile boundary hide the half-accumulator drains under MMAs
+        pp.ovl_kb = pp.nar_units ? 0 : std::max(0, std::min(knob(K_NSUB2_OVERLAP, 16), pp.kb_total / 4));
       }
       if (nsub == 1 && dense && w.splitk >= 0 && !knob_set(K_PAIR_GRID)) {
         const SplitPlan sp = split_plan(pp.num_tiles, pair_clusters(), pp.kb_total, bni);
@@ -1586,7 +1629,7 @@ int tk_gemm(const TkGemmPlan* plan0, const void* a, const void* b, const void* c
     Workspace w = plan_workspace(plan, lane);
     if (w.total > 0 && (!workspace || workspace_bytes < w.total))
       return fail(TK_ERR_CONFIG, "workspace of %lld bytes required", (long long)w.total);
-    rc = run_tc(plan, a, b, c, d, bias, static_cast<uint8_t*>(workspace), w, s);
+    rc = run_tc(plan, a, b, c, d, bias, kmask, static_cast<uint8_t*>(workspace), w, s);
     g_info.workspace_bytes = w.total;
   } else {
     rc = run_simt(plan, a, b, c, d, bias, kmask, s);

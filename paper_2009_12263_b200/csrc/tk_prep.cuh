@@ -93,6 +93,40 @@ __global__ void __launch_bounds__(256) transform_split_kernel(const __half* __re
   if (SPLIT && __syncthreads_or(nz) && threadIdx.x == 0) atomicOr(flag, 1);
 }
 
+// Block predicate (reference components.py:171-191: executed per (output block, block-K)
+// iteration, kernel.py:399-404) expanded for the tensor-core lane: one bit per K=16 MMA step of
+// every pair tile (kbits[t * kwords + s / 32], bit s % 32), so the producer skips k-blocks whose
+// four steps are all off and the MMA issuer skips single steps.  Needs every tile inside one
+// reference block (bm % 256 == 0, bn % tile_n == 0) and bk % 16 == 0.  mode 1: the diagonal
+// rule max(m0, k0) < min(m0 + bm, k0 + bk); mode 2: the host-evaluated kmask
+// [block rank (bi + bj * M/bm)][K/bk].  Tiles are numbered by the kernel's grouped raster.
+__global__ void expand_kbits_kernel(uint32_t* __restrict__ kbits, int tiles, int kwords, int num_mb, int num_nb,
+                                    int group_m, int tile_n, int64_t m, int64_t k, int64_t bm, int64_t bn,
+                                    int64_t bk, const uint8_t* __restrict__ kmask, int mode) {
+  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= int64_t(tiles) * kwords) return;
+  const int t = int(idx / kwords), w = int(idx % kwords);
+  const int per_group = group_m * num_nb, g = t / per_group, first = g * group_m;
+  const int gm = min(num_mb - first, group_m), r = t - g * per_group;
+  const int mb = first + r % gm, nb = r / gm;  // tile_coords()
+  const int64_t bi = int64_t(mb) * 256 / bm, bj = int64_t(nb) * tile_n / bn, nkb = k / bk;
+  uint32_t word = 0;
+  for (int b = 0; b < 32; ++b) {
+    const int64_t k0 = (int64_t(w) * 32 + b) * 16;
+    if (k0 >= k) break;
+    const int64_t c = k0 / bk;
+    bool run;
+    if (mode == 1) {
+      const int64_t m0 = bi * bm, kc = c * bk;
+      run = max(m0, kc) < min(m0 + bm, kc + bk);
+    } else {
+      run = kmask[(bi + bj * (m / bm)) * nkb + c] != 0;
+    }
+    word |= uint32_t(run) << b;
+  }
+  kbits[idx] = word;
+}
+
 }  // namespace tk
 
 namespace tk {

@@ -118,7 +118,36 @@ struct TcParams {
                                                  // pair NSUB 2: half-width first units (stagger)
   float* sk_ws;
   int32_t* sk_flags;
+  // pair kernel NSUB 2: k-blocks at each end of a tile run as separate lo-only and hi-only
+  // passes so one accumulator half drains while the tensor cores fill the other (0: off)
+  int32_t ovl_kb, pad8;
+  // block predicate on the tensor cores (mask or diagonal rule over a dense A, reference
+  // components.py:171-191, kernel.py:399-404): kbits[tile * kwords + kb / 8] holds 4 bits per
+  // 64-deep k-block, one per K=16 MMA step (expand_kbits_kernel); null = every step runs
+  const uint32_t* kbits;
+  int32_t kwords, pad9;
 };
+
+// the 4 MMA-step bits of k-block kb of pair tile `tile` (0xF without a predicate)
+__device__ __forceinline__ uint32_t kmask4(const TcParams& p, int tile, int kb) {
+  if (!p.kbits) return 0xFu;
+  return (__ldg(p.kbits + int64_t(tile) * p.kwords + (kb >> 3)) >> ((kb & 7) * 4)) & 0xFu;
+}
+// every step of the tile masked off: the accumulator is never written, the epilogue adds -0
+__device__ __forceinline__ bool tile_masked_out(const TcParams& p, int tile) {
+  if (!p.kbits) return false;
+  for (int w = 0; w < p.kwords; ++w)
+    if (__ldg(p.kbits + int64_t(tile) * p.kwords + w)) return false;
+  return true;
+}
+// -0.0 is the additive identity for every FP32 value (c + -0 == c, -0 + -0 == -0): a tile
+// whose every block-K iteration was skipped keeps acc = g2s_c(C) exactly as the reference
+__device__ __forceinline__ void zero_acc(uint32_t (&r)[32], bool z) {
+  if (z) {
+#pragma unroll
+    for (int jj = 0; jj < 32; ++jj) r[jj] = 0x80000000u;
+  }
+}
 
 __device__ __forceinline__ void tile_coords(const TcParams& p, int t, int& mb, int& nb) {
   const int per_group = p.group_m * p.num_nb;
@@ -278,7 +307,8 @@ __device__ __forceinline__ void split_sum(uint32_t (&r)[32], uint32_t taddr, boo
 template <int OP, int COLS, int BN, bool SK = false>
 __device__ __forceinline__ void epilogue_dense(const TcParams& p, uint64_t* tfull, uint32_t aphase,
                                                uint32_t tbase, int i, int jbase, int lane,
-                                               SkIn sk = SkIn{nullptr, 0, 0}, bool eps = false) {
+                                               SkIn sk = SkIn{nullptr, 0, 0}, bool eps = false,
+                                               bool masked = false) {
   const bool row_ok = i < p.m;
   const bool has_c = !p.c_zero;
   if (OP == OP_REAL || OP == OP_SPLIT) {
@@ -311,6 +341,7 @@ __device__ __forceinline__ void epilogue_dense(const TcParams& p, uint64_t* tful
       if constexpr (SK) sk_gather(sk, j0 - jbase + (jbase % BN), pv);
       tmem_ld_wait();
       split_sum<OP, BN>(r, taddr, eps);
+      zero_acc(r, masked);
       float out[32];
       epi_math_real<SK>(p, r, cv, pv, has_c, bias_m, bcol, out);
       if (ch + 1 < COLS / 32) load_c(j0 + 32);
@@ -417,7 +448,7 @@ __device__ __forceinline__ void epilogue_stream(const TcParams& p, uint64_t* tfu
                                                 uint32_t tbase, int i, int jbase, int lane,
                                                 float* ring, uint64_t* cfull, uint64_t* cempty,
                                                 uint32_t& cq, int row0, SkIn sk = SkIn{nullptr, 0, 0},
-                                                uint32_t* smask = nullptr) {
+                                                uint32_t* smask = nullptr, bool masked = false) {
   const bool row_ok = i < p.m;
   const bool has_c = !p.c_zero;
   float* dp = reinterpret_cast<float*>(p.d_ptr) + (row_ok ? i : 0);
@@ -468,6 +499,7 @@ __device__ __forceinline__ void epilogue_stream(const TcParams& p, uint64_t* tfu
       if (!p.sk_tma) sk_gather(sk, j0 - jbase + (jbase % BN), pv);
     }
     tmem_ld_wait();
+    zero_acc(r, masked);
     if (ch == 0) TK_TS_EPI(8);
     float out[32];
     epi_math_real<SK>(p, r, cv, pv, has_c, bias_m, bcol, out);
@@ -514,7 +546,8 @@ __device__ __forceinline__ void epilogue_stream(const TcParams& p, uint64_t* tfu
 // Any digit-mapped C/D layout and any transform program (the rare path).
 template <int OP, int COLS, int BN>
 __device__ __noinline__ void epilogue_generic(const TcParams& p, uint64_t* tfull, uint32_t aphase,
-                                              uint32_t tbase, int i, int jbase, bool eps = false) {
+                                              uint32_t tbase, int i, int jbase, bool eps = false,
+                                              bool masked = false) {
   const bool row_ok = i < p.m;
   const int64_t c_row = row_ok ? map_dim(p.c_map, 0, i) : 0;
   const int64_t d_row = row_ok ? map_dim(p.d_map, 0, i) : 0;
@@ -530,6 +563,7 @@ __device__ __noinline__ void epilogue_generic(const TcParams& p, uint64_t* tfull
     if (OP == OP_COMPLEX || OP == OP_DUAL) tmem_ld_32x32b_x32(tbase + uint32_t(BN) + col, r1);
     tmem_ld_wait();
     split_sum<OP, BN>(r0, tbase + col, eps);
+    zero_acc(r0, masked);
 #pragma unroll 1
     for (int jj = 0; jj < 32; ++jj) {
       const int j = j0 + jj;

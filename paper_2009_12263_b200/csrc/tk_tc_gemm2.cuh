@@ -104,6 +104,22 @@ __device__ __forceinline__ PairUnit unit_at(const TcParams& p, int c, int P, int
   return pair_unit(p, c + idx * P);
 }
 
+// NSUB 2 drain overlap.  A 256 x 512 tile has one 512-column accumulator: columns [0,256) (lo)
+// and [256,512) (hi), each filled by one N=256 MMA per K=16 step.  Run as K + Xs + Xe steps,
+//   [0,Xs) lo only | [0,Xs) hi only | [Xs,K-Xe) both | [K-Xe,K) lo only | [K-Xe,K) hi only
+// (k-block indices; mirrored for serpentine tiles), lo completes Xe hi-only steps before hi, so
+// its drain runs under them, and the next tile's Xs lo-only steps cover the hi drain.  Each half
+// still accumulates its k-blocks in ascending (or, serpentine, descending) order.  The first
+// unit of a cluster has nothing to overlap at its start (Xs = 0), the last none at its end
+// (Xe = 0).  Returns the k-block and the half mask (1 lo, 2 hi, 3 both) of step i.
+__device__ __forceinline__ void nsub2_step(int i, int K, int Xs, int Xe, int& kb, int& mask) {
+  if (i < Xs) { kb = i; mask = 1; }
+  else if (i < 2 * Xs) { kb = i - Xs; mask = 2; }
+  else if (i < K + Xs - Xe) { kb = i - Xs; mask = 3; }
+  else if (i < K + Xs) { kb = i - Xs; mask = 1; }
+  else { kb = i - Xs - Xe; mask = 2; }
+}
+
 template <bool DENSE_EPI, bool CSTREAM = false, int NSUB = 1, int BNI = 256, int CSL = TC2S_CSLOTS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     tc_gemm_pair_kernel(const __grid_constant__ TcParams p) {
@@ -256,13 +272,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         const int m0 = mb * 256 + int(rank) * 128;     // this CTA's rows of A
         const int n0 = nb * BNP + un.noff + int(rank) * (BNI / 2);  // this CTA's columns of B (per MMA)
         const int nsub_u = un.narrow ? 1 : NSUB;
-        const uint32_t tx = 2 * (TC2_TILE_BYTES + nsub_u * PL::B_BYTES);
         // serpentine K: every other tile of a cluster walks K downwards, so the next
         // wave starts on the K-slices the previous one loaded last (still in L2)
         const bool rev = p.serp && (lu & 1);
-        for (int ki = 0; ki < un.kb1 - un.kb0; ++ki) {
-          const int kb = rev ? un.kb1 - 1 - ki : un.kb0 + ki;
+        // NSUB 2 drain overlap (nsub2_step): lo-only / hi-only steps load one B half
+        const int X = (NSUB == 2 && !un.narrow) ? p.ovl_kb : 0;
+        const int Xs = u > 0 ? X : 0, Xe = u < nu - 1 ? X : 0;
+        const int nsteps = un.kb1 - un.kb0 + Xs + Xe;
+        for (int ki = 0; ki < nsteps; ++ki) {
+          int kq = ki, mask = (1 << nsub_u) - 1;
+          if (X) nsub2_step(ki, un.kb1 - un.kb0, Xs, Xe, kq, mask);
+          const int kb = rev ? un.kb1 - 1 - kq : un.kb0 + kq;
+          if (NSUB == 1 && !kmask4(p, un.tile, kb)) continue;  // predicate: k-block skipped entirely
           const int k0 = kb * TC_BK;
+          const uint32_t tx = 2 * (TC2_TILE_BYTES + __popc(mask) * PL::B_BYTES);
           mbar_wait(&empty[stage], phase ^ 1);
           if (no_load) {  // diagnostic: MMA issue rate without operand traffic
             if (leader) mbar_arrive(&full[stage]);
@@ -300,7 +323,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           }
 #pragma unroll
           for (int sub = 0; sub < NSUB; ++sub) {
-            if (sub >= nsub_u) break;
+            if (!(mask >> sub & 1)) continue;
             uint8_t* bt = b_tile(stage) + sub * PL::B_BYTES;
             const int nn = n0 + sub * BNI;
             if (b_mode == 0) {
@@ -353,21 +376,62 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           mbar_wait(&tempty[as], aphase ^ 1);
           tc_fence_after();
           const uint32_t d0 = tmem_base + uint32_t(as * BNI);
-          for (int kb = un.kb0; kb < un.kb1; ++kb) {  // (operand order is the producer's)
-            mbar_wait(&full[stage], phase);
-            if (local == 0 && kb == un.kb0) TK_TS(2);
-            tc_fence_after();
-            issue(stage, 0, d0, kb == un.kb0);
-            tc_commit_pair(&empty[stage], 0x3);
-            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          if (!p.kbits) {
+            for (int kb = un.kb0; kb < un.kb1; ++kb) {  // (operand order is the producer's)
+              mbar_wait(&full[stage], phase);
+              if (local == 0 && kb == un.kb0) TK_TS(2);
+              tc_fence_after();
+              issue(stage, 0, d0, kb == un.kb0);
+              tc_commit_pair(&empty[stage], 0x3);
+              if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            }
+          } else {
+            // block predicate: the producer's k order, skipped k-blocks never reach the ring;
+            // inside a block only the enabled K=16 steps issue, the first of them overwrites
+            const bool rev = p.serp && (local & 1);
+            bool first = true;
+            for (int ki = 0; ki < un.kb1 - un.kb0; ++ki) {
+              const uint32_t bits = kmask4(p, un.tile, rev ? un.kb1 - 1 - ki : un.kb0 + ki);
+              if (!bits) continue;
+              mbar_wait(&full[stage], phase);
+              tc_fence_after();
+              const uint32_t so = uint32_t(stage) * uint32_t(PL::STAGE_BYTES >> 4);
+#pragma unroll
+              for (int kk = 0; kk < TC_BK / 16; ++kk)
+                if (bits >> kk & 1u) {
+                  tc_mma_f16_pair(d0, a_desc0 + so + kk * a_kk, b_desc0 + so + kk * b_kk, idesc, first ? 0u : 1u);
+                  first = false;
+                }
+              tc_commit_pair(&empty[stage], 0x3);
+              if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            }
           }
           tc_commit_pair(&tfull[as], 0x3);
           TK_TS(3);
         } else {
           // 256 x 512 tile, one accumulator: columns [0,256) (lo) and [256,512) (hi) are drained
-          // in that order (tempty[0], tempty[1]).  The lo MMAs of the next tile start as soon as lo
-          // is drained; hi MMAs trail, holding up to STAGES operand stages, until hi is drained.
+          // in that order (tempty[0], tempty[1]); tfull[0] / tfull[1] say lo / hi are complete.
           const uint32_t tph = (local & 1) ^ 1;
+          if (p.ovl_kb > 0 && !un.narrow) {
+            // drain overlap: lo-only / hi-only steps at the tile ends (nsub2_step)
+            const int K = p.kb_total, Xs = u > 0 ? p.ovl_kb : 0, Xe = u < nu - 1 ? p.ovl_kb : 0;
+            const int nsteps = K + Xs + Xe;
+            for (int i = 0; i < nsteps; ++i) {
+              int kq, mask;
+              nsub2_step(i, K, Xs, Xe, kq, mask);
+              if (i == 0) mbar_wait(&tempty[0], tph);   // the previous tile's lo is drained
+              if (i == Xs) mbar_wait(&tempty[1], tph);  // ... and its hi (first hi step)
+              mbar_wait(&full[stage], phase);
+              tc_fence_after();
+              if (mask & 1) issue(stage, 0, tmem_base, i == 0);
+              if (mask & 2) issue(stage, 1, tmem_base + 256u, i == Xs);
+              tc_commit_pair(&empty[stage], 0x3);
+              if (i == K + Xs - 1) tc_commit_pair(&tfull[0], 0x3);  // lo complete
+              if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            }
+            tc_commit_pair(&tfull[1], 0x3);  // hi complete
+            continue;
+          }
           mbar_wait(&tempty[0], tph);
           tc_fence_after();
           if (un.narrow) {  // half-width tile: lo columns only (its epilogue also releases hi)
@@ -379,6 +443,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
               if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
             tc_commit_pair(&tfull[0], 0x3);
+            tc_commit_pair(&tfull[1], 0x3);
             continue;
           }
           bool hi_ok = false;
@@ -410,6 +475,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
           tc_commit_pair(&tfull[0], 0x3);
+          tc_commit_pair(&tfull[1], 0x3);
         }
       }
     }
@@ -520,38 +586,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       }
       const int row0 = mb * 256 + int(rank) * 128 + quarter * 32;
       float* my_ring = cring + ew * CSL * (TC_CBOX_BYTES / 4);
+      const bool masked = tile_masked_out(p, t);  // predicate skipped every k-block of the tile
       // NSUB 1: accumulator `local & 1`, one pass over this warp's 128 columns.
       // NSUB 2: one accumulator, pass 0 drains columns [0,256), pass 1 [256,512) (128 per warp).
 #pragma unroll 1
       for (int pass = 0; pass < (un.narrow ? 1 : NSUB); ++pass) {
         const int as = NSUB == 1 ? (local & 1) : 0;
         const uint32_t aphase = NSUB == 1 ? ((local >> 1) & 1) : (local & 1);
+        uint64_t* tf = tfull + (NSUB == 1 ? as : pass);  // NSUB 2: lo / hi complete
         const uint32_t tbase = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(as * BNI);
         // (a half-width tile sits in TMEM columns [0,256): shift the base by its column offset)
         const uint32_t tb = tbase - uint32_t(un.noff);
         const int jbase = nb * BNP + un.noff + pass * BNI + half * PL::WCOLS;
         if (blockIdx.x == p.dbg_cta && warp == 4 && lane == 0 && u == nu - 1) {
-          mbar_wait(tfull + as, aphase);
+          mbar_wait(tf, aphase);
           TK_TS(4);
         }
         if (CSTREAM) {
           if (sk.p)
-            epilogue_stream<PL::WCOLS, BNP, CSL, true>(p, tfull + as, aphase, tb, i, jbase, lane, my_ring,
+            epilogue_stream<PL::WCOLS, BNP, CSL, true>(p, tf, aphase, tb, i, jbase, lane, my_ring,
                                                    cfull + ew * CSL, cempty + ew * CSL, cq,
                                                    row0, sk, &smask);
           else
-            epilogue_stream<PL::WCOLS, BNP, CSL>(p, tfull + as, aphase, tb, i, jbase, lane, my_ring,
-                                                   cfull + ew * CSL, cempty + ew * CSL, cq, row0);
+            epilogue_stream<PL::WCOLS, BNP, CSL>(p, tf, aphase, tb, i, jbase, lane, my_ring,
+                                                   cfull + ew * CSL, cempty + ew * CSL, cq, row0,
+                                                   SkIn{nullptr, 0, 0}, nullptr, masked);
         } else if (p.dbg_skip_epi) {
-          mbar_wait_sleep(tfull + as, aphase);
+          mbar_wait_sleep(tf, aphase);
           tc_fence_after();
         } else if (DENSE_EPI) {
           if (sk.p)
-            epilogue_dense<OP_REAL, PL::WCOLS, BNP, true>(p, tfull + as, aphase, tb, i, jbase, lane, sk);
+            epilogue_dense<OP_REAL, PL::WCOLS, BNP, true>(p, tf, aphase, tb, i, jbase, lane, sk);
           else
-            epilogue_dense<OP_REAL, PL::WCOLS, BNP>(p, tfull + as, aphase, tb, i, jbase, lane);
+            epilogue_dense<OP_REAL, PL::WCOLS, BNP>(p, tf, aphase, tb, i, jbase, lane, SkIn{nullptr, 0, 0},
+                                                    false, masked);
         } else
-          epilogue_generic<OP_REAL, PL::WCOLS, BNP>(p, tfull + as, aphase, tb, i, jbase);
+          epilogue_generic<OP_REAL, PL::WCOLS, BNP>(p, tf, aphase, tb, i, jbase, false, masked);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[NSUB == 1 ? as : pass]), 0));

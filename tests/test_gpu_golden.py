@@ -187,3 +187,83 @@ def test_gemm_ex_raw_host_pointers_bitwise(cuda):
                         b.ctypes.data, meta["beta"], 0.0, c.ctypes.data)
     assert st == 0
     assert np.array_equal(c, z["d"])
+
+
+def _padded_cfg(m, n, k, dt, pads):
+    L = tk.layouts
+    return dataclasses.replace(
+        tk.build_dense_config(m, n, k, dt),
+        global_a_layout=L.Padded(L.ColMajor(dt, ("M", "K"), (m, k)), pads["A"]),
+        global_b_layout=L.Padded(L.ColMajor(dt, ("K", "N"), (k, n)), pads["B"]),
+        global_c_layout=L.Padded(L.ColMajor(np.float32, ("M", "N"), (m, n)), pads["C"]),
+        global_d_layout=L.Padded(L.ColMajor(np.float32, ("M", "N"), (m, n)), pads["D"]))
+
+
+def _pad_buf(x, p, dt):
+    buf = np.full((x.shape[0] + p, x.shape[1]), -7.0, dt)
+    buf[:x.shape[0]] = x
+    return buf.ravel(order="F")
+
+
+@pytest.mark.parametrize("lane", ["tcgen05", "simt"])
+def test_padded_global_layouts(cuda, lane):
+    """Padded global A / B / C / D (pads 8 / 3 / 4 / 5: A and C stay TMA-addressable, B is
+    gathered, D leaves through the register epilogue) against the reference's own run
+    (tests/golden/padded_global.npz): the padding is never read into the product nor written.
+    tcgen05 on fp16 storage within 4 * 2^-24 * sqrt(K); the exact lane on f32 bitwise."""
+    meta, z = load("padded_global")
+    m, n, k, pads = meta["m"], meta["n"], meta["k"], meta["pads"]
+    dt = np.float16 if lane == "tcgen05" else np.float32
+    cfg = _padded_cfg(m, n, k, dt, pads)
+    dbuf = np.full((m + pads["D"]) * n, 123.0, np.float32)
+    with tk.force_lane(lane):
+        cnt = tk.matmul(cfg, _pad_buf(z["a"], pads["A"], dt), _pad_buf(z["b"], pads["B"], dt),
+                        _pad_buf(z["c"], pads["C"], np.float32), dbuf)
+    assert tk.last_run()["lane"] == lane
+    full = dbuf.reshape((m + pads["D"], n), order="F")
+    want = z["d_buf"].reshape((m + pads["D"], n), order="F")
+    assert np.all(full[m:] == 123.0)
+    if lane == "simt":
+        assert np.array_equal(dbuf, z["d_buf"])
+    else:
+        assert O.rel_err(full[:m], want[:m]) <= O.tolerance(k)
+    assert dataclasses.asdict(cnt) == meta["counters"]
+
+
+@pytest.mark.parametrize("lane", ["tcgen05", "simt"])
+def test_padded_shared_builder(cuda, lane):
+    """build_dense_config(shared_pad=4): on the tensor cores the 128-byte TMA swizzle replaces
+    the padding (same arithmetic); the exact lane bitwise the reference's D."""
+    meta, z = load("padded_shared")
+    m, n, k = meta["m"], meta["n"], meta["k"]
+    dt = np.float16 if lane == "tcgen05" else np.float32
+    cfg = tk.build_dense_config(m, n, k, dt, shared_pad=meta["pad"])
+    d = np.zeros(m * n, np.float32)
+    with tk.force_lane(lane):
+        cnt = tk.matmul(cfg, F(z["a"].astype(dt)), F(z["b"].astype(dt)), F(z["c"]), d)
+    assert tk.last_run()["lane"] == lane
+    got = d.reshape((m, n), order="F")
+    if lane == "simt":
+        assert np.array_equal(got, z["d"])
+    else:
+        assert O.rel_err(got, z["d"]) <= O.tolerance(k)
+    assert dataclasses.asdict(cnt) == meta["counters"]
+
+
+def test_padded_fp16_integer_bitwise_large(cuda):
+    """Padded fp16 operands at a multi-tile size on the CTA-pair kernel, bitwise on integers."""
+    m, n, k = 1024, 1536, 1024
+    pads = {"A": 8, "B": 16, "C": 4, "D": 12}
+    rng = np.random.default_rng(415)
+    a = rng.integers(-4, 5, (m, k)).astype(np.float16)
+    b = rng.integers(-4, 5, (k, n)).astype(np.float16)
+    c = rng.integers(-4, 5, (m, n)).astype(np.float32)
+    cfg = _padded_cfg(m, n, k, np.float16, pads)
+    dev = lambda x: torch.from_numpy(x).cuda()
+    dbuf = torch.full(((m + pads["D"]) * n,), 123.0, device=cuda)
+    tk.matmul(cfg, dev(_pad_buf(a, pads["A"], np.float16)), dev(_pad_buf(b, pads["B"], np.float16)),
+              dev(_pad_buf(c, pads["C"], np.float32)), dbuf)
+    assert tk.last_run()["lane"] == "tcgen05" and tk.last_run()["plan"]["kernel"] == "pair"
+    full = dbuf.cpu().numpy().reshape((m + pads["D"], n), order="F")
+    assert np.all(full[m:] == 123.0)
+    assert np.array_equal(full[:m], O.gemm_real(a.astype(np.float32), b.astype(np.float32), c))

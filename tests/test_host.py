@@ -515,3 +515,18 @@ def test_fused_allgather_entry_validates_before_launch():
     rc = lib.tk_gemm_peers(ctypes.byref(plan2), None, None, None, None, None, None, None, 0, None,
                            peers, 1)
     assert rc == _lib.TK_ERR_CONFIG and "dense column-major" in _lib.last_error()
+
+
+def test_padded_shared_builder_resolves_like_reference():
+    """build_dense_config(shared_pad=4): the heuristic sees the padded staging footprint, as
+    the reference's (golden made by the reference, oracle/make_golden.py padded_cases)."""
+    import json
+    import os
+
+    z = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "padded_shared.npz"))
+    meta = json.loads(str(z["meta"]))
+    cfg = tk.build_dense_config(meta["m"], meta["n"], meta["k"], np.float32, shared_pad=meta["pad"])
+    res = kernel.resolve_config(cfg)
+    assert list(res.params.block_tile) == meta["block_tile"]
+    plan, _, executed = kernel.lower(res)
+    assert dataclasses.asdict(kernel._counters(res, executed)) == meta["counters"]

@@ -136,3 +136,15 @@ def test_tolerance_bound_holds_for_reference_f32():
     _, z = load("dense_f16valued")
     exact = O.exact_gemm(z["a"], z["b"], z["c"], beta=1.0)
     assert O.rel_err(z["d"], exact) <= O.tolerance(z["a"].shape[1])
+
+
+def test_padded_shared_and_global_bitwise():
+    """Padded shared staging and padded global buffers (reference layouts.py:132-188) change
+    no arithmetic: the oracle on the logical matrices reproduces the reference's D."""
+    _, z = load("padded_shared")
+    assert np.array_equal(O.gemm_real(z["a"], z["b"], z["c"]), z["d"])
+    meta, z = load("padded_global")
+    m, n, pd = meta["m"], meta["n"], meta["pads"]["D"]
+    dfull = z["d_buf"].reshape((m + pd, n), order="F")
+    assert np.array_equal(O.gemm_real(z["a"], z["b"], z["c"]), dfull[:m])
+    assert np.all(dfull[m:] == 123.0)  # padding rows never written
