@@ -29,8 +29,8 @@
 extern "C" {
 #endif
 
-#define TK_ABI_VERSION 1
-#define TK_MAX_DIGITS 3
+#define TK_ABI_VERSION 2
+#define TK_MAX_DIGITS 5   /* digits per logical dimension: StridedPermutation up to rank 5 */
 #define TK_MAX_TOPS 8
 
 /* storage / accumulation scalars */

@@ -263,7 +263,10 @@ def variant_cases():
 
 GETT_CASES = (("abcd-aebf-dfce", dict(a=8, b=4, c=4, d=6, e=4, f=6)),
               ("abc-acd-db", dict(a=8, b=16, c=4, d=8)),
-              ("ab-cad-dcb", dict(a=16, b=24, c=2, d=4)))
+              ("ab-cad-dcb", dict(a=16, b=24, c=2, d=4)),
+              # five M digits, four K digits, three N digits, all interleaved (rank-5 maps)
+              ("axbyczde-fabgchdie-xhzfigy", dict(a=2, b=4, c=2, d=2, e=2, f=2, g=4, h=2, i=2,
+                                                  x=4, y=2, z=4)))
 
 
 def gett_cases():

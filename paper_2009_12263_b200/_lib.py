@@ -14,8 +14,8 @@ from ctypes import c_double, c_int, c_int32, c_int64, c_longlong, c_void_p
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TK_SM100_LIB", os.path.join(HERE, "libtk_sm100.so"))
 
-ABI_VERSION = 1
-MAX_DIGITS = 3
+ABI_VERSION = 2
+MAX_DIGITS = 5
 MAX_TOPS = 8
 
 LANE_AUTO, LANE_TCGEN05, LANE_SIMT = 0, 1, 2

@@ -25,6 +25,8 @@
 #include "tk_tc_gemm4.cuh"
 #include "tk_tc_gemm2c.cuh"
 
+static_assert(tk::MAX_DIGITS == TK_MAX_DIGITS, "device digit maps match the C ABI");
+
 namespace {
 
 thread_local std::string g_err;
@@ -308,11 +310,11 @@ bool permuted_plan(const TkGemmPlan* p, TkGemmPlan* out) {
   if (out) {
     *out = *p;
     auto dense_cm = [](TkLayout& L, int64_t rows, int64_t cols, int64_t ld) {
+      memset(L.ext, 0, sizeof(L.ext));
+      memset(L.stride, 0, sizeof(L.stride));
       L.ndigits[0] = L.ndigits[1] = 1;
       L.ext[0][0] = rows; L.stride[0][0] = 1;
       L.ext[1][0] = cols; L.stride[1][0] = ld;
-      L.ext[0][1] = L.ext[0][2] = L.ext[1][1] = L.ext[1][2] = 0;
-      L.stride[0][1] = L.stride[0][2] = L.stride[1][1] = L.stride[1][2] = 0;
     };
     dense_cm(out->a, p->m, p->k, p->m);
     out->a.size = p->m * p->k;
@@ -514,7 +516,7 @@ tk::DigitMap to_map(const TkLayout& L) {
   tk::DigitMap m{};
   for (int d = 0; d < 2; ++d) {
     m.nd[d] = L.kind == TK_LAYOUT_STRIDED ? L.ndigits[d] : 1;
-    for (int t = 0; t < 3; ++t) {
+    for (int t = 0; t < TK_MAX_DIGITS; ++t) {
       m.e[d][t] = t < L.ndigits[d] ? L.ext[d][t] : 1;
       m.s[d][t] = t < L.ndigits[d] ? L.stride[d][t] : 0;
     }
@@ -1496,7 +1498,7 @@ namespace {
 void normalize_layout(TkLayout& L) {
   if (L.kind != TK_LAYOUT_STRIDED) return;
   for (int d = 0; d < 2; ++d) {
-    int64_t e[3], st[3];
+    int64_t e[TK_MAX_DIGITS], st[TK_MAX_DIGITS];
     int n = 0;
     for (int t = 0; t < L.ndigits[d]; ++t) {
       if (L.ext[d][t] == 1 && L.ndigits[d] > 1) continue;
@@ -1509,7 +1511,7 @@ void normalize_layout(TkLayout& L) {
       ++n;
     }
     if (n == 0) { e[0] = 1; st[0] = 1; n = 1; }
-    for (int t = 0; t < 3; ++t) {
+    for (int t = 0; t < TK_MAX_DIGITS; ++t) {
       L.ext[d][t] = t < n ? e[t] : 0;
       L.stride[d][t] = t < n ? st[t] : 0;
     }

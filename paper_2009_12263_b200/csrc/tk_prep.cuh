@@ -134,7 +134,7 @@ namespace tk {
 // Gather one plane of a half-precision operand stored under an arbitrary digit map (the
 // StridedPermutation / GETT layouts, reference layouts.py:435-506) into a dense column-major
 // rows x cols buffer, so any fused-transposition operand reaches the tensor cores through a
-// plain 2-D TMA map.  The operand is viewed as an n-digit tensor (<= 6 digits: each digit has
+// plain 2-D TMA map.  The operand is viewed as an n-digit tensor (<= 10 digits: each digit has
 // an extent, a source stride and a destination stride).  A block moves 64 x 64 tiles spanning
 // digit X (the source's fastest) and digit Y (the destination's fastest, or its next digit
 // when that is X) through shared memory: the read phase runs along X, the write phase along
@@ -145,7 +145,7 @@ namespace tk {
 struct PackDesc {
   int32_t n, fs, fd, vec_rd;   // X = fs, Y = fd; vec_rd: 16-byte reads along X
   int32_t wr_x, vec_wr, pad0, pad1;  // wr_x: destination-fastest tile digit is X; vec_wr: 16-byte writes
-  int64_t ext[6], ss[6], ds[6];
+  int64_t ext[2 * MAX_DIGITS + 1], ss[2 * MAX_DIGITS + 1], ds[2 * MAX_DIGITS + 1];
   int64_t tiles_s, tiles_d, outer;  // tiles along X, along Y, outer digit combinations
 };
 

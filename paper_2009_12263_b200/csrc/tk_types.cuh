@@ -18,11 +18,12 @@ enum { T_SCALE = 1, T_ADD = 2, T_RELU = 3 };
 constexpr int MAX_TOPS = 8;
 
 // Logical index -> element offset, one digit list per logical dimension (TkLayout).
+constexpr int MAX_DIGITS = 5;  // == TK_MAX_DIGITS
 struct DigitMap {
   int32_t nd[2];
   int32_t pad[2];
-  int64_t e[2][3];
-  int64_t s[2][3];
+  int64_t e[2][MAX_DIGITS];
+  int64_t s[2][MAX_DIGITS];
 };
 
 __host__ __device__ __forceinline__ int64_t map_dim(const DigitMap& m, int d, int64_t idx) {

@@ -33,7 +33,7 @@ from .tiling import Tile
 # layout kinds / pair modes, mirrored by TkLayoutKind / TkPairMode in include/tk_sm100.h
 KIND_STRIDED, KIND_DIAGONAL, KIND_ZERO = 0, 1, 2
 PAIR_NONE, PAIR_INTERLEAVED, PAIR_SPLIT = 0, 1, 2
-MAX_DIGITS = 3
+MAX_DIGITS = 5  # digits per logical dimension (TK_MAX_DIGITS)
 
 
 def _volume(extents) -> int:

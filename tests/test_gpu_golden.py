@@ -156,7 +156,7 @@ def test_contract_bitwise(cuda, shape):
     assert dataclasses.asdict(cnt) == meta["counters"]
 
 
-@pytest.mark.parametrize("spec", ["abcd_aebf_dfce", "abc_acd_db", "ab_cad_dcb"])
+@pytest.mark.parametrize("spec", ["abcd_aebf_dfce", "abc_acd_db", "ab_cad_dcb", "axbyczde_fabgchdie_xhzfigy"])
 def test_gett_bitwise(cuda, spec):
     """General contractions (f32: exact lane) against the reference's own outputs, with the
     reference's counters and resolved tiling."""

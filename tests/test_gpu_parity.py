@@ -492,6 +492,8 @@ def test_tensor_contraction_tcgen05(cuda, shape):
     ("abc-acd-db", dict(a=64, b=96, c=8, d=136)),                 # A gathered, B TMA, D dense
     ("ab-cad-dcb", dict(a=160, b=200, c=4, d=36)),                # 2-digit K in both operands
     ("bac-abd-dc", dict(a=24, b=16, c=72, d=200)),                # D scattered (generic epilogue)
+    # rank-5 maps: five M digits, four K digits, three N digits, interleaved in every tensor
+    ("axbyczde-fabgchdie-xhzfigy", dict(a=4, b=8, c=4, d=2, e=4, f=4, g=8, h=4, i=8, x=8, y=16, z=8)),
 ])
 @pytest.mark.parametrize("integer", [True, False])
 def test_gett_tcgen05(cuda, spec, sizes, integer):

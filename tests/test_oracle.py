@@ -95,7 +95,7 @@ def test_tensor_contraction_bitwise(shape):
     assert np.array_equal(O.tc_reference(z["a"], z["b"]), z["d"])
 
 
-GETT = ["abcd_aebf_dfce", "abc_acd_db", "ab_cad_dcb"]
+GETT = ["abcd_aebf_dfce", "abc_acd_db", "ab_cad_dcb", "axbyczde_fabgchdie_xhzfigy"]
 
 
 @pytest.mark.parametrize("spec", GETT)
