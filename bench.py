@@ -242,7 +242,8 @@ def run_ours(args):
                 "traffic_unit": "bytes/launch (dram read+write, ncu --set full)",
                 "algorithmic_flops_per_launch": flops_rank,
                 "algorithmic_bytes_per_launch": 2 * (m * k + k * n) + 8 * m * n,
-                "peak_source": f"{src} bf16 burst (MEASURED_PEAKS.json)",
+                "peak_source": ("measured bf16 burst (MEASURED_PEAKS.json)" if src == "measured" else
+                                "fallback 1590 TF/s bf16 burst (B200_PROFILING.md; MEASURED_PEAKS.json absent)"),
                 "frac_of_sustained": achieved / sustained_peak if sustained_peak else None,
                 "frac_of_spec_2250": achieved / 2250.0}
 

@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--rounds", type=int, default=3)
     ap.add_argument("--cool", type=float, default=1.0)
+    ap.add_argument("--graph", action="store_true", help="replay a CUDA graph of 10 launches (no host overhead)")
     args = ap.parse_args()
     n = args.n
     dev = torch.device("cuda")
@@ -61,17 +62,27 @@ def main():
             for _ in range(3):
                 tk.matmul(cfg, a, b, c, d, synchronize=False)
             torch.cuda.synchronize()
+            step, per = (lambda: tk.matmul(cfg, a, b, c, d, synchronize=False)), 1
+            if args.graph:
+                gr = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gr):
+                    for _ in range(10):
+                        tk.matmul(cfg, a, b, c, d, synchronize=False)
+                step, per = gr.replay, 10
+                step()
+                torch.cuda.synchronize()
             time.sleep(args.cool)
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s0.record()
             for _ in range(args.reps):
-                tk.matmul(cfg, a, b, c, d, synchronize=False)
+                step()
             s1.record()
             torch.cuda.synchronize()
-            ms = s0.elapsed_time(s1) / args.reps
+            ms = s0.elapsed_time(s1) / (args.reps * per)
             tf = 2.0 * n ** 3 / (ms * 1e-3) / 1e12
+            us = ms * 1e3
             res[setting].append((tf, mhz()))
-            print(f"round {r} {setting:40s} {tf:8.1f} TF  {mhz():7.1f} MHz  plan={tk.last_run()['plan']['kernel']}"
+            print(f"round {r} {setting:40s} {us:8.2f} us {tf:8.1f} TF  {mhz():7.1f} MHz  plan={tk.last_run()['plan']['kernel']}"
                   f"/{tk.last_run()['plan']['tile_n']}/ovl{tk.last_run()['plan']['overlap_kb']}", flush=True)
     out = {s: {"tflops_median": float(np.median([x[0] for x in v])),
                "mhz_median": float(np.median([x[1] for x in v])),
