@@ -64,7 +64,7 @@ enum Knob {
   K_SPLITK_S, K_SK_TMA, K_PDL, K_MN3D, K_PAIR_CSTREAM, K_PAIR_DTMA, K_C_PF, K_C_PF_SPREAD,
   K_NSUB2_CSL, K_STAGGER, K_PAIR_GRID, K_PAIR_DEEPC, K_PAIROPS_BN, K_DIAG_STREAM, K_D_TMA,
   K_L2_PROMO, K_POLICY_AB, K_POL_A, K_POL_B, K_PAIR_CLUSTERS, K_EX_SLABS, K_VERBOSE,
-  K_NSUB2_OVERLAP,
+  K_NSUB2_OVERLAP, K_PAIR_KPS,
   K_DBG_C_ZERO, K_DBG_SKIP_EPI, K_DBG_NO_LOAD, K_DBG_NO_MMA, K_DBG_CTA, K_COUNT
 };
 constexpr int K_FIRST_DIAG = K_DBG_C_ZERO;
@@ -74,7 +74,7 @@ const char* const kKnobNames[K_COUNT] = {
   "TK_PAIR_DTMA", "TK_C_PF", "TK_C_PF_SPREAD", "TK_NSUB2_CSL", "TK_STAGGER", "TK_PAIR_GRID",
   "TK_PAIR_DEEPC", "TK_PAIROPS_BN", "TK_DIAG_STREAM", "TK_D_TMA", "TK_L2_PROMO", "TK_POLICY_AB",
   "TK_POL_A", "TK_POL_B", "TK_PAIR_CLUSTERS", "TK_EX_SLABS", "TK_VERBOSE", "TK_NSUB2_OVERLAP",
-  "TK_DBG_C_ZERO", "TK_DBG_SKIP_EPI", "TK_DBG_NO_LOAD", "TK_DBG_NO_MMA", "TK_DBG_CTA"};
+  "TK_PAIR_KPS", "TK_DBG_C_ZERO", "TK_DBG_SKIP_EPI", "TK_DBG_NO_LOAD", "TK_DBG_NO_MMA", "TK_DBG_CTA"};
 #ifdef TK_DIAG
 constexpr int K_ENABLED = K_COUNT;
 #else
@@ -593,10 +593,10 @@ int launch_tc_variant(const tk::TcParams& prm, cudaStream_t s) {
   return TK_OK;
 }
 
-template <bool DENSE, bool CSTREAM = false, int NSUB = 1, int BNI = 256, int CSL = tk::TC2S_CSLOTS>
+template <bool DENSE, bool CSTREAM = false, int NSUB = 1, int BNI = 256, int CSL = tk::TC2S_CSLOTS, int KPS = 1>
 int launch_tc_pair(const tk::TcParams& prm, cudaStream_t s) {
-  constexpr int SMEM = tk::Tc2Plan<NSUB, CSTREAM, BNI, CSL>::SMEM;
-  auto kern = tk::tc_gemm_pair_kernel<DENSE, CSTREAM, NSUB, BNI, CSL>;
+  constexpr int SMEM = tk::Tc2Plan<NSUB, CSTREAM, BNI, CSL, KPS>::SMEM;
+  auto kern = tk::tc_gemm_pair_kernel<DENSE, CSTREAM, NSUB, BNI, CSL, KPS>;
   static bool attr[TK_MAX_DEV] = {};
   static int max_clusters_dev[TK_MAX_DEV] = {};
   const int dev = cur_dev();
@@ -665,9 +665,10 @@ int launch_tc_pair(const tk::TcParams& prm, cudaStream_t s) {
   cfg.numAttrs = run.pdl ? 1 : 0;
   TK_CUDA(cudaLaunchKernelEx(&cfg, kern, run));
   ++g_launches;
-  using PL = tk::Tc2Plan<NSUB, CSTREAM, BNI, CSL>;
+  using PL = tk::Tc2Plan<NSUB, CSTREAM, BNI, CSL, KPS>;
   info_kernel("pair");
   g_info.tile_m = 256;
+  g_info.tile_k = 64 * KPS;
   g_info.tile_n = PL::BNP;
   g_info.mma_n = BNI;
   g_info.nsub = NSUB;
@@ -696,8 +697,13 @@ int launch_tc_pair(const tk::TcParams& prm, cudaStream_t s) {
 // instantiate the pair kernel for the chosen instruction N
 template <bool DENSE, bool CSTREAM>
 int launch_tc_pair_bni(const tk::TcParams& prm, int bni, cudaStream_t s) {
-  if (bni == 64) return launch_tc_pair<DENSE, CSTREAM, 1, 64>(prm, s);
-  if (bni == 128) return launch_tc_pair<DENSE, CSTREAM, 1, 128>(prm, s);
+  // narrow tiles: two K-blocks per ring stage (halves the barrier round trips per operand byte)
+  // unless a block predicate needs per-K-block MMA bits
+  const bool kps2 = !prm.kbits && knob(K_PAIR_KPS, 2) == 2;
+  if (bni == 64) return kps2 ? launch_tc_pair<DENSE, CSTREAM, 1, 64, tk::TC2S_CSLOTS, 2>(prm, s)
+                             : launch_tc_pair<DENSE, CSTREAM, 1, 64>(prm, s);
+  if (bni == 128) return kps2 ? launch_tc_pair<DENSE, CSTREAM, 1, 128, tk::TC2S_CSLOTS, 2>(prm, s)
+                              : launch_tc_pair<DENSE, CSTREAM, 1, 128>(prm, s);
   // single wave, 256-wide tiles: a 4-slot C ring holds each warp's whole C block
   if (CSTREAM && prm.num_units <= pair_clusters() && knob(K_PAIR_DEEPC, 1))
     return launch_tc_pair<DENSE, CSTREAM, 1, 256, 4>(prm, s);

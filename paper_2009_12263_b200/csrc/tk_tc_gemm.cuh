@@ -832,7 +832,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(const __grid_con
     }
   }
 
-  if (CSTREAM && warp >= 4 && lane == 0) bulk_wait<0>();  // D stores complete before exit
+  if (CSTREAM && warp >= 4 && lane == 0) bulk_wait_read<0>();  // ring read; grid completion performs the stores
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {

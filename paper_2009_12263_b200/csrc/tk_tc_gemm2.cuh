@@ -46,16 +46,20 @@ constexpr int TC2S_SMEM = TC2S_BAR_OFFSET + 512 + 1024;
 // CSL = C-ring slots per epilogue warp (streamed-C variant): 2 in general; 4 for single-wave
 // launches, where every 32-column C box of the tile is prefetched during the mainloop and the
 // drain never waits on a C load (3 operand stages make room).
-template <int NSUB, bool CSTREAM, int BNI = 256, int CSL = TC2S_CSLOTS>
+// KPS = K-blocks (of 64) per ring stage: 2 for the narrow single-wave tiles (BNI 64 / 128), so
+// each barrier round trip (full -> MMAs -> commit -> empty -> TMA) carries twice the operand
+// bytes; a stage is then two self-contained K-block halves [A kb][B kb][A kb+1][B kb+1].
+template <int NSUB, bool CSTREAM, int BNI = 256, int CSL = TC2S_CSLOTS, int KPS = 1>
 struct Tc2Plan {
   static constexpr int B_BYTES = BNI * 64;  // BNI/2 columns x 64 K x 2 bytes per CTA per MMA
-  static constexpr int STAGE_BYTES = TC2_TILE_BYTES + NSUB * B_BYTES;
+  static constexpr int KB_BYTES = TC2_TILE_BYTES + NSUB * B_BYTES;  // one K-block's operands
+  static constexpr int STAGE_BYTES = KPS * KB_BYTES;
   static constexpr int CSLOTS = CSL;
   static constexpr int CRING_BYTES = CSTREAM ? TC_EPI_WARPS * CSL * TC_CBOX_BYTES : 0;
   static constexpr int MAX_STAGES = (226 * 1024 - 1536 - CRING_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = NSUB == 2 ? (CSTREAM ? (CSL > TC2S_CSLOTS ? MAX_STAGES : 3) : 4)
                               : CSL > TC2S_CSLOTS ? (MAX_STAGES > 8 ? 8 : MAX_STAGES)
-                              : BNI == 256 ? (CSTREAM ? TC2S_STAGES : TC2_STAGES)
+                              : (BNI == 256 && KPS == 1) ? (CSTREAM ? TC2S_STAGES : TC2_STAGES)
                               : (MAX_STAGES > 8 ? 8 : MAX_STAGES);
   static constexpr int CRING = STAGES * STAGE_BYTES;
   static constexpr int BAR_OFFSET = CRING + CRING_BYTES;
@@ -120,11 +124,12 @@ __device__ __forceinline__ void nsub2_step(int i, int K, int Xs, int Xe, int& kb
   else { kb = i - Xs - Xe; mask = 2; }
 }
 
-template <bool DENSE_EPI, bool CSTREAM = false, int NSUB = 1, int BNI = 256, int CSL = TC2S_CSLOTS>
+template <bool DENSE_EPI, bool CSTREAM = false, int NSUB = 1, int BNI = 256, int CSL = TC2S_CSLOTS, int KPS = 1>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     tc_gemm_pair_kernel(const __grid_constant__ TcParams p) {
-  using PL = Tc2Plan<NSUB, CSTREAM, BNI, CSL>;
+  using PL = Tc2Plan<NSUB, CSTREAM, BNI, CSL, KPS>;
   static_assert(NSUB == 1 || BNI == 256, "NSUB 2 uses 256-wide MMAs");
+  static_assert(KPS == 1 || NSUB == 1, "two K-blocks per stage: single-MMA tiles only (no predicate bits)");
   constexpr int STAGES = PL::STAGES;
   constexpr int BNP = PL::BNP;
   constexpr int NCBAR = CSTREAM ? TC_EPI_WARPS * CSL : 0;
@@ -192,7 +197,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
 
   auto a_tile = [&](int s) -> uint8_t* { return smem + s * PL::STAGE_BYTES; };
   auto b_tile = [&](int s) -> uint8_t* { return smem + s * PL::STAGE_BYTES + TC2_TILE_BYTES; };
-  constexpr int CH = PL::WCOLS / 32;  // 32-column chunks per epilogue warp per pass
+  constexpr int CH = PL::WCOLS / 32;
+  // KPS 2: steps of two K-blocks over [kb0, kb1) (the last one single if the count is odd),
+  // in reverse step order for serpentine tiles; ascending inside a step
+  auto kps_step = [&](const PairUnit& un, bool rev, int st, int& kb, int& cnt) {
+    const int nst = (un.kb1 - un.kb0 + 1) >> 1;
+    kb = un.kb0 + 2 * (rev ? nst - 1 - st : st);
+    cnt = un.kb1 - kb < 2 ? 1 : 2;
+  };  // 32-column chunks per epilogue warp per pass
 
   if (CSTREAM && warp == 3) {
     // ------------------------------------------------------------ C loader (both CTAs)
@@ -275,6 +287,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         // serpentine K: every other tile of a cluster walks K downwards, so the next
         // wave starts on the K-slices the previous one loaded last (still in L2)
         const bool rev = p.serp && (lu & 1);
+        if (KPS == 2) {
+          const int nst = (un.kb1 - un.kb0 + 1) >> 1;
+          for (int st = 0; st < nst; ++st) {
+            int kb, cnt;
+            kps_step(un, rev, st, kb, cnt);
+            mbar_wait(&empty[stage], phase ^ 1);
+            if (leader) mbar_arrive_expect_tx(&full[stage], uint32_t(2 * cnt * PL::KB_BYTES));
+            const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
+            for (int h = 0; h < cnt; ++h) {
+              const int k0 = (kb + h) * TC_BK;
+              uint8_t* at = a_tile(stage) + h * PL::KB_BYTES;
+              uint8_t* bt = at + TC2_TILE_BYTES;
+              if (a_mode == 0) {
+                tma_load_3d_pair(at, &p.ta[0], fb, 0, k0, m0 >> 6, pol);
+              } else if (a_mode == 1) {
+                tma_load_2d_pair(at, &p.ta[0], fb, m0, k0, pol);
+                tma_load_2d_pair(at + 8192, &p.ta[0], fb, m0 + 64, k0, pol);
+              } else {
+                tma_load_2d_pair(at, &p.ta[0], fb, k0, m0, pol);
+              }
+              if (b_mode == 0) {
+                tma_load_3d_pair(bt, &p.tb[0], fb, 0, k0, n0 >> 6, pol_b);
+              } else if (b_mode == 1) {
+                for (int hh = 0; hh < BNI / 128; ++hh)
+                  tma_load_2d_pair(bt + hh * 8192, &p.tb[0], fb, n0 + 64 * hh, k0, pol_b);
+              } else {
+                tma_load_2d_pair(bt, &p.tb[0], fb, k0, n0, pol_b);
+              }
+            }
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          }
+          continue;
+        }
         // NSUB 2 drain overlap (nsub2_step): lo-only / hi-only steps load one B half
         const int X = (NSUB == 2 && !un.narrow) ? p.ovl_kb : 0;
         const int Xs = u > 0 ? X : 0, Xe = u < nu - 1 ? X : 0;
@@ -376,7 +421,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           mbar_wait(&tempty[as], aphase ^ 1);
           tc_fence_after();
           const uint32_t d0 = tmem_base + uint32_t(as * BNI);
-          if (!p.kbits) {
+          if (KPS == 2) {
+            const bool rev = p.serp && (local & 1);
+            const int nst = (un.kb1 - un.kb0 + 1) >> 1;
+            for (int st = 0; st < nst; ++st) {
+              int kb, cnt;
+              kps_step(un, rev, st, kb, cnt);
+              mbar_wait(&full[stage], phase);
+              if (local == 0 && st == 0) TK_TS(2);
+              tc_fence_after();
+              const uint32_t so = uint32_t(stage) * uint32_t(PL::STAGE_BYTES >> 4);
+              for (int h = 0; h < cnt; ++h) {
+                const uint32_t ho = so + uint32_t(h * (PL::KB_BYTES >> 4));
+#pragma unroll
+                for (int kk = 0; kk < TC_BK / 16; ++kk)
+                  tc_mma_f16_pair(d0, a_desc0 + ho + kk * a_kk, b_desc0 + ho + kk * b_kk, idesc,
+                                  (st > 0 || h > 0 || kk > 0) ? 1u : 0u);
+              }
+              tc_commit_pair(&empty[stage], 0x3);
+              if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            }
+          } else if (!p.kbits) {
             for (int kb = un.kb0; kb < un.kb1; ++kb) {  // (operand order is the producer's)
               mbar_wait(&full[stage], phase);
               if (local == 0 && kb == un.kb0) TK_TS(2);
@@ -635,8 +700,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
   }
 
   if (CSTREAM && warp >= 4 && lane == 0) {
-    bulk_wait<0>();
-    if (p.npeer) __threadfence_system();  // peer slabs complete before the grid retires
+    if (p.npeer) {  // peer slabs complete before the grid retires
+      bulk_wait<0>();
+      __threadfence_system();
+    } else {
+      bulk_wait_read<0>();  // the ring slots are read; grid completion performs the stores
+    }
   }
   if (warp == 4 && lane == 0) TK_TS(6);
   if (blockIdx.x == 0 && threadIdx.x == 0) {

@@ -41,17 +41,20 @@ def _f32(x):
     return np.asarray(x).astype(np.float32)
 
 
-@pytest.fixture(params=["single", "pair", "pair128", "pair64", "pair512", "quad", "stream"])
+@pytest.fixture(params=["single", "pair", "pair128", "pair64", "pair64k1", "pair512", "quad", "stream"])
 def tc_kernel(request, knob):
-    """Pin the single-CTA (128x256), CTA-pair (256 x 256/128/64 tiles, or 256 x 512 with two
-    MMAs per K step), 4-CTA multicast or C-streaming tcgen05 kernel."""
+    """Pin the single-CTA (128x256), CTA-pair (256 x 256/128/64 tiles -- the narrow ones with two
+    K-blocks per ring stage, `k1` one -- or 256 x 512 with two MMAs per K step), 4-CTA multicast
+    or C-streaming tcgen05 kernel."""
     name = request.param
     if name.startswith("pair") and name != "pair":
         knob("TK_TC_KERNEL", "pair")
         if name == "pair512":
             knob("TK_PAIR_NSUB", "2")
         else:
-            knob("TK_PAIR_BNI", name[4:])
+            knob("TK_PAIR_BNI", name[4:].split("k")[0])
+            if name.endswith("k1"):
+                knob("TK_PAIR_KPS", "1")
     else:
         knob("TK_TC_KERNEL", name)
     return name
@@ -96,6 +99,35 @@ def test_dense_random_within_tolerance(cuda, dtype, mnk, tc_kernel):
     exact = O.exact_gemm(_f32(a), _f32(b), c, beta=1.0)
     assert O.rel_err(got, want) <= O.tolerance(k), O.rel_err(got, want)
     assert O.rel_err(got, exact) <= O.tolerance(k), O.rel_err(got, exact)
+
+
+@pytest.mark.parametrize("bni", ["64", "128"])
+@pytest.mark.parametrize("kps", ["1", "2"])
+@pytest.mark.parametrize("grid", ["3", "0"])
+def test_narrow_tiles_ring_stages(cuda, bni, kps, grid, knob):
+    """Narrow pair tiles with one or two K-blocks per ring stage: an odd K-block count (the last
+    stage half-filled), several tiles per cluster (TK_PAIR_GRID=3: serpentine K order and ring
+    phases carried across tiles), MN-major A and B -- bitwise on integers, plan as requested."""
+    knob("TK_TC_KERNEL", "pair")
+    knob("TK_PAIR_BNI", bni)
+    knob("TK_PAIR_KPS", kps)
+    if grid != "0":
+        knob("TK_PAIR_GRID", grid)
+    rng = np.random.default_rng(5)
+    for (m, n, k, ta, tb) in [(768, 640, 7 * 64 + 24, False, False), (512, 384, 9 * 64, True, False),
+                              (256, 512, 3 * 64, False, bni == "128")]:
+        a = _half(rng, (m, k), np.float16, True)
+        b = _half(rng, (k, n), np.float16, True)
+        c = rng.integers(-4, 5, (m, n)).astype(np.float32)
+        cfg = tk.build_dense_config(m, n, k, np.float16, trans_a=ta, trans_b=tb)
+        d = torch.zeros(m * n, dtype=torch.float32, device=cuda)
+        tk.matmul(cfg, _dev(a.T) if ta else _dev(a), _dev(b.T) if tb else _dev(b), _dev(c), d)
+        plan = tk.last_run()["plan"]
+        assert plan["kernel"] == "pair" and plan["mma_n"] == int(bni), plan
+        assert plan["tile_k"] == 64 * int(kps), plan
+        got = _host(d, (m, n))
+        want = O.gemm_real(_f32(a), _f32(b), c)
+        assert np.array_equal(got, want), (m, n, k, float(np.abs(got - want).max()))
 
 
 _SPLITK_WANT = {}
