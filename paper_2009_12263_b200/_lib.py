@@ -151,11 +151,21 @@ def tune(name: str, value=None) -> None:
     rc = load().tk_tune_set(name.encode(), None if value is None else str(value).encode())
     if rc != TK_OK:
         raise ValueError(last_error())
+    _drop_prepared()
+
+
+def _drop_prepared() -> None:
+    """Knobs can change the kernel choice and so the workspace a plan needs: forget the lowered
+    configurations (kernel._PREPARED) so the next call re-queries tk_workspace_bytes."""
+    from . import kernel
+
+    kernel._PREPARED.clear()
 
 
 def tune_reset() -> None:
     """Drop every override: knobs return to the values the environment gives."""
     load().tk_tune_reset()
+    _drop_prepared()
 
 
 def tune_get(name: str):

@@ -64,7 +64,7 @@ enum Knob {
   K_SPLITK_S, K_SK_TMA, K_PDL, K_MN3D, K_PAIR_CSTREAM, K_PAIR_DTMA, K_C_PF, K_C_PF_SPREAD,
   K_NSUB2_CSL, K_STAGGER, K_PAIR_GRID, K_PAIR_DEEPC, K_PAIROPS_BN, K_DIAG_STREAM, K_D_TMA,
   K_L2_PROMO, K_POLICY_AB, K_POL_A, K_POL_B, K_PAIR_CLUSTERS, K_EX_SLABS, K_VERBOSE,
-  K_NSUB2_OVERLAP, K_PAIR_KPS,
+  K_NSUB2_OVERLAP, K_PAIR_KPS, K_CPLX_EMBED,
   K_DBG_C_ZERO, K_DBG_SKIP_EPI, K_DBG_NO_LOAD, K_DBG_NO_MMA, K_DBG_CTA, K_COUNT
 };
 constexpr int K_FIRST_DIAG = K_DBG_C_ZERO;
@@ -74,7 +74,7 @@ const char* const kKnobNames[K_COUNT] = {
   "TK_PAIR_DTMA", "TK_C_PF", "TK_C_PF_SPREAD", "TK_NSUB2_CSL", "TK_STAGGER", "TK_PAIR_GRID",
   "TK_PAIR_DEEPC", "TK_PAIROPS_BN", "TK_DIAG_STREAM", "TK_D_TMA", "TK_L2_PROMO", "TK_POLICY_AB",
   "TK_POL_A", "TK_POL_B", "TK_PAIR_CLUSTERS", "TK_EX_SLABS", "TK_VERBOSE", "TK_NSUB2_OVERLAP",
-  "TK_PAIR_KPS", "TK_DBG_C_ZERO", "TK_DBG_SKIP_EPI", "TK_DBG_NO_LOAD", "TK_DBG_NO_MMA", "TK_DBG_CTA"};
+  "TK_PAIR_KPS", "TK_CPLX_EMBED", "TK_DBG_C_ZERO", "TK_DBG_SKIP_EPI", "TK_DBG_NO_LOAD", "TK_DBG_NO_MMA", "TK_DBG_CTA"};
 #ifdef TK_DIAG
 constexpr int K_ENABLED = K_COUNT;
 #else
@@ -263,6 +263,63 @@ bool tma_operand(const TkLayout& L, int& mn_major_dim0, int64_t& pitch) {
   return true;
 }
 
+// ---- complex embedding (tc_gemm_pair_kernel<..., EMB>): an interleaved complex GEMM run as
+// the real GEMM D^ = A~ B^ + C^ over the interleaved buffers read as real matrices (2M x N,
+// 2K x N; A~ built on chip from A^ = A as a 2M x K real matrix).  Taken when every operand is a
+// dense column-major interleaved pair buffer TMA can read, the epilogue is real-separable
+// (empty or real-scale transforms, no bias, no predicate) and the shape fills CTA-pair tiles.
+bool cplx_col(const TkLayout& L, int64_t& ld) {
+  if (L.kind != TK_LAYOUT_STRIDED || L.pair != TK_PAIR_INTERLEAVED || L.ndigits[0] != 1 || L.ndigits[1] != 1)
+    return false;
+  if (L.stride[0][0] != 1 || L.stride[1][0] < L.ext[0][0]) return false;
+  ld = L.stride[1][0];
+  return true;
+}
+bool real_scale_only(const TkTransform& t) {
+  for (int i = 0; i < t.n; ++i)
+    if (t.op[i] != TK_T_SCALE || t.im[i] != 0.0) return false;
+  return true;
+}
+bool embed_ok(const TkGemmPlan* p) {
+  if (p->op != TK_OP_COMPLEX || p->compute != TK_F32 || !is_half(p->a.scalar)) return false;
+  if (p->t_a.n || p->t_b.n || p->bias_axis || p->predicate != TK_PRED_ALWAYS) return false;
+  if (!real_scale_only(p->t_c) || !real_scale_only(p->t_r2s) || !real_scale_only(p->t_s2g)) return false;
+  int64_t lda, ldb, ldc = 0, ldd;
+  if (!cplx_col(p->a, lda) || !cplx_col(p->b, ldb) || !cplx_col(p->d, ldd)) return false;
+  if (p->c.kind != TK_LAYOUT_ZERO && !cplx_col(p->c, ldc)) return false;
+  // 16-byte TMA pitches (2*ld halves for A^ / B^, 2*ld floats for C^ / D^), 64-row A^ chunks,
+  // and enough of a problem for the CTA-pair tiles (2M >= 256 rows, > 4 block-K steps of 2K)
+  if ((lda * 4) % 16 || (ldb * 4) % 16 || (ldc * 8) % 16 || (ldd * 8) % 16) return false;
+  if (p->m % 32 || p->m < 128 || p->k <= 128) return false;
+  if (2 * p->m >= (1ll << 31) || 2 * p->k >= (1ll << 31)) return false;
+  return knob(K_CPLX_EMBED, 1) != 0;
+}
+void real_col(TkLayout& L, int64_t rows, int64_t cols, int64_t ld) {
+  const int scalar = L.scalar, kind = L.kind;
+  memset(&L, 0, sizeof(L));
+  L.kind = kind;
+  L.scalar = scalar;
+  if (kind == TK_LAYOUT_ZERO) return;
+  L.ndigits[0] = L.ndigits[1] = 1;
+  L.ext[0][0] = rows;
+  L.ext[1][0] = cols;
+  L.stride[0][0] = 1;
+  L.stride[1][0] = ld;
+  L.size = ld * (cols - 1) + rows;
+}
+// The real plan of the embedding: M' = 2M, K' = 2K; A describes A^ (2M x K, the kernel's
+// staging source), B^ / C^ / D^ the interleaved buffers as real column-major matrices.
+void embed_plan(const TkGemmPlan* p, TkGemmPlan* out) {
+  *out = *p;
+  out->op = TK_OP_REAL;
+  out->m = 2 * p->m;
+  out->k = 2 * p->k;
+  real_col(out->a, 2 * p->m, p->k, 2 * p->a.stride[1][0]);
+  real_col(out->b, 2 * p->k, p->n, 2 * p->b.stride[1][0]);
+  if (p->c.kind != TK_LAYOUT_ZERO) real_col(out->c, 2 * p->m, p->n, 2 * p->c.stride[1][0]);
+  real_col(out->d, 2 * p->m, p->n, 2 * p->d.stride[1][0]);
+}
+
 // A half-precision strided operand the TMA cannot read directly (multi-digit permutations,
 // non-unit innermost strides, non-bijective interleaved pairs) is gathered once into a dense
 // column-major workspace by pack_half_kernel and then takes the normal tensor-core path.
@@ -423,6 +480,7 @@ Workspace plan_workspace(const TkGemmPlan* p0, int lane) {
     dense_operand(packed.b, p->k, p->n);
   }
   p = &packed;
+  if (embed_ok(p0)) return w;  // complex embedding: interleaved operands are read in place
   if (p->a.kind == TK_LAYOUT_STRIDED && p->a.pair == TK_PAIR_INTERLEAVED) {
     w.a_planes = w.total;
     w.total += align256(p->m * p->k * 2 * 2);
@@ -475,7 +533,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 int make_map_2d(CUtensorMap* map, const void* base, int scalar, uint64_t inner, uint64_t outer,
-                uint64_t pitch_elems, uint32_t box_inner, uint32_t box_outer) {
+                uint64_t pitch_elems, uint32_t box_inner, uint32_t box_outer, bool swizzle = true) {
   auto enc = get_encode();
   if (!enc) return fail(TK_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const bool f32 = scalar == TK_F32;
@@ -488,7 +546,7 @@ int make_map_2d(CUtensorMap* map, const void* base, int scalar, uint64_t inner, 
                                                         : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   CUresult r = enc(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   f32 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
+                   (f32 || !swizzle) ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
                    l2_promo(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(TK_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
   return TK_OK;
@@ -593,10 +651,12 @@ int launch_tc_variant(const tk::TcParams& prm, cudaStream_t s) {
   return TK_OK;
 }
 
-template <bool DENSE, bool CSTREAM = false, int NSUB = 1, int BNI = 256, int CSL = tk::TC2S_CSLOTS, int KPS = 1>
+template <bool DENSE, bool CSTREAM = false, int NSUB = 1, int BNI = 256, int CSL = tk::TC2S_CSLOTS, int KPS = 1,
+          bool EMB = false>
 int launch_tc_pair(const tk::TcParams& prm, cudaStream_t s) {
-  constexpr int SMEM = tk::Tc2Plan<NSUB, CSTREAM, BNI, CSL, KPS>::SMEM;
-  auto kern = tk::tc_gemm_pair_kernel<DENSE, CSTREAM, NSUB, BNI, CSL, KPS>;
+  constexpr int SMEM = tk::Tc2Plan<NSUB, CSTREAM, BNI, CSL, KPS, EMB>::SMEM;
+  constexpr int THREADS = tk::Tc2Plan<NSUB, CSTREAM, BNI, CSL, KPS, EMB>::THREADS;
+  auto kern = tk::tc_gemm_pair_kernel<DENSE, CSTREAM, NSUB, BNI, CSL, KPS, EMB>;
   static bool attr[TK_MAX_DEV] = {};
   static int max_clusters_dev[TK_MAX_DEV] = {};
   const int dev = cur_dev();
@@ -608,7 +668,7 @@ int launch_tc_pair(const tk::TcParams& prm, cudaStream_t s) {
   if (!max_clusters) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * (sm_count() / 2));
-    cfg.blockDim = dim3(tk::TC_THREADS);
+    cfg.blockDim = dim3(THREADS);
     cfg.dynamicSmemBytes = SMEM;
     cudaLaunchAttribute at;
     at.id = cudaLaunchAttributeClusterDimension;
@@ -655,7 +715,7 @@ int launch_tc_pair(const tk::TcParams& prm, cudaStream_t s) {
   run.pdl = (pdl && run.sk_parts == 1) ? 1 : 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(tk::TC_THREADS);
+  cfg.blockDim = dim3(THREADS);
   cfg.dynamicSmemBytes = SMEM;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
@@ -665,8 +725,8 @@ int launch_tc_pair(const tk::TcParams& prm, cudaStream_t s) {
   cfg.numAttrs = run.pdl ? 1 : 0;
   TK_CUDA(cudaLaunchKernelEx(&cfg, kern, run));
   ++g_launches;
-  using PL = tk::Tc2Plan<NSUB, CSTREAM, BNI, CSL, KPS>;
-  info_kernel("pair");
+  using PL = tk::Tc2Plan<NSUB, CSTREAM, BNI, CSL, KPS, EMB>;
+  info_kernel(EMB ? "pair_cembed" : "pair");
   g_info.tile_m = 256;
   g_info.tile_k = 64 * KPS;
   g_info.tile_n = PL::BNP;
@@ -940,6 +1000,14 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
            const uint8_t* kmask, uint8_t* ws, const Workspace& w, cudaStream_t s) {
   TkGemmPlan rewritten;
   const TkGemmPlan* p = p0;
+  // complex embedding: from here on a real plan (M' = 2M, K' = 2K); A^ streams into the
+  // kernel's staging ring and the transform warps build A~ on chip
+  TkGemmPlan embedded;
+  const bool emb = embed_ok(p0);
+  if (emb) {
+    embed_plan(p0, &embedded);
+    p = p0 = &embedded;
+  }
   if (w.a_perm >= 0 && permuted_plan(p0, &rewritten)) {
     // A's two M digits swapped (m' = m1 + e1*m0) and gathered into a dense M' x K workspace
     TkLayout A = p0->a;
@@ -1033,7 +1101,14 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
   const void* b_plane0 = b;
   const void* planes_a[2] = {a, nullptr};
   const void* planes_b[2] = {b, nullptr};
-  if (p->a.kind == TK_LAYOUT_DIAGONAL) {
+  if (emb) {
+    // A^ (2M x K halves, pitch 2*lda) in 128-row x 32-k boxes, unswizzled, for the staging ring
+    prm.a_mn = 1;
+    prm.a_embed = 1;
+    int rc = make_map_2d(&prm.ta[0], a, p->a.scalar, p->m, p->k / 2, p->a.stride[1][0], 128, 32,
+                         /*swizzle=*/false);
+    if (rc) return rc;
+  } else if (p->a.kind == TK_LAYOUT_DIAGONAL) {
     prm.diag_a = 1;
     prm.diag = a;
   } else {
@@ -1184,7 +1259,7 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
     }
   }
   const bool pred_tc = w.kbits >= 0;  // block predicate: the CTA-pair kernel evaluates it
-  if (op == TK_OP_REAL && dense && !rmapped && !pred_tc &&
+  if (op == TK_OP_REAL && dense && !rmapped && !pred_tc && !emb &&
       (ov == 3 || (ov == 0 && (prm.diag_a || prm.kb_total <= 4 || (single_wave && !pair_ok))))) {
     const bool cs = prm.c_zero || ((prm.ldc * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(c) & 15) == 0);
     if (cs) {
@@ -1200,7 +1275,7 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
   }
   if (op == TK_OP_REAL && !prm.diag_a) {
     // CTA pair (256x256 tiles) once there are enough pair tiles to cover the SMs
-    if (ov == 4 && !pred_tc) {
+    if (ov == 4 && !pred_tc && !emb) {
       tk::TcParams pp = prm;
       pp.num_mb = int((p->m + 511) / 512);
       pp.num_nb = int((p->n + tk::TC2_BN - 1) / tk::TC2_BN);
@@ -1212,7 +1287,7 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
       if (mn && (rc = make_map_2d(&pp.tb[0], b_plane0, p->b.scalar, p->k, p->n, pitch, 64, 64))) return rc;
       return dense ? launch_tc_quad<true>(pp, s) : launch_tc_quad<false>(pp, s);
     }
-    if (ov == 2 || (ov == 0 && pair_ok) || pred_tc) {
+    if (ov == 2 || (ov == 0 && pair_ok) || pred_tc || emb) {
       tk::TcParams pp = prm;
       // 256 x 512 pair tiles (two MMAs share each A tile: 25 % fewer L2->SM bytes per flop, so
       // more flops per joule under the power cap) once K is long enough to amortise their
@@ -1226,7 +1301,7 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
       int64_t pitch;
       int rc;
       tma_operand(p->b, mn, pitch);
-      const int bni = pred_tc ? pred_bni(p) : nsub == 2 ? 256 : choose_pair_bni(p->m, p->n, /*b_mn_major=*/!mn, pair_clusters());
+      const int bni = pred_tc ? pred_bni(p) : (nsub == 2 || emb) ? 256 : choose_pair_bni(p->m, p->n, /*b_mn_major=*/!mn, pair_clusters());
       pp.num_mb = int((p->m + 255) / 256);
       pp.num_nb = int((p->n + bni * nsub - 1) / (bni * nsub));
       pp.num_tiles = pp.num_mb * pp.num_nb;
@@ -1248,13 +1323,13 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
         // Opt-in: bitwise equal, but measured 3-6 % slower (8192^3, 16384^3, 8192x16384x8192)
         // -- under the power cap the overlapped drains raise average power and lower clocks.
         const int P = pair_clusters(), S = P / 2;
-        if (knob(K_STAGGER, 0) && pp.num_tiles >= 2 * P) {
+        if (knob(K_STAGGER, 0) && pp.num_tiles >= 2 * P && !emb) {
           pp.nar_units = S;
           pp.num_units = pp.num_tiles + S;  // (>= P: the grid is all P clusters)
         }
         // drain overlap (nsub2_step in tk_tc_gemm2.cuh): 16 lo-only + 16 hi-only k-block steps
         // at each tile boundary hide the half-accumulator drains under MMAs
-        pp.ovl_kb = pp.nar_units ? 0 : std::max(0, std::min(knob(K_NSUB2_OVERLAP, 16), pp.kb_total / 4));
+        pp.ovl_kb = (pp.nar_units || emb) ? 0 : std::max(0, std::min(knob(K_NSUB2_OVERLAP, 16), pp.kb_total / 4));
       }
       if (nsub == 1 && dense && w.splitk >= 0 && !knob_set(K_PAIR_GRID)) {
         const SplitPlan sp = split_plan(pp.num_tiles, pair_clusters(), pp.kb_total, bni);
@@ -1268,15 +1343,17 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
         }
       }
       // per-CTA halves: A box 128 rows / B box bni/2 columns
-      tma_operand(p->a, mn, pitch);
       pp.mn3d = 0;
       const bool use3d = knob(K_MN3D, 1) != 0;
-      // MN-major A (M % 64 == 0 so atoms never straddle the M edge): one 3-D box per stage
-      if (mn && use3d && p->m % 64 == 0) {
-        if ((rc = make_map_mn3d(&pp.ta[0], a_plane0, p->a.scalar, p->m, p->k, pitch, 2))) return rc;
-        pp.mn3d |= 1;
+      if (!emb) {  // (embedding: ta[0] is the A^ staging map)
+        tma_operand(p->a, mn, pitch);
+        // MN-major A (M % 64 == 0 so atoms never straddle the M edge): one 3-D box per stage
+        if (mn && use3d && p->m % 64 == 0) {
+          if ((rc = make_map_mn3d(&pp.ta[0], a_plane0, p->a.scalar, p->m, p->k, pitch, 2))) return rc;
+          pp.mn3d |= 1;
+        }
+        if (!mn && (rc = make_map_2d(&pp.ta[0], a_plane0, p->a.scalar, p->k, p->m, pitch, 64, 128))) return rc;
       }
-      if (!mn && (rc = make_map_2d(&pp.ta[0], a_plane0, p->a.scalar, p->k, p->m, pitch, 64, 128))) return rc;
       tma_operand(p->b, mn, pitch);
       if (mn && (rc = make_map_2d(&pp.tb[0], b_plane0, p->b.scalar, p->k, p->n, pitch, 64, bni / 2))) return rc;
       if (!mn && use3d && p->n % 64 == 0) {
@@ -1313,6 +1390,9 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
             pp.sk_tma = 1;
           }
         }
+        if (emb)
+          return nsub == 2 ? launch_tc_pair<true, true, 2, 256, tk::TC2S_CSLOTS, 1, true>(pp, s)
+                           : launch_tc_pair<true, true, 1, 256, tk::TC2S_CSLOTS, 1, true>(pp, s);
         if (nsub == 2) {
           const int csl = knob(K_NSUB2_CSL, 2);  // C-ring slots per warp (tuning)
           if (csl == 3) return launch_tc_pair<true, true, 2, 256, 3>(pp, s);
@@ -1321,6 +1401,9 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
         }
         return launch_tc_pair_bni<true, true>(pp, bni, s);
       }
+      if (emb)  // (C / D not TMA-aligned: register epilogue)
+        return nsub == 2 ? launch_tc_pair<true, false, 2, 256, tk::TC2S_CSLOTS, 1, true>(pp, s)
+                         : launch_tc_pair<true, false, 1, 256, tk::TC2S_CSLOTS, 1, true>(pp, s);
       if (nsub == 2) return dense ? launch_tc_pair<true, false, 2>(pp, s) : launch_tc_pair<false, false, 2>(pp, s);
       return dense ? launch_tc_pair_bni<true, false>(pp, bni, s) : launch_tc_pair_bni<false, false>(pp, bni, s);
     }

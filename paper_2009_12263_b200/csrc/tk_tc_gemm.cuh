@@ -125,7 +125,8 @@ struct TcParams {
   // components.py:171-191, kernel.py:399-404): kbits[tile * kwords + kb / 8] holds 4 bits per
   // 64-deep k-block, one per K=16 MMA step (expand_kbits_kernel); null = every step runs
   const uint32_t* kbits;
-  int32_t kwords, pad9;
+  int32_t kwords;
+  int32_t a_embed;  // complex embedding: ta[0] maps A^ for the staging ring (tc_gemm_pair_kernel EMB)
 };
 
 // the 4 MMA-step bits of k-block kb of pair tile `tile` (0xF without a predicate)

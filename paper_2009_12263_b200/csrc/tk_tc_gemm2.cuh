@@ -49,7 +49,13 @@ constexpr int TC2S_SMEM = TC2S_BAR_OFFSET + 512 + 1024;
 // KPS = K-blocks (of 64) per ring stage: 2 for the narrow single-wave tiles (BNI 64 / 128), so
 // each barrier round trip (full -> MMAs -> commit -> empty -> TMA) carries twice the operand
 // bytes; a stage is then two self-contained K-block halves [A kb][B kb][A kb+1][B kb+1].
-template <int NSUB, bool CSTREAM, int BNI = 256, int CSL = TC2S_CSLOTS, int KPS = 1>
+//
+// EMB (complex embedding, see tc_gemm_pair_kernel): the producer lands a raw interleaved A box
+// (128 rows x 32 complex k, 8 KB) in the upper half of each A slot; two transform warps expand it
+// in place into the stage's A~ tile.
+constexpr int EMB_RAW_BYTES = 128 * 32 * 2;
+constexpr int EMB_THREADS = TC_THREADS + 64;  // + 2 transform warps (12, 13)
+template <int NSUB, bool CSTREAM, int BNI = 256, int CSL = TC2S_CSLOTS, int KPS = 1, bool EMB = false>
 struct Tc2Plan {
   static constexpr int B_BYTES = BNI * 64;  // BNI/2 columns x 64 K x 2 bytes per CTA per MMA
   static constexpr int KB_BYTES = TC2_TILE_BYTES + NSUB * B_BYTES;  // one K-block's operands
@@ -67,6 +73,8 @@ struct Tc2Plan {
   static constexpr int BNP = BNI * NSUB;                       // pair tile N
   static constexpr int TMEM_COLS = NSUB == 2 ? 512 : 2 * BNI;  // double-buffered for NSUB 1
   static constexpr int WCOLS = BNI / 2;                        // columns per epilogue warp per pass
+  static constexpr int THREADS = EMB ? EMB_THREADS : TC_THREADS;
+  static_assert(SMEM <= 227 * 1024, "pair kernel shared memory");
 };
 
 // One unit of the pair kernel's static schedule: a whole tile, or K-part `part` of a split tile
@@ -124,10 +132,22 @@ __device__ __forceinline__ void nsub2_step(int i, int K, int Xs, int Xe, int& kb
   else { kb = i - Xs - Xe; mask = 2; }
 }
 
-template <bool DENSE_EPI, bool CSTREAM = false, int NSUB = 1, int BNI = 256, int CSL = TC2S_CSLOTS, int KPS = 1>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
+// Complex embedding (EMB): an interleaved complex GEMM (reference ComplexOperator over
+// InterleavedComplex A/B/C/D, operators.py:140-163, layouts.py:315-394) run as the real GEMM
+//   D^ (2M x N) = A~ (2M x 2K) * B^ (2K x N) + C^,
+// where X^ is the interleaved buffer read as a plain real column-major matrix (row 2i+c /
+// k-row 2k+c = component c of element i / k) and A~ holds A^'s column k at k-row 2k and J A^ at
+// k-row 2k+1, J(x_re, x_im) = (-x_im, x_re):  D^[2i] = sum Ar Br - Ai Bi, D^[2i+1] = sum Ai Br + Ar Bi.
+// B^, C^ and D^ need no preparation (TMA reads the interleaved buffers as they are); A~ is built
+// in shared memory by two transform warps from raw A^ boxes that the producer streams through a
+// staging ring -- no de-interleave pass over HBM.  The peer CTA's A~ stage is announced to the
+// leader's full barrier by a 16-byte bulk copy (async proxy, complete_tx on the leader's barrier).
+template <bool DENSE_EPI, bool CSTREAM = false, int NSUB = 1, int BNI = 256, int CSL = TC2S_CSLOTS, int KPS = 1,
+          bool EMB = false>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EMB ? EMB_THREADS : TC_THREADS, 1)
     tc_gemm_pair_kernel(const __grid_constant__ TcParams p) {
-  using PL = Tc2Plan<NSUB, CSTREAM, BNI, CSL, KPS>;
+  using PL = Tc2Plan<NSUB, CSTREAM, BNI, CSL, KPS, EMB>;
+  static_assert(!EMB || (KPS == 1 && BNI == 256 && DENSE_EPI), "complex embedding: 256-wide tiles, dense epilogue");
   static_assert(NSUB == 1 || BNI == 256, "NSUB 2 uses 256-wide MMAs");
   static_assert(KPS == 1 || NSUB == 1, "two K-blocks per stage: single-MMA tiles only (no predicate bits)");
   constexpr int STAGES = PL::STAGES;
@@ -144,6 +164,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
   uint64_t* cempty = cfull + NCBAR;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + NCBAR);
   float* cring = reinterpret_cast<float*>(smem + PL::CRING);
+  // EMB: per-stage raw-A barriers (local) and the 16-byte relay slot, past the other barriers
+  uint64_t* afull = reinterpret_cast<uint64_t*>(smem + PL::BAR_OFFSET + 384);
+  uint8_t* relay = smem + PL::BAR_OFFSET + 448;
+  static_assert(!EMB || STAGES <= 8, "EMB barrier slots");
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -161,7 +185,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], EMB ? 2 : 1);  // EMB: + the leader's transform arrival
       mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
@@ -172,6 +196,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       mbar_init(&cfull[s], 1);
       mbar_init(&cempty[s], 1);
     }
+    if (EMB)
+      for (int s = 0; s < STAGES; ++s) mbar_init(&afull[s], 1);
     fence_mbar_init();
   }
   if (warp == 2) {
@@ -330,8 +356,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           const int kb = rev ? un.kb1 - 1 - kq : un.kb0 + kq;
           if (NSUB == 1 && !kmask4(p, un.tile, kb)) continue;  // predicate: k-block skipped entirely
           const int k0 = kb * TC_BK;
-          const uint32_t tx = 2 * (TC2_TILE_BYTES + __popc(mask) * PL::B_BYTES);
+          // (EMB: A arrives from the transform warps; +16 bytes: the peer's relay copy)
+          const uint32_t tx = EMB ? 2 * __popc(mask) * PL::B_BYTES + 16
+                                  : 2 * (TC2_TILE_BYTES + __popc(mask) * PL::B_BYTES);
           mbar_wait(&empty[stage], phase ^ 1);
+          if (EMB) {  // raw A^ box (128 rows x 32 complex k) into the upper half of the A slot
+            mbar_arrive_expect_tx(&afull[stage], EMB_RAW_BYTES);
+            tma_load_2d(a_tile(stage) + 8192, &p.ta[0], &afull[stage], m0, kb * (TC_BK / 2), pol);
+          }
           if (no_load) {  // diagnostic: MMA issue rate without operand traffic
             if (leader) mbar_arrive(&full[stage]);
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -358,7 +390,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           }
           if (leader) mbar_arrive_expect_tx(&full[stage], tx);
           const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
-          if (a_mode == 0) {
+          if (EMB) {
+          } else if (a_mode == 0) {
             tma_load_3d_pair(a_tile(stage), &p.ta[0], fb, 0, k0, m0 >> 6, pol);
           } else if (a_mode == 1) {
             tma_load_2d_pair(a_tile(stage), &p.ta[0], fb, m0, k0, pol);
@@ -544,6 +577,58 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         }
       }
     }
+  } else if (EMB && warp >= 4 + TC_EPI_WARPS) {
+    // ------------------------------------------------------------ A~ transform (both CTAs)
+    // The raw A^ box of a stage (k-row k = 256 bytes: rows [0,64) then [64,128)) sits in the upper
+    // 8 KB of the A slot.  Warp h = 0 / 1 reads M-chunk h (64 rows) of it into registers, then
+    // (after both warps have read) writes A~ chunk h: A^ k-row k -> k-rows 2k (as is) and 2k+1
+    // (J per (re, im) 32-bit pair), in the 128B-swizzled MN-major layout the TMA would produce
+    // (chunk stride 8 KB, k-row r at r*128, 16-byte granule g at g ^ (r & 7)).
+    const int h = warp - 4 - TC_EPI_WARPS;
+    const int gg = lane & 7;
+    int stage = 0;
+    uint32_t phase = 0;
+    const uint32_t relay_dst = mapa_shared(smem_u32(relay), 0);
+    const int nu = unit_count(p, cluster, nclusters);
+    for (int u = 0; u < nu; ++u) {
+      const PairUnit un = unit_at(p, cluster, nclusters, u, nu);
+      for (int ki = un.kb0; ki < un.kb1; ++ki) {
+        mbar_wait(&afull[stage], phase);
+        const uint32_t at = smem_u32(a_tile(stage));
+        const uint32_t src = at + 8192u + uint32_t(h * 128 + gg * 16);
+        uint32_t v[8][4];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(v[j][0]), "=r"(v[j][1]), "=r"(v[j][2]), "=r"(v[j][3])
+                       : "r"(src + uint32_t(((lane >> 3) + 4 * j) * 256)));
+        asm volatile("bar.sync 1, 64;" ::: "memory");  // the raw box is read: overwrite it
+        const uint32_t dst = at + uint32_t(h * 8192);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int r0 = 2 * ((lane >> 3) + 4 * j), r1 = r0 + 1;
+          asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(dst + uint32_t(r0 * 128 + ((gg ^ (r0 & 7)) << 4))),
+                       "r"(v[j][0]), "r"(v[j][1]), "r"(v[j][2]), "r"(v[j][3]) : "memory");
+          auto jx = [](uint32_t w) { return __byte_perm(w, 0, 0x1032) ^ 0x8000u; };  // (re, im) -> (-im, re)
+          asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(dst + uint32_t(r1 * 128 + ((gg ^ (r1 & 7)) << 4))),
+                       "r"(jx(v[j][0])), "r"(jx(v[j][1])), "r"(jx(v[j][2])), "r"(jx(v[j][3])) : "memory");
+        }
+        fence_proxy_async_smem();  // the generic writes are read by tcgen05.mma (async proxy)
+        asm volatile("bar.sync 1, 64;" ::: "memory");
+        if (h == 0 && lane == 0) {
+          if (leader) {
+            mbar_arrive(&full[stage]);
+          } else {  // relay: complete_tx on the leader's full barrier through the async proxy
+            asm volatile(
+                "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], 16, [%2];" ::"r"(
+                    relay_dst),
+                "r"(smem_u32(relay)), "r"(mapa_shared(smem_u32(&full[stage]), 0))
+                : "memory");
+          }
+        }
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue (both CTAs)
     const int ew = warp - 4;
@@ -568,7 +653,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       float* sk_row = p.sk_ws ? p.sk_ws + (int64_t(un.sk_tile) * (p.sk_parts - 1) * 2 + int(rank)) * blk +
                                     row_local
                               : nullptr;
-      if (NSUB == 1 && un.role == 1) {
+      if (NSUB == 1 && !EMB && un.role == 1) {
         // K-part: raw FP32 accumulator -> workspace, then count this warp in
         const int as = local & 1;
         const uint32_t aphase = (local >> 1) & 1;
@@ -635,7 +720,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         continue;
       }
       SkIn sk{nullptr, 0, 0};
-      if (NSUB == 1 && un.role == 2) {
+      if (NSUB == 1 && !EMB && un.role == 2) {
         // last K-part: wait until every warp of every other part has published its partial
         // (with sk_tma the C loader waits and the partials arrive through the ring)
         if (lane == 0 && !(CSTREAM && p.sk_tma)) {
@@ -668,7 +753,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           TK_TS(4);
         }
         if (CSTREAM) {
-          if (sk.p)
+          if (!EMB && sk.p)
             epilogue_stream<PL::WCOLS, BNP, CSL, true>(p, tf, aphase, tb, i, jbase, lane, my_ring,
                                                    cfull + ew * CSL, cempty + ew * CSL, cq,
                                                    row0, sk, &smask);
@@ -680,7 +765,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           mbar_wait_sleep(tf, aphase);
           tc_fence_after();
         } else if (DENSE_EPI) {
-          if (sk.p)
+          if (!EMB && sk.p)
             epilogue_dense<OP_REAL, PL::WCOLS, BNP, true>(p, tf, aphase, tb, i, jbase, lane, sk);
           else
             epilogue_dense<OP_REAL, PL::WCOLS, BNP>(p, tf, aphase, tb, i, jbase, lane, SkIn{nullptr, 0, 0},
@@ -699,7 +784,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     }
   }
 
-  if (CSTREAM && warp >= 4 && lane == 0) {
+  if (CSTREAM && warp >= 4 && warp < 4 + TC_EPI_WARPS && lane == 0) {
     if (p.npeer) {  // peer slabs complete before the grid retires
       bulk_wait<0>();
       __threadfence_system();

@@ -370,6 +370,109 @@ def _unpack_pair(t, shape, split):
     return p0.reshape(shape, order="F"), p1.reshape(shape, order="F")
 
 
+def _complex_case(rng, m, n, k, half, integer, c_zero=False):
+    if integer:
+        g = lambda s: rng.integers(-4, 5, s).astype(np.float32)
+    else:
+        g = lambda s: rng.standard_normal(s).astype(np.float32)
+    q = (lambda x: x.astype(tk.BFLOAT16).astype(np.float32)) if half == "bf16" else \
+        (lambda x: x.astype(np.float16).astype(np.float32))
+    a = (q(g((m, k))), q(g((k, m)).T.copy()))
+    b = (q(g((k, n))), q(g((k, n))))
+    c = np.zeros((m, n), np.complex64) if c_zero else (g((m, n)) + 1j * g((m, n))).astype(np.complex64)
+    return a, b, c
+
+
+def _pack_half_pair(p0, p1, half):
+    """Interleaved pair buffer of f16 / bf16 halves (column-major) on the device."""
+    dt = tk.BFLOAT16 if half == "bf16" else np.float16
+    flat = np.stack([p0.astype(dt).ravel(order="F"), p1.astype(dt).ravel(order="F")], axis=1).ravel()
+    if half == "bf16":
+        return torch.from_numpy(flat.view(np.uint16)).view(torch.bfloat16).cuda()
+    return torch.from_numpy(flat).cuda()
+
+
+@pytest.mark.parametrize("half", ["f16", "bf16"])
+@pytest.mark.parametrize("nsub", ["1", "2"])
+@pytest.mark.parametrize("mnk", [(256, 384, 320), (512, 768, 1000), (384, 1280, 200)])
+def test_complex_embedding_interleaved(cuda, half, nsub, mnk, knob):
+    """Interleaved complex GEMM as the real embedding D^ = A~ B^ + C^ (tc_gemm_pair_kernel EMB):
+    A~ built on chip by the transform warps, no de-interleave pass (one launch); integer inputs
+    bitwise equal to the oracle and to the de-interleaving pair-operator kernel
+    (TK_CPLX_EMBED=0), random inputs within the complex bound (reference operators.py:140-163)."""
+    knob("TK_PAIR_NSUB", nsub)
+    m, n, k = mnk
+    rng = np.random.default_rng(11)
+    ht = tk.COMPLEXBF16 if half == "bf16" else tk.COMPLEX32
+    cfg = tk.build_complex_config(m, n, k, ht)
+    for integer in (True, False):
+        a, b, c = _complex_case(rng, m, n, k, half, integer)
+        cbuf = _pack_pair(c.real, c.imag, None, False)
+        outs = []
+        for embed in ("1", "0"):
+            knob("TK_CPLX_EMBED", embed)
+            d = torch.zeros_like(cbuf)
+            tk.matmul(cfg, _pack_half_pair(*a, half), _pack_half_pair(*b, half), cbuf, d)
+            run = tk.last_run()
+            assert run["lane"] == "tcgen05"
+            if embed == "1":
+                assert run["plan"]["kernel"] == "pair_cembed" and run["launches"] == 1, run["plan"]
+            else:
+                assert run["plan"]["kernel"] != "pair_cembed" and run["launches"] == 3, run["plan"]
+            outs.append(_unpack_pair(d, (m, n), False))
+        z = lambda x: np.asfortranarray((x[0] + 1j * x[1]).astype(np.complex64))
+        want = O.gemm_pair(z(a), z(b), np.asfortranarray(c))
+        got = outs[0]
+        if integer:
+            assert np.array_equal(got[0], want.real) and np.array_equal(got[1], want.imag)
+            assert all(np.array_equal(x, y) for x, y in zip(outs[0], outs[1]))
+        else:
+            err = max(O.rel_err(got[0], want.real), O.rel_err(got[1], want.imag))
+            assert err <= O.tolerance(k, 8.0), err
+
+
+def test_complex_embedding_gemm_ex_and_edges(cuda, knob):
+    """gemm_ex-style epilogues (alpha * (AB + beta/alpha * C), api.py:129-141): real alpha / beta
+    scale the real-separable epilogue (still the embedding), a complex alpha does not (the
+    pair-operator kernel); C / D at an 8-byte offset (the embedding's register epilogue);
+    beta = 0 -- integer inputs, bitwise."""
+    rng = np.random.default_rng(12)
+    m, n, k = 256, 512, 192
+    a, b, c = _complex_case(rng, m, n, k, "f16", True)
+    z = lambda x: np.asfortranarray((x[0] + 1j * x[1]).astype(np.complex64))
+    A, B = z(a), z(b)
+    for alpha, beta, kern in [(2.0, 0.5, "pair_cembed"), (1.0, 0.0, "pair_cembed"),
+                              (1.0 + 1.0j, 1.0, None)]:
+        cdev = _pack_pair(c.real, c.imag, None, False)
+        cfg = tk.build_complex_config(m, n, k, tk.COMPLEX32)
+        if (alpha, beta) != (1.0, 1.0):
+            cfg = dataclasses.replace(cfg, transform_g2s_c=tk.components.scale(np.complex64(beta / alpha)),
+                                      transform_r2s_d=tk.components.scale(np.complex64(alpha)))
+        d = torch.zeros_like(cdev)
+        tk.matmul(cfg, _pack_half_pair(*a, "f16"), _pack_half_pair(*b, "f16"), cdev, d)
+        plan = tk.last_run()["plan"]
+        if kern:
+            assert plan["kernel"] == kern, plan
+        else:
+            assert plan["kernel"] != "pair_cembed", plan
+        got = _unpack_pair(d, (m, n), False)
+        want = alpha * (A.astype(np.complex128) @ B.astype(np.complex128)) + beta * c
+        assert np.array_equal(got[0], want.real.astype(np.float32)), (alpha, beta)
+        assert np.array_equal(got[1], want.imag.astype(np.float32)), (alpha, beta)
+    # C and D 8 bytes into their allocations: not TMA-aligned -> the embedding's register epilogue
+    cfg = tk.build_complex_config(m, n, k, tk.COMPLEX32)
+    cbig = torch.zeros(2 * m * n + 2, dtype=torch.float32, device=cuda)
+    cbig[2:] = _pack_pair(c.real, c.imag, None, False)
+    dbig = torch.zeros_like(cbig)
+    tk.matmul(cfg, _pack_half_pair(*a, "f16"), _pack_half_pair(*b, "f16"), cbig[2:], dbig[2:])
+    plan = tk.last_run()["plan"]
+    assert plan["kernel"] == "pair_cembed" and plan["c_stream"] == 0, plan
+    got = _unpack_pair(dbig[2:], (m, n), False)
+    want = A.astype(np.complex128) @ B.astype(np.complex128) + c
+    assert np.array_equal(got[0], want.real.astype(np.float32))
+    assert np.array_equal(got[1], want.imag.astype(np.float32))
+
+
 @pytest.mark.parametrize("kernel", ["auto", "single", "tensor"])
 @pytest.mark.parametrize("n", [256, 1024, 640])
 def test_diagonal_variant(cuda, n, kernel, knob):

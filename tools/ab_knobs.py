@@ -27,7 +27,7 @@ from paper_2009_12263_b200 import _lib  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("case", choices=["dense", "dense_c0", "fused"])
+    ap.add_argument("case", choices=["dense", "dense_c0", "fused", "complex_il", "complex_split"])
     ap.add_argument("n", type=int)
     ap.add_argument("settings", nargs="+")
     ap.add_argument("--reps", type=int, default=20)
@@ -43,7 +43,16 @@ def main():
     b = torch.randn(n * n, generator=g, device=dev).half()
     c = torch.randn(n * n, generator=g, device=dev)
     d = torch.empty(n * n, device=dev)
-    if args.case == "fused":
+    flops = 2.0 * n ** 3
+    if args.case.startswith("complex"):
+        split = args.case == "complex_split"
+        a = torch.randn(2 * n * n, generator=g, device=dev).half()
+        b = torch.randn(2 * n * n, generator=g, device=dev).half()
+        c = torch.randn(2 * n * n, generator=g, device=dev)
+        d = torch.empty(2 * n * n, device=dev)
+        cfg = tk.build_complex_config(n, n, n, tk.COMPLEX32, split=split)
+        flops = 8.0 * n ** 3
+    elif args.case == "fused":
         cfg = tk.build_fused_config(n, n, n, np.float16, bias=torch.randn(n, generator=g, device=dev),
                                     relu_on_c=True, relu_on_d=True, add_a=0.5, add_b=-0.25)
     else:
@@ -79,7 +88,7 @@ def main():
             s1.record()
             torch.cuda.synchronize()
             ms = s0.elapsed_time(s1) / (args.reps * per)
-            tf = 2.0 * n ** 3 / (ms * 1e-3) / 1e12
+            tf = flops / (ms * 1e-3) / 1e12
             us = ms * 1e3
             res[setting].append((tf, mhz()))
             print(f"round {r} {setting:40s} {us:8.2f} us {tf:8.1f} TF  {mhz():7.1f} MHz  plan={tk.last_run()['plan']['kernel']}"
