@@ -64,7 +64,7 @@ enum Knob {
   K_SPLITK_S, K_SK_TMA, K_PDL, K_MN3D, K_PAIR_CSTREAM, K_PAIR_DTMA, K_C_PF, K_C_PF_SPREAD,
   K_NSUB2_CSL, K_STAGGER, K_PAIR_GRID, K_PAIR_DEEPC, K_PAIROPS_BN, K_DIAG_STREAM, K_D_TMA,
   K_L2_PROMO, K_POLICY_AB, K_POL_A, K_POL_B, K_PAIR_CLUSTERS, K_EX_SLABS, K_VERBOSE,
-  K_NSUB2_OVERLAP, K_PAIR_KPS, K_CPLX_EMBED,
+  K_NSUB2_OVERLAP, K_PAIR_KPS, K_CPLX_EMBED, K_POL_C, K_POL_D, K_SIMT_TILED,
   K_DBG_C_ZERO, K_DBG_SKIP_EPI, K_DBG_NO_LOAD, K_DBG_NO_MMA, K_DBG_CTA, K_COUNT
 };
 constexpr int K_FIRST_DIAG = K_DBG_C_ZERO;
@@ -74,7 +74,7 @@ const char* const kKnobNames[K_COUNT] = {
   "TK_PAIR_DTMA", "TK_C_PF", "TK_C_PF_SPREAD", "TK_NSUB2_CSL", "TK_STAGGER", "TK_PAIR_GRID",
   "TK_PAIR_DEEPC", "TK_PAIROPS_BN", "TK_DIAG_STREAM", "TK_D_TMA", "TK_L2_PROMO", "TK_POLICY_AB",
   "TK_POL_A", "TK_POL_B", "TK_PAIR_CLUSTERS", "TK_EX_SLABS", "TK_VERBOSE", "TK_NSUB2_OVERLAP",
-  "TK_PAIR_KPS", "TK_CPLX_EMBED", "TK_DBG_C_ZERO", "TK_DBG_SKIP_EPI", "TK_DBG_NO_LOAD", "TK_DBG_NO_MMA", "TK_DBG_CTA"};
+  "TK_PAIR_KPS", "TK_CPLX_EMBED", "TK_POL_C", "TK_POL_D", "TK_SIMT_TILED", "TK_DBG_C_ZERO", "TK_DBG_SKIP_EPI", "TK_DBG_NO_LOAD", "TK_DBG_NO_MMA", "TK_DBG_CTA"};
 #ifdef TK_DIAG
 constexpr int K_ENABLED = K_COUNT;
 #else
@@ -1205,6 +1205,8 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
   prm.pol_a = prm.pol_b = prm.pol_ab ? 1 : 0;
   prm.pol_a = knob(K_POL_A, prm.pol_a);
   prm.pol_b = knob(K_POL_B, prm.pol_b);
+  prm.pol_c = knob(K_POL_C, 0);  // streamed C loads / D stores: no L2 hint unless tuned
+  prm.pol_d = knob(K_POL_D, 0);
   const bool pair = op == TK_OP_COMPLEX || op == TK_OP_DUAL;  // pair-valued epilogue
   // real operator: C/D rows may follow any digit map (GETT outputs whose M indices are not
   // one contiguous run) as long as columns are one strided digit -- the register epilogue
@@ -1523,6 +1525,20 @@ tk::SimtLayout to_simt(const TkLayout& L, const void* ptr) {
 
 template <int OP, typename T, typename Acc>
 int launch_simt(const tk::SimtParams& sp, cudaStream_t s) {
+  if (OP == tk::OP_REAL && sp.predicate == 0 && knob(K_SIMT_TILED, 1)) {  // 128 x 128 smem tiles
+    const dim3 grid(unsigned((sp.m + tk::ST_BM - 1) / tk::ST_BM), unsigned((sp.n + tk::ST_BN - 1) / tk::ST_BN));
+    if (grid.y <= 65535) {
+      tk::simt_tiled_kernel<T, Acc><<<grid, tk::ST_THREADS, 0, s>>>(sp);
+      TK_CUDA(cudaGetLastError());
+      ++g_launches;
+      info_kernel("simt");
+      g_info.tile_m = tk::ST_BM;
+      g_info.tile_n = tk::ST_BN;
+      g_info.tile_k = tk::ST_BK;
+      g_info.grid_ctas = int(grid.x * grid.y);
+      return TK_OK;
+    }
+  }
   const int64_t total = sp.m * sp.n;
   const int threads = 128;
   tk::simt_gemm_kernel<OP, T, Acc><<<int((total + threads - 1) / threads), threads, 0, s>>>(sp);

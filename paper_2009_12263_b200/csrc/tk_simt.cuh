@@ -192,4 +192,70 @@ __global__ void simt_gemm_kernel(const __grid_constant__ SimtParams p) {
   }
 }
 
+// Tiled form of the real operator (predicate "always"): the same per-element arithmetic as
+// simt_gemm_kernel -- acc starts at round(g2s_c(C)), then acc = acc + a*b for k ascending with
+// separate mul / add roundings (no FMA contraction), then the r2s / bias / s2g stages -- so it
+// is bitwise identical to it and to the reference (_core.pyx:16-68), but each A / B element
+// (transformed by its g2s program once) is staged in shared memory and reused by a 128 x 128
+// output tile, 8 x 8 outputs per thread.  Operand loads go through the layouts' digit maps, so
+// every layout the generic kernel takes is valid here too.
+constexpr int ST_BM = 128, ST_BN = 128, ST_BK = 16, ST_TM = 8, ST_TN = 8, ST_THREADS = 256;
+template <typename T, typename Acc>
+__global__ void __launch_bounds__(ST_THREADS) simt_tiled_kernel(const __grid_constant__ SimtParams p) {
+  __shared__ T As[ST_BK][ST_BM];
+  __shared__ T Bs[ST_BK][ST_BN];
+  const int tid = threadIdx.x;
+  const int64_t m0 = int64_t(blockIdx.x) * ST_BM, n0 = int64_t(blockIdx.y) * ST_BN;
+  const int tr = (tid & 15) * ST_TM, tc = (tid >> 4) * ST_TN;
+  Acc acc[ST_TM][ST_TN];
+#pragma unroll
+  for (int ii = 0; ii < ST_TM; ++ii)
+#pragma unroll
+    for (int jj = 0; jj < ST_TN; ++jj) {
+      const int64_t i = m0 + tr + ii, j = n0 + tc + jj;
+      acc[ii][jj] = Acc(0);
+      if (i < p.m && j < p.n) acc[ii][jj] = Acc(round_to(p.c.scalar, prog(p.t_c, load_real<T>(p.c, i, j))));
+    }
+  for (int64_t k0 = 0; k0 < p.k; k0 += ST_BK) {
+    const int kc = int(min(int64_t(ST_BK), p.k - k0));
+#pragma unroll
+    for (int q = 0; q < ST_BK * ST_BM / ST_THREADS; ++q) {  // A: consecutive threads, consecutive rows
+      const int e = tid + q * ST_THREADS, kk = e / ST_BM, mm = e % ST_BM;
+      const int64_t i = m0 + mm, k = k0 + kk;
+      As[kk][mm] = (i < p.m && kk < kc) ? prog(p.t_a, load_real<T>(p.a, i, k)) : T(0);
+    }
+#pragma unroll
+    for (int q = 0; q < ST_BK * ST_BN / ST_THREADS; ++q) {  // B: consecutive threads, consecutive k
+      const int e = tid + q * ST_THREADS, kk = e % ST_BK, nn = e / ST_BK;
+      const int64_t j = n0 + nn, k = k0 + kk;
+      Bs[kk][nn] = (j < p.n && kk < kc) ? prog(p.t_b, load_real<T>(p.b, k, j)) : T(0);
+    }
+    __syncthreads();
+    for (int kk = 0; kk < kc; ++kk) {  // (only the real k: no padded terms enter any sum)
+      T a[ST_TM], b[ST_TN];
+#pragma unroll
+      for (int ii = 0; ii < ST_TM; ++ii) a[ii] = As[kk][tr + ii];
+#pragma unroll
+      for (int jj = 0; jj < ST_TN; ++jj) b[jj] = Bs[kk][tc + jj];
+#pragma unroll
+      for (int ii = 0; ii < ST_TM; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < ST_TN; ++jj) acc[ii][jj] = add_rn(acc[ii][jj], mul_rn(Acc(a[ii]), Acc(b[jj])));
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int ii = 0; ii < ST_TM; ++ii)
+#pragma unroll
+    for (int jj = 0; jj < ST_TN; ++jj) {
+      const int64_t i = m0 + tr + ii, j = n0 + tc + jj;
+      if (i >= p.m || j >= p.n) continue;
+      T v = T(round_to(p.d.scalar, prog(p.t_r2s, acc[ii][jj])));
+      if (p.bias_axis)
+        v = T(round_to(p.d.scalar, add_rn(v, load_as<T>(p.bias, p.bias_scalar, p.bias_axis == 1 ? j : i))));
+      v = prog(p.t_s2g, v);
+      store_as<T>(const_cast<void*>(p.d.ptr), p.d.scalar, map_dim(p.d.map, 0, i) + map_dim(p.d.map, 1, j), v);
+    }
+}
+
 }  // namespace tk

@@ -126,7 +126,8 @@ struct TcParams {
   // 64-deep k-block, one per K=16 MMA step (expand_kbits_kernel); null = every step runs
   const uint32_t* kbits;
   int32_t kwords;
-  int32_t a_embed;  // complex embedding: ta[0] maps A^ for the staging ring (tc_gemm_pair_kernel EMB)
+  int32_t a_embed;
+  int32_t pol_c, pol_d;  // L2 policies of the streamed C loads / D stores (0 none, 1 evict_last, 2 evict_first)  // complex embedding: ta[0] maps A^ for the staging ring (tc_gemm_pair_kernel EMB)
 };
 
 // the 4 MMA-step bits of k-block kb of pair tile `tile` (0xF without a predicate)
@@ -511,7 +512,10 @@ __device__ __forceinline__ void epilogue_stream(const TcParams& p, uint64_t* tfu
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        tma_store_2d(&p.tdmap, box, row0, j0);   // the map clips rows >= M / columns >= N
+        if (p.pol_d)  // L2 hint for the D stream (tuning: TK_POL_D)
+          tma_store_2d_hint(&p.tdmap, box, row0, j0, policy_code(p.pol_d));
+        else
+          tma_store_2d(&p.tdmap, box, row0, j0);  // the map clips rows >= M / columns >= N
         for (int q = 0; q < p.npeer; ++q) tma_store_2d(&p.tdpeer[q], box, row0, j0);  // peers (NVLink)
         bulk_commit();
         if (ch == 0) TK_TS_EPI(10);

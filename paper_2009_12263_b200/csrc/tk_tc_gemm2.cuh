@@ -284,7 +284,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EMB ? EMB_THREADS : 
             tma_load_2d(smem + PL::CRING + bi * TC_CBOX_BYTES, &p.tcmap, &cfull[bi],
                         mb * 256 + int(rank) * 128 + (w & 3) * 32,
                         nb * BNP + un.noff + (ch / CH) * BNI + (w >> 2) * PL::WCOLS + (ch % CH) * 32,
-                        policy_evict_normal());
+                        policy_code(p.pol_c));
           }
         }
       }

@@ -113,6 +113,39 @@ def dense(n, m=None, k=None, dtype="fp16", trans="nn", name=None):
     return sec
 
 
+def simt_f32(n):
+    """The reference's default dtype (build_dense_config(..., np.float32), api.py:166) on the exact
+    CUDA-core lane (reference operation order, bitwise): device buffers, no graph."""
+    cfg = tk.build_dense_config(n, n, n, np.float32)
+    a, b, c, d = rnd(n * n, torch.float32), rnd(n * n, torch.float32), rnd(n * n, torch.float32), \
+        torch.empty(n * n, device=dev)
+    cfg = kernel.resolve_config(cfg)
+    sec = timeit(lambda: tk.gemm_execute(cfg, a, b, c, d, synchronize=False), reps=3, warm=1)
+    report(f"simt f32 {n}^3 (exact lane)", sec, 2.0 * n ** 3, "TFLOPS", tk.last_run()["lane"])
+
+
+def host_numpy(n):
+    """The drop-in call a reference user makes: tk.matmul on numpy host buffers (fp16 A/B,
+    fp32 C/D) -- staging copies to the device and D back to the host inside the call."""
+    import time
+
+    rng = np.random.default_rng(0)
+    a = rng.standard_normal(n * n).astype(np.float16)
+    b = rng.standard_normal(n * n).astype(np.float16)
+    c = rng.standard_normal(n * n).astype(np.float32)
+    d = np.empty(n * n, np.float32)
+    cfg = tk.build_dense_config(n, n, n, tk.FLOAT16)
+    for _ in range(2):
+        tk.matmul(cfg, a, b, c, d)
+    t0 = time.perf_counter()
+    reps = 5
+    for _ in range(reps):
+        tk.matmul(cfg, a, b, c, d)
+    sec = (time.perf_counter() - t0) / reps
+    report(f"host numpy matmul {n}^3 (wall clock, copies included)", sec, 2.0 * n ** 3, "TFLOPS",
+           tk.last_run()["lane"])
+
+
 def cublas_ref(n, dtype=torch.float16):
     """cuBLAS on the same operation (fp16/bf16 A,B; fp32 C,D; D = A*B + C) via torch.addmm with
     out_dtype=float32 -- the library baseline for the sweep (graph-replayed when GRAPH=1)."""
@@ -233,6 +266,12 @@ if __name__ == "__main__":
     if "sweep" in which:
         for n in (1024, 2048, 4096, 16384):
             dense(n)
+    if "simt" in which:
+        for n in (1024, 2048):
+            simt_f32(n)
+    if "host" in which:
+        for n in (2048, 8192):
+            host_numpy(n)
     if "cublas" in which:
         for n in (1024, 2048, 4096, 8192, 16384):
             cublas_ref(n)
