@@ -1534,7 +1534,7 @@ int launch_simt(const tk::SimtParams& sp, cudaStream_t s) {
       info_kernel("simt");
       g_info.tile_m = tk::ST_BM;
       g_info.tile_n = tk::ST_BN;
-      g_info.tile_k = tk::ST_BK;
+      g_info.tile_k = sizeof(T) == 8 ? tk::ST_BK / 2 : tk::ST_BK;
       g_info.grid_ctas = int(grid.x * grid.y);
       return TK_OK;
     }

@@ -200,13 +200,23 @@ __global__ void simt_gemm_kernel(const __grid_constant__ SimtParams p) {
 // output tile, 8 x 8 outputs per thread.  Operand loads go through the layouts' digit maps, so
 // every layout the generic kernel takes is valid here too.
 constexpr int ST_BM = 128, ST_BN = 128, ST_BK = 16, ST_TM = 8, ST_TN = 8, ST_THREADS = 256;
+// element (i, k) of a real operand: plain strided layouts skip the digit decomposition
+template <typename T>
+__device__ __forceinline__ T load_op(const SimtLayout& L, bool plain, int64_t i, int64_t k) {
+  if (plain) return load_as<T>(L.ptr, L.scalar, i * L.map.s[0][0] + k * L.map.s[1][0]);
+  return load_real<T>(L, i, k);
+}
 template <typename T, typename Acc>
-__global__ void __launch_bounds__(ST_THREADS) simt_tiled_kernel(const __grid_constant__ SimtParams p) {
-  __shared__ T As[ST_BK][ST_BM];
-  __shared__ T Bs[ST_BK][ST_BN];
+__global__ void __launch_bounds__(ST_THREADS, 1) simt_tiled_kernel(const __grid_constant__ SimtParams p) {
+  constexpr int BK = sizeof(T) == 8 ? ST_BK / 2 : ST_BK;  // f64 tiles: half depth (48 KB static smem)
+  constexpr int ST_LA = BK * ST_BM / ST_THREADS, ST_LB = BK * ST_BN / ST_THREADS;  // loads per thread
+  __shared__ T As[2][BK][ST_BM];
+  __shared__ T Bs[2][BK][ST_BN];
   const int tid = threadIdx.x;
   const int64_t m0 = int64_t(blockIdx.x) * ST_BM, n0 = int64_t(blockIdx.y) * ST_BN;
   const int tr = (tid & 15) * ST_TM, tc = (tid >> 4) * ST_TN;
+  const bool a_plain = p.a.kind == L_STRIDED && p.a.map.nd[0] == 1 && p.a.map.nd[1] == 1;
+  const bool b_plain = p.b.kind == L_STRIDED && p.b.map.nd[0] == 1 && p.b.map.nd[1] == 1;
   Acc acc[ST_TM][ST_TN];
 #pragma unroll
   for (int ii = 0; ii < ST_TM; ++ii)
@@ -216,33 +226,57 @@ __global__ void __launch_bounds__(ST_THREADS) simt_tiled_kernel(const __grid_con
       acc[ii][jj] = Acc(0);
       if (i < p.m && j < p.n) acc[ii][jj] = Acc(round_to(p.c.scalar, prog(p.t_c, load_real<T>(p.c, i, j))));
     }
-  for (int64_t k0 = 0; k0 < p.k; k0 += ST_BK) {
-    const int kc = int(min(int64_t(ST_BK), p.k - k0));
+  // operand tiles, transformed once per element (g2s programs), zero outside the matrix;
+  // A: consecutive threads take consecutive rows, B: consecutive k
+  T ra[ST_LA], rb[ST_LB];
+  auto fetch = [&](int64_t k0) {
 #pragma unroll
-    for (int q = 0; q < ST_BK * ST_BM / ST_THREADS; ++q) {  // A: consecutive threads, consecutive rows
+    for (int q = 0; q < ST_LA; ++q) {
       const int e = tid + q * ST_THREADS, kk = e / ST_BM, mm = e % ST_BM;
       const int64_t i = m0 + mm, k = k0 + kk;
-      As[kk][mm] = (i < p.m && kk < kc) ? prog(p.t_a, load_real<T>(p.a, i, k)) : T(0);
+      ra[q] = (i < p.m && k < p.k) ? prog(p.t_a, load_op<T>(p.a, a_plain, i, k)) : T(0);
     }
 #pragma unroll
-    for (int q = 0; q < ST_BK * ST_BN / ST_THREADS; ++q) {  // B: consecutive threads, consecutive k
-      const int e = tid + q * ST_THREADS, kk = e % ST_BK, nn = e / ST_BK;
+    for (int q = 0; q < ST_LB; ++q) {
+      const int e = tid + q * ST_THREADS, kk = e % BK, nn = e / BK;
       const int64_t j = n0 + nn, k = k0 + kk;
-      Bs[kk][nn] = (j < p.n && kk < kc) ? prog(p.t_b, load_real<T>(p.b, k, j)) : T(0);
+      rb[q] = (j < p.n && k < p.k) ? prog(p.t_b, load_op<T>(p.b, b_plain, k, j)) : T(0);
     }
-    __syncthreads();
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < ST_LA; ++q) {
+      const int e = tid + q * ST_THREADS;
+      As[buf][e / ST_BM][e % ST_BM] = ra[q];
+    }
+#pragma unroll
+    for (int q = 0; q < ST_LB; ++q) {
+      const int e = tid + q * ST_THREADS;
+      Bs[buf][e % BK][e / BK] = rb[q];
+    }
+  };
+  fetch(0);
+  stash(0);
+  __syncthreads();
+  int buf = 0;
+  for (int64_t k0 = 0; k0 < p.k; k0 += BK) {
+    const int kc = int(min(int64_t(BK), p.k - k0));
+    const bool more = k0 + BK < p.k;
+    if (more) fetch(k0 + BK);  // next tile's loads in flight under this tile's math
     for (int kk = 0; kk < kc; ++kk) {  // (only the real k: no padded terms enter any sum)
       T a[ST_TM], b[ST_TN];
 #pragma unroll
-      for (int ii = 0; ii < ST_TM; ++ii) a[ii] = As[kk][tr + ii];
+      for (int ii = 0; ii < ST_TM; ++ii) a[ii] = As[buf][kk][tr + ii];
 #pragma unroll
-      for (int jj = 0; jj < ST_TN; ++jj) b[jj] = Bs[kk][tc + jj];
+      for (int jj = 0; jj < ST_TN; ++jj) b[jj] = Bs[buf][kk][tc + jj];
 #pragma unroll
       for (int ii = 0; ii < ST_TM; ++ii)
 #pragma unroll
         for (int jj = 0; jj < ST_TN; ++jj) acc[ii][jj] = add_rn(acc[ii][jj], mul_rn(Acc(a[ii]), Acc(b[jj])));
     }
+    if (more) stash(buf ^ 1);
     __syncthreads();
+    buf ^= 1;
   }
 #pragma unroll
   for (int ii = 0; ii < ST_TM; ++ii)

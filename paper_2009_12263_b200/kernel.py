@@ -27,9 +27,11 @@ bit).  There is no host lane.
 from __future__ import annotations
 
 import contextlib
+import copy
 import contextvars
 import ctypes
 import dataclasses
+import threading
 from dataclasses import dataclass, field
 from typing import Callable, Optional
 
@@ -424,8 +426,16 @@ _LAST = {"lane": None, "launches": 0}
 
 
 def last_run() -> dict:
-    """Lane and device-kernel count of the most recent gemm_execute in this process."""
-    return dict(_LAST)
+    """Lane, device-kernel count and on-chip plan (tk_last_plan_info) of the most recent
+    gemm_execute in this process.  The plan is read from the library when asked for, not on
+    every call (the library keeps it per thread, so it is available to the calling thread)."""
+    pending = _LAST.get("plan_thread")
+    if pending is not None:
+        _LAST["plan"] = _lib.plan_info() if pending == threading.get_ident() else None
+        _LAST["plan_thread"] = None
+    out = dict(_LAST)
+    out.pop("plan_thread", None)
+    return out
 
 
 class _Prepared:
@@ -564,8 +574,11 @@ def gemm_execute(config: KernelConfig, a, b, c, d, *, stream=None, synchronize: 
             raise RuntimeError(f"libtk_sm100: {_lib.last_error()}")
         _LAST["lane"] = _lib.LANE_NAMES[prep.lane_id]
         _LAST["launches"] = lib.tk_last_launch_count()
-        _LAST["plan"] = _lib.plan_info()
-        _note_onchip(_LAST["plan"])
+        if _audit.get() is not None:  # the allocation audit logs the launched plan now
+            _LAST["plan"], _LAST["plan_thread"] = _lib.plan_info(), None
+            _note_onchip(_LAST["plan"])
+        else:
+            _LAST["plan_thread"] = threading.get_ident()
         if D.host is not None:
             s.synchronize()
             D.copy_back()
@@ -575,7 +588,7 @@ def gemm_execute(config: KernelConfig, a, b, c, d, *, stream=None, synchronize: 
             # asynchronous: keep workspace / staging alive until the stream consumes them
             for t in (A.dev, B.dev, C.dev) + ((ws,) if ws is not None else ()):
                 t.record_stream(s)
-    return dataclasses.replace(prep.counters)
+    return copy.copy(prep.counters)
 
 
 def _note_onchip(info):
