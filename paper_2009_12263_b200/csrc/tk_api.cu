@@ -64,7 +64,7 @@ enum Knob {
   K_SPLITK_S, K_SK_TMA, K_PDL, K_MN3D, K_PAIR_CSTREAM, K_PAIR_DTMA, K_C_PF, K_C_PF_SPREAD,
   K_NSUB2_CSL, K_STAGGER, K_PAIR_GRID, K_PAIR_DEEPC, K_PAIROPS_BN, K_DIAG_STREAM, K_D_TMA,
   K_L2_PROMO, K_POLICY_AB, K_POL_A, K_POL_B, K_PAIR_CLUSTERS, K_EX_SLABS, K_VERBOSE,
-  K_NSUB2_OVERLAP, K_PAIR_KPS, K_CPLX_EMBED, K_POL_C, K_POL_D, K_SIMT_TILED,
+  K_NSUB2_OVERLAP, K_PAIR_KPS, K_CPLX_EMBED, K_POL_C, K_POL_D, K_SIMT_TILED, K_GATHER,
   K_DBG_C_ZERO, K_DBG_SKIP_EPI, K_DBG_NO_LOAD, K_DBG_NO_MMA, K_DBG_CTA, K_COUNT
 };
 constexpr int K_FIRST_DIAG = K_DBG_C_ZERO;
@@ -74,7 +74,7 @@ const char* const kKnobNames[K_COUNT] = {
   "TK_PAIR_DTMA", "TK_C_PF", "TK_C_PF_SPREAD", "TK_NSUB2_CSL", "TK_STAGGER", "TK_PAIR_GRID",
   "TK_PAIR_DEEPC", "TK_PAIROPS_BN", "TK_DIAG_STREAM", "TK_D_TMA", "TK_L2_PROMO", "TK_POLICY_AB",
   "TK_POL_A", "TK_POL_B", "TK_PAIR_CLUSTERS", "TK_EX_SLABS", "TK_VERBOSE", "TK_NSUB2_OVERLAP",
-  "TK_PAIR_KPS", "TK_CPLX_EMBED", "TK_POL_C", "TK_POL_D", "TK_SIMT_TILED", "TK_DBG_C_ZERO", "TK_DBG_SKIP_EPI", "TK_DBG_NO_LOAD", "TK_DBG_NO_MMA", "TK_DBG_CTA"};
+  "TK_PAIR_KPS", "TK_CPLX_EMBED", "TK_POL_C", "TK_POL_D", "TK_SIMT_TILED", "TK_GATHER", "TK_DBG_C_ZERO", "TK_DBG_SKIP_EPI", "TK_DBG_NO_LOAD", "TK_DBG_NO_MMA", "TK_DBG_CTA"};
 #ifdef TK_DIAG
 constexpr int K_ENABLED = K_COUNT;
 #else
@@ -320,6 +320,96 @@ void embed_plan(const TkGemmPlan* p, TkGemmPlan* out) {
   real_col(out->d, 2 * p->m, p->n, 2 * p->d.stride[1][0]);
 }
 
+// ---- digit-mapped operands read in place (GETT / tensor contractions on the CTA-pair kernel):
+// a half operand with <= 2 digits per GEMM dimension whose fastest digit is contiguous becomes a
+// 5-D TMA map -- MN-major {64, K0, MN0/64, MN1, K1} or K-major {64, MN0, MN1, K0/64, K1} -- whose
+// box lands in shared memory exactly as the dense operand's tile would, so no pack pass runs.
+// Needs the contiguous digit's run to hold whole CTA blocks: MN0 % 128 == 0 (a 128-row A half,
+// 64 / 128 B columns) and, with two K digits, K0 % 64 == 0.
+CUtensorMapL2promotion l2_promo();
+PFN_cuTensorMapEncodeTiled_v12000 get_encode();
+struct Gather {
+  int g = 0;                          // 1 MN-major, 2 K-major
+  int64_t e0 = 1, s0 = 0, e1 = 1, s1 = 0;  // MN digits (extent, stride in elements)
+  int64_t f0 = 1, t0 = 0, f1 = 1, t1 = 0;  // K digits
+};
+bool gather_layout(const TkLayout& L, int role, Gather& gl) {
+  if (L.kind != TK_LAYOUT_STRIDED || L.pair || !is_half(L.scalar) || !knob(K_GATHER, 1)) return false;
+  const int dm = role == 0 ? 0 : 1, dk = 1 - dm;
+  if (L.ndigits[dm] > 2 || L.ndigits[dk] > 2) return false;
+  Gather g;
+  g.e0 = L.ext[dm][0]; g.s0 = L.stride[dm][0];
+  if (L.ndigits[dm] == 2) { g.e1 = L.ext[dm][1]; g.s1 = L.stride[dm][1]; }
+  g.f0 = L.ext[dk][0]; g.t0 = L.stride[dk][0];
+  if (L.ndigits[dk] == 2) { g.f1 = L.ext[dk][1]; g.t1 = L.stride[dk][1]; }
+  auto ok16 = [](int64_t st) { return st > 0 && (st * 2) % 16 == 0 && st * 2 < (int64_t(1) << 40); };
+  if (g.s0 == 1) {
+    g.g = 1;
+    if (g.e0 % 128 || !ok16(g.t0) || (g.e1 > 1 && !ok16(g.s1)) || (g.f1 > 1 && (!ok16(g.t1) || g.f0 % 64))) return false;
+  } else if (g.t0 == 1) {
+    // (the contiguous K digit is cut into 64-element chunks: they must tile it exactly, since a
+    // chunk past its end would read the next MN row instead of zero-filling)
+    g.g = 2;
+    if (!ok16(g.s0) || g.f0 % 64 || (g.e1 > 1 && (!ok16(g.s1) || g.e0 % 128)) || (g.f1 > 1 && !ok16(g.t1)))
+      return false;
+  } else {
+    return false;
+  }
+  if (g.e0 >= (int64_t(1) << 31) || g.f0 >= (int64_t(1) << 31)) return false;
+  gl = g;
+  return true;
+}
+// the 5-D map of a gathered operand; box_mn = the CTA's rows (A: 128) or columns (B: BNI/2)
+int make_map_gather(CUtensorMap* map, const void* base, int scalar, const Gather& g, uint32_t box_mn) {
+  auto enc = get_encode();
+  if (!enc) return fail(TK_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[5];
+  cuuint64_t strides[4];
+  cuuint32_t box[5];
+  const cuuint64_t unit = 16;  // stride of an extent-1 dimension (never stepped)
+  if (g.g == 1) {
+    dims[0] = 64; dims[1] = g.f0; dims[2] = g.e0 / 64; dims[3] = g.e1; dims[4] = g.f1;
+    strides[0] = g.t0 * 2; strides[1] = 128; strides[2] = g.e1 > 1 ? g.s1 * 2 : unit;
+    strides[3] = g.f1 > 1 ? g.t1 * 2 : unit;
+    box[0] = 64; box[1] = 64; box[2] = box_mn / 64; box[3] = 1; box[4] = 1;
+  } else {
+    dims[0] = 64; dims[1] = g.e0; dims[2] = g.e1; dims[3] = g.f0 / 64; dims[4] = g.f1;
+    strides[0] = g.s0 * 2; strides[1] = g.e1 > 1 ? g.s1 * 2 : unit; strides[2] = 128;
+    strides[3] = g.f1 > 1 ? g.t1 * 2 : unit;
+    box[0] = 64; box[1] = box_mn; box[2] = 1; box[3] = 1; box[4] = 1;
+  }
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = enc(map, scalar == TK_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5,
+                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, l2_promo(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(TK_ERR_CUDA, "cuTensorMapEncodeTiled (5-D gather) failed (%d)", int(r));
+  return TK_OK;
+}
+
+// The plan runs on the CTA-pair kernel with plain operands (so a digit-mapped operand may be
+// gathered by the TMA instead of packed): the dispatch in run_tc takes the pair path for it.
+bool gather_path(const TkGemmPlan* p) {
+  const int ov = knob(K_TC_KERNEL, 0);
+  return p->op == TK_OP_REAL && !p->t_a.n && !p->t_b.n && p->a.kind == TK_LAYOUT_STRIDED &&
+         p->predicate == TK_PRED_ALWAYS && p->m > 128 && (p->k + 63) / 64 > 4 && (ov == 0 || ov == 2);
+}
+// tensor contraction: A with its two M digits swapped (m' = m1 + e1*m0, see permuted_plan)
+TkLayout swapped_a(const TkLayout& A0) {
+  TkLayout A = A0;
+  std::swap(A.ext[0][0], A.ext[0][1]);
+  std::swap(A.stride[0][0], A.stride[0][1]);
+  return A;
+}
+// B's shared-memory major-ness on the pair kernel: MN-major when N is contiguous (dense or
+// gathered); a packed B is K-major
+bool b_mn_major(const TkLayout& b) {
+  int mn;
+  int64_t pitch;
+  if (tma_operand(b, mn, pitch)) return !mn;
+  Gather g;
+  return gather_layout(b, 1, g) && g.g == 1;
+}
+
 // A half-precision strided operand the TMA cannot read directly (multi-digit permutations,
 // non-unit innermost strides, non-bijective interleaved pairs) is gathered once into a dense
 // column-major workspace by pack_half_kernel and then takes the normal tensor-core path.
@@ -463,18 +553,24 @@ Workspace plan_workspace(const TkGemmPlan* p0, int lane) {
   if (lane != TK_LANE_TCGEN05) return w;
   TkGemmPlan rewritten;
   const TkGemmPlan* p = p0;
+  Gather gl;
   if (permuted_plan(p0, &rewritten)) {
-    w.a_perm = w.total;
-    w.total += align256(p0->m * p0->k * 2);
+    if (gather_path(&rewritten) && gather_layout(swapped_a(p0->a), 0, gl)) {
+      rewritten.a = swapped_a(p0->a);  // read in place by a 5-D TMA map
+    } else {
+      w.a_perm = w.total;
+      w.total += align256(p0->m * p0->k * 2);
+    }
     p = &rewritten;
   }
   TkGemmPlan packed = *p;
-  if (pack_needed(p->a)) {
+  const bool gp = gather_path(p);
+  if (pack_needed(p->a) && !(gp && gather_layout(p->a, 0, gl))) {
     w.a_pack = w.total;
     w.total += align256(p->m * p->k * 2 * (p->a.pair ? 2 : 1));
     dense_operand(packed.a, p->m, p->k);
   }
-  if (pack_needed(p->b)) {
+  if (pack_needed(p->b) && !(gp && gather_layout(p->b, 1, gl))) {
     w.b_pack = w.total;
     w.total += align256(p->k * p->n * 2 * (p->b.pair ? 2 : 1));
     dense_operand(packed.b, p->k, p->n);
@@ -797,9 +893,7 @@ SplitPlan split_plan(int64_t tiles, int clusters, int kb_total, int bnp) {
 }
 
 int64_t split_ws_bytes(int64_t m, int64_t n, int64_t k, const TkLayout& b) {
-  int mn;
-  int64_t pitch;
-  const bool b_mn = tma_operand(b, mn, pitch) ? !mn : false;
+  const bool b_mn = b_mn_major(b);
   const int bni = choose_pair_bni(m, n, b_mn, pair_clusters());
   const int64_t tiles = ((m + 255) / 256) * ((n + bni - 1) / bni);
   return split_plan(tiles, pair_clusters(), int((k + 63) / 64), bni).ws_bytes;
@@ -1008,15 +1102,18 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
     embed_plan(p0, &embedded);
     p = p0 = &embedded;
   }
-  if (w.a_perm >= 0 && permuted_plan(p0, &rewritten)) {
-    // A's two M digits swapped (m' = m1 + e1*m0) and gathered into a dense M' x K workspace
-    TkLayout A = p0->a;
-    std::swap(A.ext[0][0], A.ext[0][1]);
-    std::swap(A.stride[0][0], A.stride[0][1]);
-    uint16_t* at = reinterpret_cast<uint16_t*>(ws + w.a_perm);
-    int rc0 = launch_pack(A, a, at, p0->m, p0->k, s);
-    if (rc0) return rc0;
-    a = at;
+  if (permuted_plan(p0, &rewritten)) {
+    // A's two M digits swapped (m' = m1 + e1*m0): gathered into a dense M' x K workspace, or
+    // (no a_perm workspace) read in place by the pair kernel's 5-D TMA map
+    const TkLayout A = swapped_a(p0->a);
+    if (w.a_perm >= 0) {
+      uint16_t* at = reinterpret_cast<uint16_t*>(ws + w.a_perm);
+      int rc0 = launch_pack(A, a, at, p0->m, p0->k, s);
+      if (rc0) return rc0;
+      a = at;
+    } else {
+      rewritten.a = A;
+    }
     p = &rewritten;
   }
   TkGemmPlan packed;
@@ -1111,6 +1208,13 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
   } else if (p->a.kind == TK_LAYOUT_DIAGONAL) {
     prm.diag_a = 1;
     prm.diag = a;
+  } else if (Gather ga; !pack_needed(p->a) ? false : gather_layout(p->a, 0, ga)) {
+    // digit-mapped A read in place (5-D TMA map built with the pair kernel's box below)
+    prm.a_g = ga.g;
+    prm.a_mn = ga.g == 1;
+    prm.ga_e0 = int(ga.e0);
+    prm.ga_f0 = int(ga.f0);
+    if (int rc = make_map_gather(&prm.ta[0], a, p->a.scalar, ga, 128)) return rc;
   } else {
     int mn;
     int64_t pitch;
@@ -1138,7 +1242,14 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
     }
   }
   // ---- B operand
-  {
+  Gather gb;
+  if (pack_needed(p->b) && gather_layout(p->b, 1, gb)) {
+    // digit-mapped B read in place (the map, whose box depends on the pair tile, is built there)
+    prm.b_g = gb.g;
+    prm.b_mn = gb.g == 1;
+    prm.gb_e0 = int(gb.e0);
+    prm.gb_f0 = int(gb.f0);
+  } else {
     int mn_k;  // 1: dim0 (K) contiguous -> K-major smem; 0: N contiguous -> MN-major
     int64_t pitch;
     tma_operand(p->b, mn_k, pitch);
@@ -1303,7 +1414,8 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
       int64_t pitch;
       int rc;
       tma_operand(p->b, mn, pitch);
-      const int bni = pred_tc ? pred_bni(p) : (nsub == 2 || emb) ? 256 : choose_pair_bni(p->m, p->n, /*b_mn_major=*/!mn, pair_clusters());
+      const int bni = pred_tc ? pred_bni(p) : (nsub == 2 || emb) ? 256
+                      : choose_pair_bni(p->m, p->n, /*b_mn_major=*/prm.b_g ? prm.b_mn != 0 : !mn, pair_clusters());
       pp.num_mb = int((p->m + 255) / 256);
       pp.num_nb = int((p->n + bni * nsub - 1) / (bni * nsub));
       pp.num_tiles = pp.num_mb * pp.num_nb;
@@ -1347,7 +1459,7 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
       // per-CTA halves: A box 128 rows / B box bni/2 columns
       pp.mn3d = 0;
       const bool use3d = knob(K_MN3D, 1) != 0;
-      if (!emb) {  // (embedding: ta[0] is the A^ staging map)
+      if (!emb && !prm.a_g) {  // (embedding: ta[0] is the A^ staging map; gathered A: the 5-D map)
         tma_operand(p->a, mn, pitch);
         // MN-major A (M % 64 == 0 so atoms never straddle the M edge): one 3-D box per stage
         if (mn && use3d && p->m % 64 == 0) {
@@ -1356,9 +1468,13 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
         }
         if (!mn && (rc = make_map_2d(&pp.ta[0], a_plane0, p->a.scalar, p->k, p->m, pitch, 64, 128))) return rc;
       }
-      tma_operand(p->b, mn, pitch);
-      if (mn && (rc = make_map_2d(&pp.tb[0], b_plane0, p->b.scalar, p->k, p->n, pitch, 64, bni / 2))) return rc;
-      if (!mn && use3d && p->n % 64 == 0) {
+      if (prm.b_g) {  // digit-mapped B: 5-D map, this CTA's bni/2 columns per box
+        Gather gbx;
+        gather_layout(p->b, 1, gbx);
+        if ((rc = make_map_gather(&pp.tb[0], b_plane0, p->b.scalar, gbx, uint32_t(bni / 2)))) return rc;
+      } else if (tma_operand(p->b, mn, pitch), mn) {
+        if ((rc = make_map_2d(&pp.tb[0], b_plane0, p->b.scalar, p->k, p->n, pitch, 64, bni / 2))) return rc;
+      } else if (use3d && p->n % 64 == 0) {
         if ((rc = make_map_mn3d(&pp.tb[0], b_plane0, p->b.scalar, p->n, p->k, pitch, bni / 128))) return rc;
         pp.mn3d |= 2;
       }

@@ -127,7 +127,11 @@ struct TcParams {
   const uint32_t* kbits;
   int32_t kwords;
   int32_t a_embed;
-  int32_t pol_c, pol_d;  // L2 policies of the streamed C loads / D stores (0 none, 1 evict_last, 2 evict_first)  // complex embedding: ta[0] maps A^ for the staging ring (tc_gemm_pair_kernel EMB)
+  int32_t pol_c, pol_d;  // L2 policies of the streamed C loads / D stores (0 none, 1 evict_last, 2 evict_first)
+  // digit-mapped (GETT / TC) operands read in place through 5-D TMA maps ta[0] / tb[0] (pair kernel):
+  // 0 none, 1 MN-major {64, K0, MN0/64, MN1, K1}, 2 K-major {64, MN0, MN1, K0/64, K1}; e0 / f0 =
+  // extent of the operand's fastest MN / K digit
+  int32_t a_g, b_g, ga_e0, ga_f0, gb_e0, gb_f0;  // complex embedding: ta[0] maps A^ for the staging ring (tc_gemm_pair_kernel EMB)
 };
 
 // the 4 MMA-step bits of k-block kb of pair tile `tile` (0xF without a predicate)

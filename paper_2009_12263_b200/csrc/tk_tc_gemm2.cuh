@@ -132,6 +132,17 @@ __device__ __forceinline__ void nsub2_step(int i, int K, int Xs, int Xe, int& kb
   else { kb = i - Xs - Xe; mask = 2; }
 }
 
+// 5-D coordinates of the box at (mn0, k0) of a digit-mapped operand (TcParams::a_g / b_g):
+// MN-major {64, K0, MN0/64, MN1, K1}, K-major {64, MN0, MN1, K0/64, K1}
+__device__ __forceinline__ void gather_load(void* dst, const CUtensorMap* m, uint32_t bar, int g, int e0, int f0,
+                                            int mn0, int k0, uint64_t pol) {
+  const int kq = k0 / f0, kr = k0 - kq * f0, mq = mn0 / e0, mr = mn0 - mq * e0;
+  if (g == 1)
+    tma_load_5d_pair(dst, m, bar, 0, kr, mr >> 6, mq, kq, pol);
+  else
+    tma_load_5d_pair(dst, m, bar, 0, mr, mq, kr >> 6, kq, pol);
+}
+
 // Complex embedding (EMB): an interleaved complex GEMM (reference ComplexOperator over
 // InterleavedComplex A/B/C/D, operators.py:140-163, layouts.py:315-394) run as the real GEMM
 //   D^ (2M x N) = A~ (2M x 2K) * B^ (2K x N) + C^,
@@ -325,7 +336,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EMB ? EMB_THREADS : 
               const int k0 = (kb + h) * TC_BK;
               uint8_t* at = a_tile(stage) + h * PL::KB_BYTES;
               uint8_t* bt = at + TC2_TILE_BYTES;
-              if (a_mode == 0) {
+              if (p.a_g) {
+                gather_load(at, &p.ta[0], fb, p.a_g, p.ga_e0, p.ga_f0, m0, k0, pol);
+              } else if (a_mode == 0) {
                 tma_load_3d_pair(at, &p.ta[0], fb, 0, k0, m0 >> 6, pol);
               } else if (a_mode == 1) {
                 tma_load_2d_pair(at, &p.ta[0], fb, m0, k0, pol);
@@ -333,7 +346,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EMB ? EMB_THREADS : 
               } else {
                 tma_load_2d_pair(at, &p.ta[0], fb, k0, m0, pol);
               }
-              if (b_mode == 0) {
+              if (p.b_g) {
+                gather_load(bt, &p.tb[0], fb, p.b_g, p.gb_e0, p.gb_f0, n0, k0, pol_b);
+              } else if (b_mode == 0) {
                 tma_load_3d_pair(bt, &p.tb[0], fb, 0, k0, n0 >> 6, pol_b);
               } else if (b_mode == 1) {
                 for (int hh = 0; hh < BNI / 128; ++hh)
@@ -391,6 +406,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EMB ? EMB_THREADS : 
           if (leader) mbar_arrive_expect_tx(&full[stage], tx);
           const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
           if (EMB) {
+          } else if (p.a_g) {
+            gather_load(a_tile(stage), &p.ta[0], fb, p.a_g, p.ga_e0, p.ga_f0, m0, k0, pol);
           } else if (a_mode == 0) {
             tma_load_3d_pair(a_tile(stage), &p.ta[0], fb, 0, k0, m0 >> 6, pol);
           } else if (a_mode == 1) {
@@ -404,7 +421,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EMB ? EMB_THREADS : 
             if (!(mask >> sub & 1)) continue;
             uint8_t* bt = b_tile(stage) + sub * PL::B_BYTES;
             const int nn = n0 + sub * BNI;
-            if (b_mode == 0) {
+            if (p.b_g) {
+              gather_load(bt, &p.tb[0], fb, p.b_g, p.gb_e0, p.gb_f0, nn, k0, pol_b);
+            } else if (b_mode == 0) {
               tma_load_3d_pair(bt, &p.tb[0], fb, 0, k0, nn >> 6, pol_b);
             } else if (b_mode == 1) {  // 64-column atoms (BNI >= 128)
               for (int h = 0; h < BNI / 128; ++h)

@@ -547,7 +547,10 @@ def gemm_execute(config: KernelConfig, a, b, c, d, *, stream=None, synchronize: 
     device = d.device if isinstance(d, torch.Tensor) and d.is_cuda else \
         torch.device("cuda", torch.cuda.current_device())
     lib = _lib.load()
-    with torch.cuda.device(device):
+    # (the device guard is only entered when D lives on another device than the current one)
+    guard = torch.cuda.device(device) if device.index != torch.cuda.current_device() else \
+        contextlib.nullcontext()
+    with guard:
         A = _Buf(a, prep.np_dtypes[0], "A", device)
         B = _Buf(b, prep.np_dtypes[1], "B", device)
         C = _Buf(c, prep.np_dtypes[2], "C", device)

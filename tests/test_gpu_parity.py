@@ -622,6 +622,43 @@ def test_tensor_contraction_tcgen05(cuda, shape):
     assert counters.global_stores == na * nb * nc
 
 
+@pytest.mark.parametrize("spec,sizes,packs", [
+    # A MN-major with two M and two K digits read in place; B's contiguous digit is a second N
+    # digit, so B is packed
+    ("abcd-aebf-dfce", dict(a=128, b=4, c=128, d=64, e=64, f=5), 1),
+    # A K-major (K contiguous) with two M and two K digits, interleaved in memory; B plain
+    ("abc-daeb-dec", dict(a=128, b=4, c=256, d=64, e=5), 0),
+    # B MN-major with two N digits around the K digit (256-wide and 128-wide pair tiles)
+    ("abc-ad-bdc", dict(a=512, b=128, c=4, d=320), 0),
+    ("abc-ad-bdc", dict(a=256, b=128, c=2, d=320), 0),
+])
+def test_gett_tma_gather(cuda, spec, sizes, packs, knob):
+    """Digit-mapped operands read in place through 5-D TMA maps (no pack pass): bitwise equal
+    on integer inputs to the oracle and to the packed path (TK_GATHER=0), with the expected
+    number of pack launches."""
+    rng = np.random.default_rng(19)
+    d_idx, a_idx, b_idx = spec.split("-")
+    a = _half(rng, [sizes[i] for i in a_idx], np.float16, True)
+    b = _half(rng, [sizes[i] for i in b_idx], np.float16, True)
+    fa = torch.from_numpy(np.asfortranarray(a).ravel(order="F")).cuda()
+    fb = torch.from_numpy(np.asfortranarray(b).ravel(order="F")).cuda()
+    cfg = tk.build_gett_config(spec, sizes, np.float16)
+    d_size = int(np.prod([sizes[i] for i in d_idx]))
+    want = O.gett_reference(spec, _f32(a), _f32(b))
+    outs = {}
+    for gather in ("1", "0"):
+        knob("TK_GATHER", gather)
+        d = torch.zeros(d_size, dtype=torch.float32, device=cuda)
+        tk.matmul(cfg, fa, fb, torch.empty(0, dtype=torch.float32, device=cuda), d)
+        run = tk.last_run()
+        assert run["lane"] == "tcgen05" and run["plan"]["kernel"] == "pair", run
+        outs[gather] = (d.cpu().numpy().reshape(want.shape, order="F"), run["launches"])
+    assert outs["1"][1] == 1 + packs, outs["1"][1]
+    assert outs["0"][1] > outs["1"][1], (outs["0"][1], outs["1"][1])
+    assert np.array_equal(outs["1"][0], want), float(np.abs(outs["1"][0] - want).max())
+    assert np.array_equal(outs["1"][0], outs["0"][0])
+
+
 @pytest.mark.parametrize("spec,sizes", [
     ("abcd-aebf-dfce", dict(a=32, b=8, c=16, d=24, e=16, f=24)),   # A, B gathered; D dense
     ("abc-acd-db", dict(a=64, b=96, c=8, d=136)),                 # A gathered, B TMA, D dense
