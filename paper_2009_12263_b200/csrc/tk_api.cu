@@ -855,6 +855,7 @@ template <bool DENSE, bool CSTREAM>
 int launch_tc_pair_bni(const tk::TcParams& prm, int bni, cudaStream_t s) {
   // narrow tiles: two K-blocks per ring stage (halves the barrier round trips per operand byte)
   // unless a block predicate needs per-K-block MMA bits
+  // (4 K-blocks per stage measured +1 % at 1024^3 and -20 % at 1536^3, where only one stage fits)
   const bool kps2 = !prm.kbits && knob(K_PAIR_KPS, 2) == 2;
   if (bni == 64) return kps2 ? launch_tc_pair<DENSE, CSTREAM, 1, 64, tk::TC2S_CSLOTS, 2>(prm, s)
                              : launch_tc_pair<DENSE, CSTREAM, 1, 64>(prm, s);

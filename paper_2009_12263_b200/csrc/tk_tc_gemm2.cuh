@@ -160,7 +160,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EMB ? EMB_THREADS : 
   using PL = Tc2Plan<NSUB, CSTREAM, BNI, CSL, KPS, EMB>;
   static_assert(!EMB || (KPS == 1 && BNI == 256 && DENSE_EPI), "complex embedding: 256-wide tiles, dense epilogue");
   static_assert(NSUB == 1 || BNI == 256, "NSUB 2 uses 256-wide MMAs");
-  static_assert(KPS == 1 || NSUB == 1, "two K-blocks per stage: single-MMA tiles only (no predicate bits)");
+  static_assert(KPS == 1 || NSUB == 1, "several K-blocks per stage: single-MMA tiles only (no predicate bits)");
   constexpr int STAGES = PL::STAGES;
   constexpr int BNP = PL::BNP;
   constexpr int NCBAR = CSTREAM ? TC_EPI_WARPS * CSL : 0;
@@ -238,9 +238,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EMB ? EMB_THREADS : 
   // KPS 2: steps of two K-blocks over [kb0, kb1) (the last one single if the count is odd),
   // in reverse step order for serpentine tiles; ascending inside a step
   auto kps_step = [&](const PairUnit& un, bool rev, int st, int& kb, int& cnt) {
-    const int nst = (un.kb1 - un.kb0 + 1) >> 1;
-    kb = un.kb0 + 2 * (rev ? nst - 1 - st : st);
-    cnt = un.kb1 - kb < 2 ? 1 : 2;
+    const int nst = (un.kb1 - un.kb0 + KPS - 1) / KPS;
+    kb = un.kb0 + KPS * (rev ? nst - 1 - st : st);
+    cnt = un.kb1 - kb < KPS ? un.kb1 - kb : KPS;
   };  // 32-column chunks per epilogue warp per pass
 
   if (CSTREAM && warp == 3) {
@@ -324,8 +324,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EMB ? EMB_THREADS : 
         // serpentine K: every other tile of a cluster walks K downwards, so the next
         // wave starts on the K-slices the previous one loaded last (still in L2)
         const bool rev = p.serp && (lu & 1);
-        if (KPS == 2) {
-          const int nst = (un.kb1 - un.kb0 + 1) >> 1;
+        if (KPS > 1) {
+          const int nst = (un.kb1 - un.kb0 + KPS - 1) / KPS;
           for (int st = 0; st < nst; ++st) {
             int kb, cnt;
             kps_step(un, rev, st, kb, cnt);
@@ -473,9 +473,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EMB ? EMB_THREADS : 
           mbar_wait(&tempty[as], aphase ^ 1);
           tc_fence_after();
           const uint32_t d0 = tmem_base + uint32_t(as * BNI);
-          if (KPS == 2) {
+          if (KPS > 1) {
             const bool rev = p.serp && (local & 1);
-            const int nst = (un.kb1 - un.kb0 + 1) >> 1;
+            const int nst = (un.kb1 - un.kb0 + KPS - 1) / KPS;
             for (int st = 0; st < nst; ++st) {
               int kb, cnt;
               kps_step(un, rev, st, kb, cnt);
