@@ -351,7 +351,10 @@ def run_ours(args):
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 # sm_mhz_in_kernel (clock64 / globaltimer inside the GEMM) is the clock the
                 # kernel ran at; NVML's sm_mhz over a short timed region can miss the load
-                "clocks": {"sm_mhz_in_kernel": kernel_mhz, **sampler.summary()},
+                "clocks": {"sm_mhz_in_kernel": kernel_mhz, **sampler.summary(),
+                           "note": "sm_mhz_in_kernel = clock64 / %globaltimer inside the GEMM (the effective "
+                                   "clock); NVML's sm_mhz / power_w over a short region report the requested "
+                                   "clock and a lagging power average ('sustained' holds a seconds-long run)"},
                 "sustained": sustained,
                 "library_baseline": library,
                 "allgather_d": allgather,
