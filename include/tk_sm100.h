@@ -164,7 +164,7 @@ const char* tk_last_error(void);
  * here the per-CTA shared-memory stages, C ring and TMEM accumulator columns are the analogue).
  * Sizes in bytes unless noted. */
 typedef struct TkPlanInfo {
-  char kernel[32];          /* "pair", "pair_ops", "single", "stream", "quad", "diag_stream", "simt" */
+  char kernel[32];          /* "pair", "pair_cembed", "pair_ops", "ksplit", "single", "stream", "quad", "diag_stream", "simt" */
   int32_t lane;             /* TkLane of the launch, -1 before any */
   int32_t op;               /* TkOperator */
   int32_t tile_m, tile_n;   /* output tile per cluster (or CTA) */

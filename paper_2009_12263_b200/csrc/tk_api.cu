@@ -24,6 +24,7 @@
 #include "tk_tc_gemm2.cuh"
 #include "tk_tc_gemm4.cuh"
 #include "tk_tc_gemm2c.cuh"
+#include "tk_tc_gemm_ks.cuh"
 
 static_assert(tk::MAX_DIGITS == TK_MAX_DIGITS, "device digit maps match the C ABI");
 
@@ -64,7 +65,8 @@ enum Knob {
   K_SPLITK_S, K_SK_TMA, K_PDL, K_MN3D, K_PAIR_CSTREAM, K_PAIR_DTMA, K_C_PF, K_C_PF_SPREAD,
   K_NSUB2_CSL, K_STAGGER, K_PAIR_GRID, K_PAIR_DEEPC, K_PAIROPS_BN, K_DIAG_STREAM, K_D_TMA,
   K_L2_PROMO, K_POLICY_AB, K_POL_A, K_POL_B, K_PAIR_CLUSTERS, K_EX_SLABS, K_VERBOSE,
-  K_NSUB2_OVERLAP, K_PAIR_KPS, K_CPLX_EMBED, K_POL_C, K_POL_D, K_SIMT_TILED, K_GATHER,
+  K_NSUB2_OVERLAP, K_PAIR_KPS, K_CPLX_EMBED, K_POL_C, K_POL_D, K_SIMT_TILED, K_GATHER, K_KSPLIT,
+  K_KSPLIT_KPS,
   K_DBG_C_ZERO, K_DBG_SKIP_EPI, K_DBG_NO_LOAD, K_DBG_NO_MMA, K_DBG_CTA, K_COUNT
 };
 constexpr int K_FIRST_DIAG = K_DBG_C_ZERO;
@@ -74,7 +76,8 @@ const char* const kKnobNames[K_COUNT] = {
   "TK_PAIR_DTMA", "TK_C_PF", "TK_C_PF_SPREAD", "TK_NSUB2_CSL", "TK_STAGGER", "TK_PAIR_GRID",
   "TK_PAIR_DEEPC", "TK_PAIROPS_BN", "TK_DIAG_STREAM", "TK_D_TMA", "TK_L2_PROMO", "TK_POLICY_AB",
   "TK_POL_A", "TK_POL_B", "TK_PAIR_CLUSTERS", "TK_EX_SLABS", "TK_VERBOSE", "TK_NSUB2_OVERLAP",
-  "TK_PAIR_KPS", "TK_CPLX_EMBED", "TK_POL_C", "TK_POL_D", "TK_SIMT_TILED", "TK_GATHER", "TK_DBG_C_ZERO", "TK_DBG_SKIP_EPI", "TK_DBG_NO_LOAD", "TK_DBG_NO_MMA", "TK_DBG_CTA"};
+  "TK_PAIR_KPS", "TK_CPLX_EMBED", "TK_POL_C", "TK_POL_D", "TK_SIMT_TILED", "TK_GATHER", "TK_KSPLIT",
+  "TK_KSPLIT_KPS", "TK_DBG_C_ZERO", "TK_DBG_SKIP_EPI", "TK_DBG_NO_LOAD", "TK_DBG_NO_MMA", "TK_DBG_CTA"};
 #ifdef TK_DIAG
 constexpr int K_ENABLED = K_COUNT;
 #else
@@ -546,6 +549,7 @@ struct SplitPlan;
 SplitPlan split_plan(int64_t tiles, int clusters, int kb_total, int bnp);
 int choose_pair_bni(int64_t m, int64_t n, bool b_mn_major, int clusters);
 int pair_clusters();
+int tc_kernel_override();
 int64_t split_ws_bytes(int64_t m, int64_t n, int64_t k, const TkLayout& b);
 
 Workspace plan_workspace(const TkGemmPlan* p0, int lane) {
@@ -865,6 +869,105 @@ int launch_tc_pair_bni(const tk::TcParams& prm, int bni, cudaStream_t s) {
   if (CSTREAM && prm.num_units <= pair_clusters() && knob(K_PAIR_DEEPC, 1))
     return launch_tc_pair<DENSE, CSTREAM, 1, 256, 4>(prm, s);
   return launch_tc_pair<DENSE, CSTREAM, 1, 256>(prm, s);
+}
+
+// On-chip split-K (tk_tc_gemm_ks.cuh): 4-CTA clusters, two CTA pairs per 256 x 128 tile, one
+// K half each, reduced through distributed shared memory.  Single wave only: every tile is one
+// cluster, so the tile count may not exceed the co-resident 4-CTA clusters.
+template <int KPS>
+int ksplit_max_clusters() {
+  using PL = tk::KsPlan<128, KPS>;
+  static int cache[TK_MAX_DEV] = {};
+  const int dev = cur_dev();
+  int& mc = cache[dev];
+  if (!mc) {
+    auto kern = tk::tc_gemm_ksplit_kernel<128, KPS>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PL::SMEM) != cudaSuccess) {
+      cudaGetLastError();
+      return mc = -1;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(4 * (sm_count() / 4));
+    cfg.blockDim = dim3(tk::TC_THREADS);
+    cfg.dynamicSmemBytes = PL::SMEM;
+    cudaLaunchAttribute at;
+    at.id = cudaLaunchAttributeClusterDimension;
+    at.val.clusterDim.x = 4;
+    at.val.clusterDim.y = 1;
+    at.val.clusterDim.z = 1;
+    cfg.attrs = &at;
+    cfg.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&mc, kern, &cfg) != cudaSuccess || mc <= 0) {
+      cudaGetLastError();
+      mc = -1;
+    }
+    if (knob(K_VERBOSE, 0)) fprintf(stderr, "tk: k-split kernel max active clusters %d\n", mc);
+  }
+  return mc;
+}
+// one K-block per stage: measured faster than two here (1024^3 8.0 vs 8.4 us, 1024^2 x 8192
+// 21.3 vs 24.4 us) -- unlike the whole-K narrow tiles, whose stage count is not the limit
+int ksplit_kps() { return knob(K_KSPLIT_KPS, 1) == 2 ? 2 : 1; }
+int ksplit_clusters() { return ksplit_kps() == 1 ? ksplit_max_clusters<1>() : ksplit_max_clusters<2>(); }
+
+template <int KPS>
+int launch_tc_ksplit(const tk::TcParams& prm, cudaStream_t s) {
+  using PL = tk::KsPlan<128, KPS>;
+  tk::TcParams run = prm;
+  run.pdl = knob(K_PDL, 1) ? 1 : 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(4 * run.num_tiles);
+  cfg.blockDim = dim3(tk::TC_THREADS);
+  cfg.dynamicSmemBytes = PL::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = run.pdl ? 1 : 0;
+  TK_CUDA(cudaLaunchKernelEx(&cfg, tk::tc_gemm_ksplit_kernel<128, KPS>, run));
+  ++g_launches;
+  info_kernel("ksplit");
+  g_info.tile_m = 256;
+  g_info.tile_k = 64 * KPS;
+  g_info.tile_n = 128;
+  g_info.mma_n = 128;
+  g_info.nsub = 1;
+  g_info.mmas_per_k16 = 1;
+  g_info.cluster = 4;
+  g_info.stages = PL::STAGES;
+  g_info.stage_bytes = PL::STAGE_BYTES;
+  g_info.cring_bytes = PL::CRING_BYTES;
+  g_info.smem_bytes = PL::SMEM;
+  g_info.tmem_cols = PL::TMEM_COLS;
+  g_info.grid_ctas = 4 * run.num_tiles;
+  g_info.tiles = g_info.units = run.num_tiles;
+  g_info.sk_parts = 2;
+  g_info.sk_tiles = run.num_tiles;
+  g_info.group_m = run.group_m;
+  g_info.pdl = run.pdl;
+  g_info.c_stream = 1;
+  g_info.d_tma = 1;
+  return TK_OK;
+}
+
+// Use the on-chip split-K kernel?  TK_KSPLIT: 0 never, 1 auto (default), 2 whenever legal.
+// Auto compares the per-k-block ingest model of choose_pair_bni: whole-K pair tiles (waves x
+// KB x t(bni)) against half-K 256 x 128 tiles (KB/2 x t(128) + the reduce-scatter, ~1500 clocks).
+bool ksplit_choice(int64_t m, int64_t n, int kb_total, int pair_bni, int clusters) {
+  const int mode = knob(K_KSPLIT, 1);
+  if (mode == 0 || kb_total < 4) return false;
+  // (auto leaves pinned pair-kernel configurations -- TK_TC_KERNEL / TK_PAIR_BNI -- alone)
+  if (mode == 1 && (tc_kernel_override() != 0 || knob_set(K_PAIR_BNI))) return false;
+  const int64_t tiles = ((m + 255) / 256) * ((n + 127) / 128);
+  const int mc = ksplit_clusters();
+  if (mc <= 0 || tiles > mc) return false;
+  if (mode == 2) return true;
+  auto per_kb = [](int bni) { return std::max(2.0 * bni, (16384.0 + 64.0 * bni) / 60.0); };
+  const int64_t ptiles = ((m + 255) / 256) * ((n + pair_bni - 1) / pair_bni);
+  const double t_pair = double((ptiles + clusters - 1) / clusters) * kb_total * per_kb(pair_bni);
+  const double t_ks = 0.5 * kb_total * per_kb(128) + 500.0;
+  return t_ks < t_pair;
 }
 
 // Split-K of a poorly filled last wave: with T tiles over P clusters, W = T / P full waves and
@@ -1415,8 +1518,12 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
       int64_t pitch;
       int rc;
       tma_operand(p->b, mn, pitch);
-      const int bni = pred_tc ? pred_bni(p) : (nsub == 2 || emb) ? 256
+      int bni = pred_tc ? pred_bni(p) : (nsub == 2 || emb) ? 256
                       : choose_pair_bni(p->m, p->n, /*b_mn_major=*/prm.b_g ? prm.b_mn != 0 : !mn, pair_clusters());
+      // on-chip split-K of single-wave shapes (256 x 128 tiles, K halves on two CTA pairs)
+      const bool ks = nsub == 1 && !pred_tc && !emb && !prm.a_g && !prm.b_g && dense && !rmapped &&
+                      ksplit_choice(p->m, p->n, pp.kb_total, bni, pair_clusters());
+      if (ks) bni = 128;
       pp.num_mb = int((p->m + 255) / 256);
       pp.num_nb = int((p->n + bni * nsub - 1) / (bni * nsub));
       pp.num_tiles = pp.num_mb * pp.num_nb;
@@ -1446,7 +1553,7 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
         // at each tile boundary hide the half-accumulator drains under MMAs
         pp.ovl_kb = (pp.nar_units || emb) ? 0 : std::max(0, std::min(knob(K_NSUB2_OVERLAP, 16), pp.kb_total / 4));
       }
-      if (nsub == 1 && dense && w.splitk >= 0 && !knob_set(K_PAIR_GRID)) {
+      if (nsub == 1 && dense && w.splitk >= 0 && !knob_set(K_PAIR_GRID) && !ks) {
         const SplitPlan sp = split_plan(pp.num_tiles, pair_clusters(), pp.kb_total, bni);
         if (sp.parts > 1 && sp.ws_bytes <= split_ws_bytes(p->m, p->n, p->k, p->b)) {
           pp.sk_first = sp.first;
@@ -1518,6 +1625,7 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
           if (csl == 4) return launch_tc_pair<true, true, 2, 256, 4>(pp, s);
           return launch_tc_pair<true, true, 2>(pp, s);
         }
+        if (ks && !pp.npeer) return ksplit_kps() == 1 ? launch_tc_ksplit<1>(pp, s) : launch_tc_ksplit<2>(pp, s);
         return launch_tc_pair_bni<true, true>(pp, bni, s);
       }
       if (emb)  // (C / D not TMA-aligned: register epilogue)
@@ -1794,6 +1902,8 @@ int tk_debug_pair_ts(double* out) {
   unsigned long long v[16];
   if (cudaMemcpyFromSymbol(v, tk::g_dbg_ts, sizeof(v)) != cudaSuccess) return 2;
   for (int i = 0; i < 16; ++i) out[i] = v[i] >= v[0] ? double(v[i] - v[0]) * 1e-3 : -1.0;
+  // (k-split kernel: slot 15 = the previous launch's exit, signed, relative to this entry)
+  if (v[15]) out[15] = double(int64_t(v[15] - v[0])) * 1e-3;
   return 0;
 }
 

@@ -41,13 +41,17 @@ def _f32(x):
     return np.asarray(x).astype(np.float32)
 
 
-@pytest.fixture(params=["single", "pair", "pair128", "pair64", "pair64k1", "pair512", "quad", "stream"])
+@pytest.fixture(params=["single", "pair", "pair128", "pair64", "pair64k1", "pair512", "quad", "stream",
+                        "ksplit"])
 def tc_kernel(request, knob):
     """Pin the single-CTA (128x256), CTA-pair (256 x 256/128/64 tiles -- the narrow ones with two
     K-blocks per ring stage, `k1` one -- or 256 x 512 with two MMAs per K step), 4-CTA multicast
-    or C-streaming tcgen05 kernel."""
+    or C-streaming tcgen05 kernel; `ksplit` forces the on-chip split-K kernel wherever it is legal
+    (single-wave shapes on the pair path)."""
     name = request.param
-    if name.startswith("pair") and name != "pair":
+    if name == "ksplit":
+        knob("TK_KSPLIT", "2")
+    elif name.startswith("pair") and name != "pair":
         knob("TK_TC_KERNEL", "pair")
         if name == "pair512":
             knob("TK_PAIR_NSUB", "2")
@@ -128,6 +132,62 @@ def test_narrow_tiles_ring_stages(cuda, bni, kps, grid, knob):
         got = _host(d, (m, n))
         want = O.gemm_real(_f32(a), _f32(b), c)
         assert np.array_equal(got, want), (m, n, k, float(np.abs(got - want).max()))
+
+
+@pytest.mark.parametrize("kps", ["1", "2"])
+@pytest.mark.parametrize("case", [
+    (1024, 1024, 1024, False, False, "f16"),      # the C2 low end: 32 tiles of 256 x 128
+    (1000, 520, 4104, False, False, "bf16"),      # M / N tails, odd k-block count (65)
+    (512, 768, 7 * 64 + 24, True, False, "f16"),  # K-major A, K tail inside the last block
+    (768, 384, 640, False, True, "f16"),          # MN-major B
+    (256, 128, 320, True, True, "bf16"),          # one cluster, 5 k-blocks (2 + 3)
+])
+def test_ksplit_on_chip(cuda, case, kps, knob):
+    """On-chip split-K (4-CTA clusters: two CTA pairs per 256 x 128 tile, one K half each,
+    partials reduce-scattered through distributed shared memory): integer inputs bitwise equal
+    to the oracle with bias + ReLU, random inputs within the sqrt(K) bound with the C3
+    alpha/beta scaling, and the plan really is the k-split kernel."""
+    m, n, k, ta, tb, dt = case
+    dtype = tk.BFLOAT16 if dt == "bf16" else np.dtype(np.float16)
+    knob("TK_KSPLIT", "2")
+    knob("TK_KSPLIT_KPS", kps)
+    rng = np.random.default_rng(23)
+    for integer in (True, False):
+        a, b = _half(rng, (m, k), dtype, integer), _half(rng, (k, n), dtype, integer)
+        c = (rng.integers(-4, 5, (m, n)) if integer else rng.standard_normal((m, n))).astype(np.float32)
+        bias = (rng.integers(-4, 5, n) if integer else rng.standard_normal(n)).astype(np.float32)
+        cfg = dataclasses.replace(tk.build_dense_config(m, n, k, dtype, trans_a=ta, trans_b=tb),
+                                  epilogue=tk.components.BiasEpilogue(torch.from_numpy(bias).cuda()),
+                                  transform_s2g_d=tk.components.relu)
+        al, be = 1.5, 0.5
+        if not integer:
+            cfg = dataclasses.replace(cfg, transform_g2s_c=tk.components.scale(be / al),
+                                      transform_r2s_d=tk.components.scale(al))
+        d = torch.full((m * n,), float("nan"), dtype=torch.float32, device=cuda)
+        tk.matmul(cfg, _dev(a.T) if ta else _dev(a), _dev(b.T) if tb else _dev(b), _dev(c), d)
+        plan = tk.last_run()["plan"]
+        assert plan["kernel"] == "ksplit" and plan["cluster"] == 4, plan
+        assert plan["tile_k"] == 64 * int(kps), plan
+        got = _host(d, (m, n))
+        if integer:
+            want = np.maximum(O.gemm_real(_f32(a), _f32(b), c) + bias[None, :], 0)
+            assert np.array_equal(got, want), (case, float(np.abs(got - want).max()))
+        else:
+            prod = _f32(a).astype(np.float64) @ _f32(b).astype(np.float64)
+            want = np.maximum(al * (prod + (be / al) * c) + bias[None, :], 0)
+            assert O.rel_err(got, want) <= O.tolerance(k), O.rel_err(got, want)
+
+
+def test_ksplit_auto_choice(cuda):
+    """The default dispatch takes the on-chip split-K kernel for 1024^3 (single wave of 256 x 128
+    tiles) and keeps whole-K pair tiles where there are enough of them (2048^3)."""
+    for n, want in ((1024, "ksplit"), (2048, "pair")):
+        a = torch.ones(n * n, dtype=torch.float16, device=cuda)
+        c = torch.zeros(n * n, device=cuda)
+        d = torch.empty(n * n, device=cuda)
+        tk.matmul(tk.build_dense_config(n, n, n, np.float16), a, a, c, d)
+        assert tk.last_run()["plan"]["kernel"] == want, (n, tk.last_run()["plan"])
+        assert torch.all(d == n)
 
 
 _SPLITK_WANT = {}
@@ -651,7 +711,9 @@ def test_gett_tma_gather(cuda, spec, sizes, packs, knob):
         d = torch.zeros(d_size, dtype=torch.float32, device=cuda)
         tk.matmul(cfg, fa, fb, torch.empty(0, dtype=torch.float32, device=cuda), d)
         run = tk.last_run()
-        assert run["lane"] == "tcgen05" and run["plan"]["kernel"] == "pair", run
+        # (packed operands may take the on-chip split-K kernel: a single-wave shape)
+        assert run["lane"] == "tcgen05" and run["plan"]["kernel"] in ("pair", "ksplit"), run
+        assert gather == "0" or run["plan"]["kernel"] == "pair", run
         outs[gather] = (d.cpu().numpy().reshape(want.shape, order="F"), run["launches"])
     assert outs["1"][1] == 1 + packs, outs["1"][1]
     assert outs["0"][1] > outs["1"][1], (outs["0"][1], outs["1"][1])
