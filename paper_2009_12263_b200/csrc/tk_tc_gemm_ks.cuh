@@ -40,20 +40,30 @@ struct KsPlan {
   static constexpr int BOXES = 4 * HALF_COLS / 32;              // 32x32 C/D boxes per CTA
   static constexpr int CRING_BYTES = BOXES * TC_CBOX_BYTES;     // one C box per box, prefetched
   static constexpr int XBUF_BYTES = 128 * HALF_COLS * 4;        // partner's partial (FP32)
-  static constexpr int FIXED = CRING_BYTES + XBUF_BYTES + 512 + 1024;
+  // the partner's partial lands in this CTA's operand ring once that is idle (XBUF, after the
+  // 32 KB where the outgoing half is staged): the ring gets the room (8 stages instead of 6)
+  static constexpr int FIXED = CRING_BYTES + 512 + 1024;
   static constexpr int MAX_STAGES = (227 * 1024 - FIXED) / STAGE_BYTES;
-  static constexpr int STAGES = MAX_STAGES > 8 ? 8 : MAX_STAGES;
+#ifndef TK_KS_MAX_STAGES
+#define TK_KS_MAX_STAGES 8
+#endif
+  static constexpr int STAGES = MAX_STAGES > TK_KS_MAX_STAGES ? TK_KS_MAX_STAGES : MAX_STAGES;
   static constexpr int CRING = STAGES * STAGE_BYTES;
-  static constexpr int XBUF = CRING + CRING_BYTES;
-  static constexpr int BAR_OFFSET = XBUF + XBUF_BYTES;
+  static constexpr int XBUF = XBUF_BYTES;  // inside the ring: [0, XBUF) stages the outgoing half
+  static constexpr int BAR_OFFSET = CRING + CRING_BYTES;
   static constexpr int SMEM = BAR_OFFSET + 512 + 1024;
   static constexpr int TMEM_COLS = BNI < 32 ? 32 : BNI;
   static_assert(BOXES == TC_EPI_WARPS, "one C/D box per epilogue warp");
+  static_assert(2 * XBUF_BYTES <= STAGES * STAGE_BYTES, "staging + partial fit in the ring");
   static_assert(STAGES >= 2 && SMEM <= 227 * 1024, "k-split kernel shared memory");
 };
 
-template <int BNI, int KPS>
-__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(TC_THREADS, 1)
+// NT = output tiles per cluster along N (cluster = 4*NT CTAs).  NT = 2: the two tiles' pairs
+// (ranks 4nn + 2q + h) need the same A rows and K half, so each CTA fetches one 64-row atom of
+// its 128 A rows and multicasts it to itself and its twin r^4 -- half the L2 reads of A; a ring
+// stage is then released only when both twins' MMAs have consumed it.
+template <int BNI, int KPS, int NT>
+__global__ void __cluster_dims__(4 * NT, 1, 1) __launch_bounds__(TC_THREADS, 1)
     tc_gemm_ksplit_kernel(const __grid_constant__ TcParams p) {
   using PL = KsPlan<BNI, KPS>;
   static_assert(BNI == 128, "256 x 128 tiles (N=128 pair MMAs, 64 finalised columns per CTA)");
@@ -66,7 +76,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(TC_THREADS, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* xfull = tfull + 1;
   uint64_t* cfull = xfull + 1;  // [TC_EPI_WARPS]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cfull + TC_EPI_WARPS);
+  uint64_t* xready = cfull + TC_EPI_WARPS;  // the partner's ring is idle: its partial may be sent
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xready + 1);
   float* cring = reinterpret_cast<float*>(smem + PL::CRING);
   const uint32_t xbuf = smem_u32(smem + PL::XBUF);
 
@@ -74,10 +85,12 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(TC_THREADS, 1)
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) TK_TS(0);
   const uint32_t rank = cluster_ctarank();
-  const uint32_t q = rank >> 1, h = rank & 1;
+  const uint32_t nn = rank >> 2, q = (rank >> 1) & 1, h = rank & 1;
   const uint32_t lead = rank & ~1u, partner = rank ^ 2u;
-  const uint16_t pair_mask = uint16_t(0x3u << (2 * q));
-  const int tile = blockIdx.x >> 2;
+  const uint16_t pair_mask = uint16_t(0x3u << (rank & ~1u));
+  // ring-stage release: this pair, and (NT 2) the twin pair whose A atoms land here too
+  const uint16_t empty_mask = NT == 2 ? uint16_t((0x3u << (2 * q)) | (0x3u << (4 + 2 * q))) : pair_mask;
+  const int tile = blockIdx.x / (4 * NT);
   const int kbh = p.kb_total / 2;
   const int kb0 = q ? kbh : 0, kb1 = q ? p.kb_total : kbh;
 
@@ -90,11 +103,12 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(TC_THREADS, 1)
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], NT);
     }
     mbar_init(tfull, 1);
     mbar_init(xfull, 1);
     for (int w = 0; w < TC_EPI_WARPS; ++w) mbar_init(&cfull[w], 1);
+    mbar_init(xready, 1);
     fence_mbar_init();
     // the partner's partial: XBUF_BYTES of bulk-copy complete_tx (may land before this phase's
     // expect_tx is visible to it: the pending arrival keeps the phase open until then)
@@ -119,6 +133,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(TC_THREADS, 1)
 
   int mb, nb;
   tile_coords(p, tile, mb, nb);
+  nb = nb * NT + int(nn);                    // (NT 2: p.num_nb counts 256-column tile pairs)
   const int row0 = mb * 256 + int(h) * 128;  // this CTA's rows
 
   if (warp == 0) {
@@ -141,7 +156,13 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(TC_THREADS, 1)
           const int k0 = (kb + hh) * TC_BK;
           uint8_t* at = smem + stage * PL::STAGE_BYTES + hh * PL::KB_BYTES;
           uint8_t* bt = at + PL::A_BYTES;
-          if (a_mode == 0) {
+          if (NT == 2) {  // A atom nn (64 rows; ta[0] has 64 x 64 boxes) to this CTA and its twin
+            const uint16_t mc = uint16_t((1u << rank) | (1u << (rank ^ 4u)));
+            if (p.a_mn)
+              tma_load_2d_pair_mc(at + nn * 8192, &p.ta[0], &full[stage], mc, row0 + 64 * int(nn), k0, pol);
+            else
+              tma_load_2d_pair_mc(at + nn * 8192, &p.ta[0], &full[stage], mc, k0, row0 + 64 * int(nn), pol);
+          } else if (a_mode == 0) {
             tma_load_3d_pair(at, &p.ta[0], fb, 0, k0, row0 >> 6, pol);
           } else if (a_mode == 1) {
             tma_load_2d_pair(at, &p.ta[0], fb, row0, k0, pol);
@@ -193,7 +214,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(TC_THREADS, 1)
             tc_mma_f16_pair(tmem_base, a_desc0 + ho + kk * a_kk, b_desc0 + ho + kk * b_kk, idesc,
                             (kb > kb0 || hh > 0 || kk > 0) ? 1u : 0u);
         }
-        tc_commit_pair(&empty[stage], pair_mask);
+        tc_commit_pair(&empty[stage], empty_mask);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
       tc_commit_pair(tfull, pair_mask);
@@ -211,12 +232,17 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(TC_THREADS, 1)
     const int sw = row_local & 7;
     mbar_wait_sleep(tfull, 0);
     TK_TS_EPI(4);
-    if (warp == 4 && lane == 0) TK_TSMAX(11);
+    if (warp == 4 && lane == 0) {
+      TK_TSMAX(11);
+      // every MMA of this pair -- hence every read of this CTA's ring -- has completed: the
+      // partner may now write its partial into the ring
+      mbar_arrive_cluster(mapa_shared(smem_u32(xready), partner));
+    }
     tc_fence_after();
     {  // ship the partner's columns of this warp's chunk: stage them (swizzled like the
        // partner's buffer) in this CTA's operand ring -- free once the accumulator is full, all
        // MMAs and hence all operand reads having completed -- and move the warp's 4 KB with one
-       // bulk copy that completes on the partner's barrier
+       // bulk copy into the partner's ring (once it is idle too) that completes on its barrier
       uint32_t r[32];
       tmem_ld_32x32b_x32(tlane + uint32_t((q ^ 1u) * PL::HALF_COLS + chunk * 32), r);
       tmem_ld_wait();
@@ -229,6 +255,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(TC_THREADS, 1)
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
+        mbar_wait(xready, 0);  // the partner's ring is idle
         asm volatile(
             "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], 4096, [%2];" ::"r"(
                 mapa_shared(xbuf + uint32_t(chunk * 16384 + quarter * 4096), partner)),

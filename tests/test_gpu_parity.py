@@ -134,6 +134,7 @@ def test_narrow_tiles_ring_stages(cuda, bni, kps, grid, knob):
         assert np.array_equal(got, want), (m, n, k, float(np.abs(got - want).max()))
 
 
+@pytest.mark.parametrize("nt", ["1", "2"])
 @pytest.mark.parametrize("kps", ["1", "2"])
 @pytest.mark.parametrize("case", [
     (1024, 1024, 1024, False, False, "f16"),      # the C2 low end: 32 tiles of 256 x 128
@@ -142,15 +143,17 @@ def test_narrow_tiles_ring_stages(cuda, bni, kps, grid, knob):
     (768, 384, 640, False, True, "f16"),          # MN-major B
     (256, 128, 320, True, True, "bf16"),          # one cluster, 5 k-blocks (2 + 3)
 ])
-def test_ksplit_on_chip(cuda, case, kps, knob):
-    """On-chip split-K (4-CTA clusters: two CTA pairs per 256 x 128 tile, one K half each,
-    partials reduce-scattered through distributed shared memory): integer inputs bitwise equal
-    to the oracle with bias + ReLU, random inputs within the sqrt(K) bound with the C3
-    alpha/beta scaling, and the plan really is the k-split kernel."""
+def test_ksplit_on_chip(cuda, case, kps, nt, knob):
+    """On-chip split-K (two CTA pairs per 256 x 128 tile, one K half each, partials
+    reduce-scattered through distributed shared memory; 4-CTA clusters, or 8 with two tiles
+    sharing multicast A atoms -- the shapes include a second tile wholly past N): integer inputs
+    bitwise equal to the oracle with bias + ReLU, random inputs within the sqrt(K) bound with the
+    C3 alpha/beta scaling, and the plan really is the k-split kernel."""
     m, n, k, ta, tb, dt = case
     dtype = tk.BFLOAT16 if dt == "bf16" else np.dtype(np.float16)
     knob("TK_KSPLIT", "2")
     knob("TK_KSPLIT_KPS", kps)
+    knob("TK_KSPLIT_NT", nt)
     rng = np.random.default_rng(23)
     for integer in (True, False):
         a, b = _half(rng, (m, k), dtype, integer), _half(rng, (k, n), dtype, integer)
@@ -166,8 +169,11 @@ def test_ksplit_on_chip(cuda, case, kps, knob):
         d = torch.full((m * n,), float("nan"), dtype=torch.float32, device=cuda)
         tk.matmul(cfg, _dev(a.T) if ta else _dev(a), _dev(b.T) if tb else _dev(b), _dev(c), d)
         plan = tk.last_run()["plan"]
-        assert plan["kernel"] == "ksplit" and plan["cluster"] == 4, plan
-        assert plan["tile_k"] == 64 * int(kps), plan
+        if plan["kernel"] == "pair":  # 8-CTA clusters: only ~15 are co-resident on a B200
+            assert nt == "2" and ((m + 255) // 256) * ((n + 255) // 256) >= 15, plan
+        else:
+            assert plan["kernel"] == "ksplit" and plan["cluster"] == 4 * int(nt), plan
+            assert plan["tile_k"] == 64 * int(kps), plan
         got = _host(d, (m, n))
         if integer:
             want = np.maximum(O.gemm_real(_f32(a), _f32(b), c) + bias[None, :], 0)

@@ -60,13 +60,13 @@ def main():
         cfg = kernel.resolve_config(tk.build_dense_config(m, n, k, tk.FLOAT16))
         row = []
         ref = None
-        for label, ks, kps, pdl in (("pair", "0", None, None), ("ks2", "2", "2", None), ("ks1", "2", "1", None),
-                                    ("ks1-nopdl", "2", "1", "0"), ("auto", None, None, None)):
+        for label, ks, kps, pdl in (("pair", "0", None, None), ("ks-nt1", "2", "1", None), ("ks-nt2", "2", "2", None),
+                                    ("auto", None, None, None)):
             _lib.tune_reset()
             if ks is not None:
                 _lib.tune("TK_KSPLIT", ks)
             if kps is not None:
-                _lib.tune("TK_KSPLIT_KPS", kps)
+                _lib.tune("TK_KSPLIT_NT", kps)
             if pdl is not None:
                 _lib.tune("TK_PDL", pdl)
             d = torch.empty(m * n, device=dev)
