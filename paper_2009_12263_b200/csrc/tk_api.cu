@@ -1784,7 +1784,14 @@ int launch_simt(const tk::SimtParams& sp, cudaStream_t s) {
   if (OP == tk::OP_REAL && sp.predicate == 0 && knob(K_SIMT_TILED, 1)) {  // 128 x 128 smem tiles
     const dim3 grid(unsigned((sp.m + tk::ST_BM - 1) / tk::ST_BM), unsigned((sp.n + tk::ST_BN - 1) / tk::ST_BN));
     if (grid.y <= 65535) {
-      tk::simt_tiled_kernel<T, Acc><<<grid, tk::ST_THREADS, 0, s>>>(sp);
+      const int want = sizeof(T) == 4 ? tk::S_F32 : tk::S_F64;
+      auto plain = [&](const tk::SimtLayout& L) {
+        return L.kind == tk::L_STRIDED && L.pair == 0 && L.scalar == want && L.map.nd[0] == 1 && L.map.nd[1] == 1;
+      };
+      if (plain(sp.a) && plain(sp.b) && sp.t_a.n == 0 && sp.t_b.n == 0)
+        tk::simt_tiled_kernel<T, Acc, true><<<grid, tk::ST_THREADS, 0, s>>>(sp);
+      else
+        tk::simt_tiled_kernel<T, Acc><<<grid, tk::ST_THREADS, 0, s>>>(sp);
       TK_CUDA(cudaGetLastError());
       ++g_launches;
       info_kernel("simt");

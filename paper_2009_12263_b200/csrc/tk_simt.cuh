@@ -197,24 +197,44 @@ __global__ void simt_gemm_kernel(const __grid_constant__ SimtParams p) {
 // separate mul / add roundings (no FMA contraction), then the r2s / bias / s2g stages -- so it
 // is bitwise identical to it and to the reference (_core.pyx:16-68), but each A / B element
 // (transformed by its g2s program once) is staged in shared memory and reused by a 128 x 128
-// output tile, 8 x 8 outputs per thread.  Operand loads go through the layouts' digit maps, so
+// output tile, 8 x 8 outputs per thread (two 4 x 4 blocks per dimension, 64 apart).  Operand loads go through the layouts' digit maps, so
 // every layout the generic kernel takes is valid here too.
 constexpr int ST_BM = 128, ST_BN = 128, ST_BK = 16, ST_TM = 8, ST_TN = 8, ST_THREADS = 256;
+// 4 consecutive shared-memory elements (16-byte vector loads)
+template <typename T>
+__device__ __forceinline__ void lds4(const T* src, T (&dst)[4], int at) {
+  if constexpr (sizeof(T) == 4) {
+    const float4 v = *reinterpret_cast<const float4*>(src);
+    dst[at] = v.x; dst[at + 1] = v.y; dst[at + 2] = v.z; dst[at + 3] = v.w;
+  } else {
+    const double2 v0 = *reinterpret_cast<const double2*>(src);
+    const double2 v1 = *reinterpret_cast<const double2*>(src + 2);
+    dst[at] = v0.x; dst[at + 1] = v0.y; dst[at + 2] = v1.x; dst[at + 3] = v1.y;
+  }
+}
 // element (i, k) of a real operand: plain strided layouts skip the digit decomposition
 template <typename T>
 __device__ __forceinline__ T load_op(const SimtLayout& L, bool plain, int64_t i, int64_t k) {
   if (plain) return load_as<T>(L.ptr, L.scalar, i * L.map.s[0][0] + k * L.map.s[1][0]);
   return load_real<T>(L, i, k);
 }
-template <typename T, typename Acc>
-__global__ void __launch_bounds__(ST_THREADS, 1) simt_tiled_kernel(const __grid_constant__ SimtParams p) {
+// Thread (r, c) = (tid % 16, tid / 16) owns rows {4r..4r+3, 64+4r..64+4r+3} and the same
+// pattern of columns: its operand reads are 16-byte vectors at consecutive addresses across the
+// warp (conflict-free), two CTAs share an SM (<= 128 registers).
+// FAST: plain strided A / B stored at T's precision with identity g2s programs (the reference's
+// default f32 / f64 configs) -- direct loads; FP32 accumulation fits two CTAs per SM (<= 128
+// registers), f64 accumulators alone take 128.
+template <typename T, typename Acc, bool FAST = false>
+__global__ void __launch_bounds__(ST_THREADS, (FAST && sizeof(Acc) == 4) ? 2 : 1) simt_tiled_kernel(const __grid_constant__ SimtParams p) {
   constexpr int BK = sizeof(T) == 8 ? ST_BK / 2 : ST_BK;  // f64 tiles: half depth (48 KB static smem)
   constexpr int ST_LA = BK * ST_BM / ST_THREADS, ST_LB = BK * ST_BN / ST_THREADS;  // loads per thread
   __shared__ T As[2][BK][ST_BM];
   __shared__ T Bs[2][BK][ST_BN];
   const int tid = threadIdx.x;
   const int64_t m0 = int64_t(blockIdx.x) * ST_BM, n0 = int64_t(blockIdx.y) * ST_BN;
-  const int tr = (tid & 15) * ST_TM, tc = (tid >> 4) * ST_TN;
+  const int tr = (tid & 15) * 4, tc = (tid >> 4) * 4;
+  auto row_of = [&](int ii) { return tr + (ii & 3) + (ii >> 2) * 64; };
+  auto col_of = [&](int jj) { return tc + (jj & 3) + (jj >> 2) * 64; };
   const bool a_plain = p.a.kind == L_STRIDED && p.a.map.nd[0] == 1 && p.a.map.nd[1] == 1;
   const bool b_plain = p.b.kind == L_STRIDED && p.b.map.nd[0] == 1 && p.b.map.nd[1] == 1;
   Acc acc[ST_TM][ST_TN];
@@ -222,7 +242,7 @@ __global__ void __launch_bounds__(ST_THREADS, 1) simt_tiled_kernel(const __grid_
   for (int ii = 0; ii < ST_TM; ++ii)
 #pragma unroll
     for (int jj = 0; jj < ST_TN; ++jj) {
-      const int64_t i = m0 + tr + ii, j = n0 + tc + jj;
+      const int64_t i = m0 + row_of(ii), j = n0 + col_of(jj);
       acc[ii][jj] = Acc(0);
       if (i < p.m && j < p.n) acc[ii][jj] = Acc(round_to(p.c.scalar, prog(p.t_c, load_real<T>(p.c, i, j))));
     }
@@ -234,13 +254,21 @@ __global__ void __launch_bounds__(ST_THREADS, 1) simt_tiled_kernel(const __grid_
     for (int q = 0; q < ST_LA; ++q) {
       const int e = tid + q * ST_THREADS, kk = e / ST_BM, mm = e % ST_BM;
       const int64_t i = m0 + mm, k = k0 + kk;
-      ra[q] = (i < p.m && k < p.k) ? prog(p.t_a, load_op<T>(p.a, a_plain, i, k)) : T(0);
+      if constexpr (FAST)
+        ra[q] = (i < p.m && k < p.k) ? reinterpret_cast<const T*>(p.a.ptr)[i * p.a.map.s[0][0] + k * p.a.map.s[1][0]]
+                                     : T(0);
+      else
+        ra[q] = (i < p.m && k < p.k) ? prog(p.t_a, load_op<T>(p.a, a_plain, i, k)) : T(0);
     }
 #pragma unroll
     for (int q = 0; q < ST_LB; ++q) {
       const int e = tid + q * ST_THREADS, kk = e % BK, nn = e / BK;
       const int64_t j = n0 + nn, k = k0 + kk;
-      rb[q] = (j < p.n && k < p.k) ? prog(p.t_b, load_op<T>(p.b, b_plain, k, j)) : T(0);
+      if constexpr (FAST)
+        rb[q] = (j < p.n && k < p.k) ? reinterpret_cast<const T*>(p.b.ptr)[k * p.b.map.s[0][0] + j * p.b.map.s[1][0]]
+                                     : T(0);
+      else
+        rb[q] = (j < p.n && k < p.k) ? prog(p.t_b, load_op<T>(p.b, b_plain, k, j)) : T(0);
     }
   };
   auto stash = [&](int buf) {
@@ -265,10 +293,18 @@ __global__ void __launch_bounds__(ST_THREADS, 1) simt_tiled_kernel(const __grid_
     if (more) fetch(k0 + BK);  // next tile's loads in flight under this tile's math
     for (int kk = 0; kk < kc; ++kk) {  // (only the real k: no padded terms enter any sum)
       T a[ST_TM], b[ST_TN];
+      T a0[4], a1[4], b0[4], b1[4];
+      lds4(&As[buf][kk][tr], a0, 0);
+      lds4(&As[buf][kk][tr + 64], a1, 0);
+      lds4(&Bs[buf][kk][tc], b0, 0);
+      lds4(&Bs[buf][kk][tc + 64], b1, 0);
 #pragma unroll
-      for (int ii = 0; ii < ST_TM; ++ii) a[ii] = As[buf][kk][tr + ii];
-#pragma unroll
-      for (int jj = 0; jj < ST_TN; ++jj) b[jj] = Bs[buf][kk][tc + jj];
+      for (int q = 0; q < 4; ++q) {
+        a[q] = a0[q];
+        a[q + 4] = a1[q];
+        b[q] = b0[q];
+        b[q + 4] = b1[q];
+      }
 #pragma unroll
       for (int ii = 0; ii < ST_TM; ++ii)
 #pragma unroll
@@ -282,7 +318,7 @@ __global__ void __launch_bounds__(ST_THREADS, 1) simt_tiled_kernel(const __grid_
   for (int ii = 0; ii < ST_TM; ++ii)
 #pragma unroll
     for (int jj = 0; jj < ST_TN; ++jj) {
-      const int64_t i = m0 + tr + ii, j = n0 + tc + jj;
+      const int64_t i = m0 + row_of(ii), j = n0 + col_of(jj);
       if (i >= p.m || j >= p.n) continue;
       T v = T(round_to(p.d.scalar, prog(p.t_r2s, acc[ii][jj])));
       if (p.bias_axis)

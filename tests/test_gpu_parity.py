@@ -650,6 +650,28 @@ def test_simt_f32_bitwise(cuda):
     assert np.array_equal(d.reshape((m, n), order="F"), want)
 
 
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("case", [(256, 256, 256, False, False), (200, 136, 72, True, False),
+                                  (384, 136, 264, False, True), (136, 640, 48, True, True)])
+def test_simt_dense_fast_path_bitwise(cuda, dtype, case):
+    """The reference's default dtypes (build_dense_config(..., np.float32 / np.float64)) on the
+    exact lane's direct-load tiled kernel: bitwise equal to the oracle (reference order, separate
+    mul / add roundings) with tails in every dimension and transposed operands."""
+    m, n, k, ta, tb = case
+    rng = np.random.default_rng(8)
+    a = rng.standard_normal((m, k)).astype(dtype)
+    b = rng.standard_normal((k, n)).astype(dtype)
+    c = rng.standard_normal((m, n)).astype(dtype)
+    cfg = tk.build_dense_config(m, n, k, dtype, trans_a=ta, trans_b=tb)
+    d = np.zeros(m * n, dtype)
+    ab = (a.T if ta else a).ravel(order="F")
+    bb = (b.T if tb else b).ravel(order="F")
+    tk.matmul(cfg, ab, bb, c.ravel(order="F"), d)
+    assert tk.last_run()["lane"] == "simt"
+    want = O.gemm_real(a, b, c)
+    assert np.array_equal(d.reshape((m, n), order="F"), want)
+
+
 def test_simt_complex_dual_bitwise(cuda):
     m, n, k = 40, 24, 32
     rng = np.random.default_rng(8)

@@ -180,3 +180,19 @@ def test_fused_allgather_two_ranks_one_gpu(shape, mode):
             pytest.skip(f"CUDA IPC unavailable in this sandbox: {ok}")
         assert ok is True, (rank, ok)
         assert got_mode == mode, (rank, got_mode)
+
+
+def test_bench_self_launch_dry_run():
+    """`bench.py --gpus 2` without a torchrun environment re-launches itself with two ranks
+    (gloo dry run: rank plumbing only) and reports n_gpus == 2 seen by both ranks."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run"],
+                         capture_output=True, text=True, timeout=240, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([x for x in out.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["ranks_seen"] == 2 and line["dry_run"], line
