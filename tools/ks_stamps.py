@@ -18,7 +18,7 @@ NAMES = {"ksplit": ["entry", "inputs ok", "1st full", "sent", "acc full", "parti
                     "D read", "max exit", "max D issued", "max acc full", "max inputs ok", "max 1st full",
                     "pre-math"],
          "pair": ["entry", "prologue", "1st full", "last MMA issued", "last acc full", "epilogue done",
-                  "stores drained", "exit"]}
+                  "stores drained", "exit", "epi:tmem", "epi:math", "epi:store", "epi:C ready"]}
 SHAPES = [tuple(int(x) for x in s.split("x")) for s in
           os.environ.get("SHAPES", "512x512x512,1024x1024x1024,1024x1024x8192").split(",")]
 for (m, n, k) in SHAPES:
