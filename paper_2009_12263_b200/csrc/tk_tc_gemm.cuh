@@ -214,6 +214,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define TK_STAMPS 0  // CTA timestamps for tools/ts_probe.py (build with -DTK_STAMPS=1): ~60 ns per K block on the MMA thread
 #endif
 #define TK_TS(i) do { if (TK_STAMPS && blockIdx.x == p.dbg_cta) g_dbg_ts[i] = gtimer(); } while (0)
+// stamps builds: the latest value over all CTAs of a launch (globaltimer only grows)
+#define TK_TSMAX(i) do { if (TK_STAMPS) atomicMax(&g_dbg_ts[i], gtimer()); } while (0)
 #define TK_TS_EPI(i) do { if (TK_STAMPS && blockIdx.x == p.dbg_cta && (threadIdx.x >> 5) == 4 && (threadIdx.x & 31) == 0) g_dbg_ts[i] = gtimer(); } while (0)
 
 // Split-K partials to fold into the accumulator before the epilogue: this thread's row of the

@@ -221,7 +221,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EMB ? EMB_THREADS : 
   const uint32_t tmem_base = *tmem_slot;
   if (p.pdl) {
     // let the next launch in the stream start its prologue as our CTAs retire, and do not touch
-    // global memory before the previous grid (the producer of our inputs) has completed
+    // global memory before the previous grid (the producer of our inputs) has completed.
+    // (Waiting per role instead -- the producer only right before its first TMA load -- took
+    // ~1 us off the first stage at 1024-2048^3 but measured -1..+2.5 % overall: reverted.)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
   }
@@ -336,6 +338,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EMB ? EMB_THREADS : 
             int kb, cnt;
             kps_step(un, rev, st, kb, cnt);
             mbar_wait(&empty[stage], phase ^ 1);
+            if (lu == 0 && st == 0) { if (leader) TK_TS(12); TK_TSMAX(13); }
             if (leader) mbar_arrive_expect_tx(&full[stage], uint32_t(2 * cnt * PL::KB_BYTES));
             const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
             for (int h = 0; h < cnt; ++h) {
@@ -409,6 +412,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EMB ? EMB_THREADS : 
                   tma_prefetch_l2_2d(&p.tcmap, mb * 256 + int(rank) * 128 + r * 32, nb * BNP + un.noff + c * 32);
             }
           }
+          if (lu == 0 && ki == 0) { if (leader) TK_TS(12); TK_TSMAX(13); }
           if (leader) mbar_arrive_expect_tx(&full[stage], tx);
           const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
           if (EMB) {

@@ -27,9 +27,6 @@
 
 namespace tk {
 
-// stamps builds: the latest value over all CTAs of a launch (globaltimer only grows)
-#define TK_TSMAX(i) do { if (TK_STAMPS) atomicMax(&g_dbg_ts[i], gtimer()); } while (0)
-
 template <int BNI, int KPS>
 struct KsPlan {
   static constexpr int A_BYTES = 128 * 64 * 2;                  // this CTA's 128 rows x 64 k

@@ -8,7 +8,7 @@ while [ $# -ge 2 ]; do
   name=$1; flags=$2; shift 2
   mkdir -p "$ROOT/build/var_$name"
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -shared -Xcompiler -fPIC \
-    -cudart static --split-compile=0 $flags -o "$ROOT/build/var_$name/libtk_sm100.so" "$ROOT/paper_2009_12263_b200/csrc/tk_api.cu" \
+    -cudart static $flags -o "$ROOT/build/var_$name/libtk_sm100.so" "$ROOT/paper_2009_12263_b200/csrc/tk_api.cu" \
     > "$ROOT/build/var_$name/build.log" 2>&1 &
   pids+=($!)
 done

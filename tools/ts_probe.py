@@ -14,7 +14,7 @@ from paper_2009_12263_b200 import _lib, kernel  # noqa: E402
 
 lib = _lib.load()
 names = ["entry", "prologue", "1st full", "last MMA issued", "last acc full", "epilogue done", "stores drained",
-         "exit", "epi:tmem", "epi:math", "epi:store", "epi:C ready"]
+         "exit", "epi:tmem", "epi:math", "epi:store", "epi:C ready", "1st issue", "max 1st issue"]
 SHAPES = [tuple(int(x) for x in s.split("x")) for s in
           os.environ.get("SHAPES", "1024x1024x320,1024x1024x1024,1024x1024x4096,2048x2048x2048").split(",")]
 for (m, n, k) in SHAPES:
