@@ -184,6 +184,22 @@ def test_ksplit_on_chip(cuda, case, kps, nt, knob):
             assert O.rel_err(got, want) <= O.tolerance(k), O.rel_err(got, want)
 
 
+def test_ksplit_zero_c(cuda, knob):
+    """The k-split kernel with a Zero C layout (no C loads: D = A*B), integer inputs bitwise."""
+    knob("TK_KSPLIT", "2")
+    m, n, k = 768, 512, 1000 // 8 * 8
+    rng = np.random.default_rng(29)
+    a = _half(rng, (m, k), np.float16, True)
+    b = _half(rng, (k, n), np.float16, True)
+    cfg = tk.build_dense_config(m, n, k, np.float16)
+    cfg = dataclasses.replace(cfg, global_c_layout=tk.layouts.Zero(np.float32, ("M", "N"), (m, n)))
+    d = torch.full((m * n,), float("nan"), dtype=torch.float32, device=cuda)
+    tk.matmul(cfg, _dev(a), _dev(b), torch.empty(0, dtype=torch.float32, device=cuda), d)
+    assert tk.last_run()["plan"]["kernel"] == "ksplit", tk.last_run()["plan"]
+    want = O.gemm_real(_f32(a), _f32(b), np.zeros((m, n), np.float32))
+    assert np.array_equal(_host(d, (m, n)), want)
+
+
 def test_ksplit_auto_choice(cuda):
     """The default dispatch takes the on-chip split-K kernel for 1024^3 (single wave of 256 x 128
     tiles) and keeps whole-K pair tiles where there are enough of them (2048^3)."""
