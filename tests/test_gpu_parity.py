@@ -142,6 +142,7 @@ def test_narrow_tiles_ring_stages(cuda, bni, kps, grid, knob):
     (512, 768, 7 * 64 + 24, True, False, "f16"),  # K-major A, K tail inside the last block
     (768, 384, 640, False, True, "f16"),          # MN-major B
     (256, 128, 320, True, True, "bf16"),          # one cluster, 5 k-blocks (2 + 3)
+    (200, 40, 1024, False, False, "f16"),         # one partial M block, N < the finalised half
 ])
 def test_ksplit_on_chip(cuda, case, kps, nt, knob):
     """On-chip split-K (two CTA pairs per 256 x 128 tile, one K half each, partials
@@ -197,6 +198,25 @@ def test_ksplit_zero_c(cuda, knob):
     tk.matmul(cfg, _dev(a), _dev(b), torch.empty(0, dtype=torch.float32, device=cuda), d)
     assert tk.last_run()["plan"]["kernel"] == "ksplit", tk.last_run()["plan"]
     want = O.gemm_real(_f32(a), _f32(b), np.zeros((m, n), np.float32))
+    assert np.array_equal(_host(d, (m, n)), want)
+
+
+def test_ksplit_bias_m_relu(cuda, knob):
+    """k-split kernel with a bias along M and ReLU, both finalising halves: bitwise on integers."""
+    knob("TK_KSPLIT", "2")
+    m, n, k = 512, 384, 640
+    rng = np.random.default_rng(31)
+    a = _half(rng, (m, k), np.float16, True)
+    b = _half(rng, (k, n), np.float16, True)
+    c = rng.integers(-4, 5, (m, n)).astype(np.float32)
+    bias = rng.integers(-4, 5, m).astype(np.float32)
+    cfg = dataclasses.replace(tk.build_dense_config(m, n, k, np.float16),
+                              epilogue=tk.components.BiasEpilogue(torch.from_numpy(bias).cuda(), axis="m"),
+                              transform_s2g_d=tk.components.relu)
+    d = torch.full((m * n,), float("nan"), dtype=torch.float32, device=cuda)
+    tk.matmul(cfg, _dev(a), _dev(b), _dev(c), d)
+    assert tk.last_run()["plan"]["kernel"] == "ksplit", tk.last_run()["plan"]
+    want = np.maximum(O.gemm_real(_f32(a), _f32(b), c) + bias[:, None], 0)
     assert np.array_equal(_host(d, (m, n)), want)
 
 
