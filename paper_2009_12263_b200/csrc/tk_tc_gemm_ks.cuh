@@ -107,8 +107,8 @@ __global__ void __cluster_dims__(4 * NT, 1, 1) __launch_bounds__(TC_THREADS, 1)
     for (int w = 0; w < TC_EPI_WARPS; ++w) mbar_init(&cfull[w], 1);
     mbar_init(xready, 1);
     fence_mbar_init();
-    // the partner's partial: XBUF_BYTES of bulk-copy complete_tx (may land before this phase's
-    // expect_tx is visible to it: the pending arrival keeps the phase open until then)
+    // the partner's partial: XBUF_BYTES of bulk-copy complete_tx, sent only after this CTA's
+    // xready arrival (its ring is idle), long after this initialisation is cluster-visible
     mbar_arrive_expect_tx(xfull, PL::XBUF_BYTES);
   }
   if (warp == 2) {
