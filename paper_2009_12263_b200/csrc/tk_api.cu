@@ -66,7 +66,7 @@ enum Knob {
   K_NSUB2_CSL, K_STAGGER, K_PAIR_GRID, K_PAIR_DEEPC, K_PAIROPS_BN, K_DIAG_STREAM, K_D_TMA,
   K_L2_PROMO, K_POLICY_AB, K_POL_A, K_POL_B, K_PAIR_CLUSTERS, K_EX_SLABS, K_VERBOSE,
   K_NSUB2_OVERLAP, K_PAIR_KPS, K_CPLX_EMBED, K_POL_C, K_POL_D, K_SIMT_TILED, K_GATHER, K_KSPLIT,
-  K_KSPLIT_KPS, K_KSPLIT_NT,
+  K_KSPLIT_KPS, K_KSPLIT_NT, K_KSPLIT_BNI,
   K_DBG_C_ZERO, K_DBG_SKIP_EPI, K_DBG_NO_LOAD, K_DBG_NO_MMA, K_DBG_CTA, K_COUNT
 };
 constexpr int K_FIRST_DIAG = K_DBG_C_ZERO;
@@ -77,7 +77,7 @@ const char* const kKnobNames[K_COUNT] = {
   "TK_PAIR_DEEPC", "TK_PAIROPS_BN", "TK_DIAG_STREAM", "TK_D_TMA", "TK_L2_PROMO", "TK_POLICY_AB",
   "TK_POL_A", "TK_POL_B", "TK_PAIR_CLUSTERS", "TK_EX_SLABS", "TK_VERBOSE", "TK_NSUB2_OVERLAP",
   "TK_PAIR_KPS", "TK_CPLX_EMBED", "TK_POL_C", "TK_POL_D", "TK_SIMT_TILED", "TK_GATHER", "TK_KSPLIT",
-  "TK_KSPLIT_KPS", "TK_KSPLIT_NT", "TK_DBG_C_ZERO", "TK_DBG_SKIP_EPI", "TK_DBG_NO_LOAD", "TK_DBG_NO_MMA", "TK_DBG_CTA"};
+  "TK_KSPLIT_KPS", "TK_KSPLIT_NT", "TK_KSPLIT_BNI", "TK_DBG_C_ZERO", "TK_DBG_SKIP_EPI", "TK_DBG_NO_LOAD", "TK_DBG_NO_MMA", "TK_DBG_CTA"};
 #ifdef TK_DIAG
 constexpr int K_ENABLED = K_COUNT;
 #else
@@ -875,14 +875,14 @@ int launch_tc_pair_bni(const tk::TcParams& prm, int bni, cudaStream_t s) {
 // one K half each, reduced through distributed shared memory; NT = 2 puts two N-adjacent tiles
 // in one 8-CTA cluster that multicasts the shared A atoms.  Single wave only: every cluster owns
 // its tile(s), so there may not be more of them than co-resident clusters.
-template <int KPS, int NT>
+template <int BNI, int KPS, int NT>
 int ksplit_max_clusters() {
-  using PL = tk::KsPlan<128, KPS>;
+  using PL = tk::KsPlan<BNI, KPS>;
   static int cache[TK_MAX_DEV] = {};
   const int dev = cur_dev();
   int& mc = cache[dev];
   if (!mc) {
-    auto kern = tk::tc_gemm_ksplit_kernel<128, KPS, NT>;
+    auto kern = tk::tc_gemm_ksplit_kernel<BNI, KPS, NT>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PL::SMEM) != cudaSuccess) {
       cudaGetLastError();
       return mc = -1;
@@ -902,21 +902,28 @@ int ksplit_max_clusters() {
       cudaGetLastError();
       mc = -1;
     }
-    if (knob(K_VERBOSE, 0)) fprintf(stderr, "tk: k-split kernel (%d-CTA clusters) max active clusters %d\n", 4 * NT, mc);
+    if (knob(K_VERBOSE, 0))
+      fprintf(stderr, "tk: k-split kernel (256x%d tiles, %d-CTA clusters) max active clusters %d\n", BNI, 4 * NT, mc);
   }
   return mc;
 }
 // one K-block per stage: measured faster than two here (1024^3 8.0 vs 8.4 us, 1024^2 x 8192
 // 21.3 vs 24.4 us) -- unlike the whole-K narrow tiles, whose stage count is not the limit
 int ksplit_kps() { return knob(K_KSPLIT_KPS, 1) == 2 ? 2 : 1; }
-int ksplit_clusters(int nt) {
-  if (ksplit_kps() == 1) return nt == 2 ? ksplit_max_clusters<1, 2>() : ksplit_max_clusters<1, 1>();
-  return nt == 2 ? ksplit_max_clusters<2, 2>() : ksplit_max_clusters<2, 1>();
+// k-split variants: 1 = 256 x 128 tiles, 4-CTA clusters; 2 = the same, two tiles per 8-CTA
+// cluster with multicast A; 3 = 256 x 256 tiles, 4-CTA clusters
+int ksplit_clusters(int variant) {
+  const bool k1 = ksplit_kps() == 1;
+  switch (variant) {
+    case 1: return k1 ? ksplit_max_clusters<128, 1, 1>() : ksplit_max_clusters<128, 2, 1>();
+    case 2: return k1 ? ksplit_max_clusters<128, 1, 2>() : ksplit_max_clusters<128, 2, 2>();
+    default: return k1 ? ksplit_max_clusters<256, 1, 1>() : ksplit_max_clusters<256, 2, 1>();
+  }
 }
 
-template <int KPS, int NT>
+template <int BNI, int KPS, int NT>
 int launch_tc_ksplit(const tk::TcParams& prm, cudaStream_t s) {
-  using PL = tk::KsPlan<128, KPS>;
+  using PL = tk::KsPlan<BNI, KPS>;
   tk::TcParams run = prm;
   run.pdl = knob(K_PDL, 1) ? 1 : 0;
   cudaLaunchConfig_t cfg = {};
@@ -929,13 +936,13 @@ int launch_tc_ksplit(const tk::TcParams& prm, cudaStream_t s) {
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = run.pdl ? 1 : 0;
-  TK_CUDA(cudaLaunchKernelEx(&cfg, tk::tc_gemm_ksplit_kernel<128, KPS, NT>, run));
+  TK_CUDA(cudaLaunchKernelEx(&cfg, tk::tc_gemm_ksplit_kernel<BNI, KPS, NT>, run));
   ++g_launches;
   info_kernel("ksplit");
   g_info.tile_m = 256;
   g_info.tile_k = 64 * KPS;
-  g_info.tile_n = 128 * NT;
-  g_info.mma_n = 128;
+  g_info.tile_n = BNI * NT;
+  g_info.mma_n = BNI;
   g_info.nsub = 1;
   g_info.mmas_per_k16 = 1;
   g_info.cluster = 4 * NT;
@@ -954,16 +961,21 @@ int launch_tc_ksplit(const tk::TcParams& prm, cudaStream_t s) {
   g_info.d_tma = 1;
   return TK_OK;
 }
-int launch_tc_ksplit_any(const tk::TcParams& prm, int nt, cudaStream_t s) {
-  if (ksplit_kps() == 1) return nt == 2 ? launch_tc_ksplit<1, 2>(prm, s) : launch_tc_ksplit<1, 1>(prm, s);
-  return nt == 2 ? launch_tc_ksplit<2, 2>(prm, s) : launch_tc_ksplit<2, 1>(prm, s);
+int launch_tc_ksplit_any(const tk::TcParams& prm, int variant, cudaStream_t s) {
+  const bool k1 = ksplit_kps() == 1;
+  switch (variant) {
+    case 1: return k1 ? launch_tc_ksplit<128, 1, 1>(prm, s) : launch_tc_ksplit<128, 2, 1>(prm, s);
+    case 2: return k1 ? launch_tc_ksplit<128, 1, 2>(prm, s) : launch_tc_ksplit<128, 2, 2>(prm, s);
+    default: return k1 ? launch_tc_ksplit<256, 1, 1>(prm, s) : launch_tc_ksplit<256, 2, 1>(prm, s);
+  }
 }
 
 // Use the on-chip split-K kernel?  TK_KSPLIT: 0 never, 1 auto (default), 2 whenever legal.
 // Auto compares the per-k-block ingest model of choose_pair_bni: whole-K pair tiles (waves x
-// KB x t(bni)) against half-K 256 x 128 tiles (KB/2 x t(128) + the reduce-scatter).  Returns the
-// tiles per cluster (2: 8-CTA clusters with A multicast, when they all fit; TK_KSPLIT_NT pins
-// it), or 0 for the pair kernel.
+// KB x t(bni)) against half-K tiles (KB/2 x t(tile width) + the reduce-scatter).  Returns the
+// variant (ksplit_clusters), or 0 for the pair kernel: 256 x 128 tiles when they all fit the
+// co-resident 4-CTA clusters, else 256 x 256 tiles when those fit; TK_KSPLIT_NT=2 asks for
+// 8-CTA clusters, TK_KSPLIT_BNI=256 for the wide tiles.
 int ksplit_choice(int64_t m, int64_t n, int kb_total, int pair_bni, int clusters) {
   const int mode = knob(K_KSPLIT, 1);
   if (mode == 0 || kb_total < 4) return 0;
@@ -971,22 +983,25 @@ int ksplit_choice(int64_t m, int64_t n, int kb_total, int pair_bni, int clusters
   if (mode == 1 && (tc_kernel_override() != 0 || knob_set(K_PAIR_BNI))) return 0;
   const int64_t tiles = ((m + 255) / 256) * ((n + 127) / 128);
   const int64_t tiles2 = ((m + 255) / 256) * ((n + 255) / 256);
-  const int want_nt = knob(K_KSPLIT_NT, 0);
-  int nt = 0;
-  if (want_nt != 1) {
-    const int mc2 = ksplit_clusters(2);
-    if (mc2 > 0 && tiles2 <= mc2) nt = 2;
+  const int want_nt = knob(K_KSPLIT_NT, 0), want_bni = knob(K_KSPLIT_BNI, 0);
+  int v = 0;
+  if (want_nt == 2) {
+    const int mc = ksplit_clusters(2);
+    if (mc > 0 && tiles2 <= mc) v = 2;
+  } else if (want_bni != 256) {
+    const int mc = ksplit_clusters(1);
+    if (mc > 0 && tiles <= mc) v = 1;
   }
-  if (!nt && want_nt != 2) {
-    const int mc1 = ksplit_clusters(1);
-    if (mc1 > 0 && tiles <= mc1) nt = 1;
+  if (!v && want_nt != 2 && want_bni != 128) {
+    const int mc = ksplit_clusters(3);
+    if (mc > 0 && tiles2 <= mc) v = 3;
   }
-  if (!nt || mode == 2) return nt;
+  if (!v || mode == 2) return v;
   auto per_kb = [](int bni) { return std::max(2.0 * bni, (16384.0 + 64.0 * bni) / 60.0); };
   const int64_t ptiles = ((m + 255) / 256) * ((n + pair_bni - 1) / pair_bni);
   const double t_pair = double((ptiles + clusters - 1) / clusters) * kb_total * per_kb(pair_bni);
-  const double t_ks = 0.5 * kb_total * per_kb(128) + 500.0;
-  return t_ks < t_pair ? nt : 0;
+  const double t_ks = 0.5 * kb_total * per_kb(v == 3 ? 256 : 128) + (v == 3 ? 800.0 : 500.0);
+  return t_ks < t_pair ? v : 0;
 }
 
 // Split-K of a poorly filled last wave: with T tiles over P clusters, W = T / P full waves and
@@ -1540,10 +1555,10 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
       int bni = pred_tc ? pred_bni(p) : (nsub == 2 || emb) ? 256
                       : choose_pair_bni(p->m, p->n, /*b_mn_major=*/prm.b_g ? prm.b_mn != 0 : !mn, pair_clusters());
       // on-chip split-K of single-wave shapes (256 x 128 tiles, K halves on two CTA pairs)
-      const int ks_nt = (nsub == 1 && !pred_tc && !emb && !prm.a_g && !prm.b_g && dense && !rmapped)
-                            ? ksplit_choice(p->m, p->n, pp.kb_total, bni, pair_clusters()) : 0;
-      const bool ks = ks_nt > 0;
-      if (ks) bni = 128;
+      const int ks_v = (nsub == 1 && !pred_tc && !emb && !prm.a_g && !prm.b_g && dense && !rmapped)
+                           ? ksplit_choice(p->m, p->n, pp.kb_total, bni, pair_clusters()) : 0;
+      const bool ks = ks_v > 0;
+      if (ks) bni = ks_v == 3 ? 256 : 128;
       pp.num_mb = int((p->m + 255) / 256);
       pp.num_nb = int((p->n + bni * nsub - 1) / (bni * nsub));
       pp.num_tiles = pp.num_mb * pp.num_nb;
@@ -1647,7 +1662,7 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
         }
         if (ks && !pp.npeer) {
           tk::TcParams kp = pp;
-          if (ks_nt == 2) {  // tile pairs; A in 64-row atoms (each CTA multicasts one)
+          if (ks_v == 2) {  // tile pairs; A in 64-row atoms (each CTA multicasts one)
             kp.num_nb = int((p->n + 255) / 256);
             kp.num_tiles = kp.num_mb * kp.num_nb;
             tma_operand(p->a, mn, pitch);
@@ -1655,7 +1670,7 @@ int run_tc(const TkGemmPlan* p0, const void* a, const void* b, const void* c, vo
                          : make_map_2d(&kp.ta[0], a_plane0, p->a.scalar, p->k, p->m, pitch, 64, 64)))
               return rc;
           }
-          return launch_tc_ksplit_any(kp, ks_nt, s);
+          return launch_tc_ksplit_any(kp, ks_v, s);
         }
         return launch_tc_pair_bni<true, true>(pp, bni, s);
       }

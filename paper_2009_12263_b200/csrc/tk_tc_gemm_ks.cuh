@@ -9,6 +9,9 @@
 // re-read half as often) while still occupying 128 SMs: each SM ingests 8 x 24 KB instead of
 // 16 x 20 KB and issues half as many MMA steps.
 //
+// BNI = 256 (256 x 256 tiles, 128 finalised columns and two C/D boxes per epilogue warp) takes
+// the single-wave shapes whose 256 x 128 tiles outnumber the co-resident clusters (2048 x 1024).
+//
 // Cluster ranks: r = 2q + h.  Pair q (leader rank 2q) accumulates k-blocks
 // [q*KB/2, (q+1)*KB/2) of the tile (the reference's k-ascending order inside each half,
 // kernel.py:399-404); h selects the 128-row half of the tile (as in the pair kernel).
@@ -50,7 +53,8 @@ struct KsPlan {
   static constexpr int BAR_OFFSET = CRING + CRING_BYTES;
   static constexpr int SMEM = BAR_OFFSET + 512 + 1024;
   static constexpr int TMEM_COLS = BNI < 32 ? 32 : BNI;
-  static_assert(BOXES == TC_EPI_WARPS, "one C/D box per epilogue warp");
+  static constexpr int CPW = BOXES / TC_EPI_WARPS;              // boxes (32-column chunks) per epilogue warp
+  static_assert(CPW * TC_EPI_WARPS == BOXES, "whole boxes per epilogue warp");
   static_assert(2 * XBUF_BYTES <= STAGES * STAGE_BYTES, "staging + partial fit in the ring");
   static_assert(STAGES >= 2 && SMEM <= 227 * 1024, "k-split kernel shared memory");
 };
@@ -63,7 +67,8 @@ template <int BNI, int KPS, int NT>
 __global__ void __cluster_dims__(4 * NT, 1, 1) __launch_bounds__(TC_THREADS, 1)
     tc_gemm_ksplit_kernel(const __grid_constant__ TcParams p) {
   using PL = KsPlan<BNI, KPS>;
-  static_assert(BNI == 128, "256 x 128 tiles (N=128 pair MMAs, 64 finalised columns per CTA)");
+  static_assert(BNI == 128 || (BNI == 256 && NT == 1),
+                "256 x 128 tiles (64 finalised columns per CTA) or 256 x 256 (128, 4-CTA clusters)");
   constexpr int STAGES = PL::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -72,8 +77,8 @@ __global__ void __cluster_dims__(4 * NT, 1, 1) __launch_bounds__(TC_THREADS, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* xfull = tfull + 1;
-  uint64_t* cfull = xfull + 1;  // [TC_EPI_WARPS]
-  uint64_t* xready = cfull + TC_EPI_WARPS;  // the partner's ring is idle: its partial may be sent
+  uint64_t* cfull = xfull + 1;  // [BOXES]
+  uint64_t* xready = cfull + PL::BOXES;  // the partner's ring is idle: its partial may be sent
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xready + 1);
   float* cring = reinterpret_cast<float*>(smem + PL::CRING);
   const uint32_t xbuf = smem_u32(smem + PL::XBUF);
@@ -104,7 +109,7 @@ __global__ void __cluster_dims__(4 * NT, 1, 1) __launch_bounds__(TC_THREADS, 1)
     }
     mbar_init(tfull, 1);
     mbar_init(xfull, 1);
-    for (int w = 0; w < TC_EPI_WARPS; ++w) mbar_init(&cfull[w], 1);
+    for (int w = 0; w < PL::BOXES; ++w) mbar_init(&cfull[w], 1);
     mbar_init(xready, 1);
     fence_mbar_init();
     // the partner's partial: XBUF_BYTES of bulk-copy complete_tx, sent only after this CTA's
@@ -169,8 +174,9 @@ __global__ void __cluster_dims__(4 * NT, 1, 1) __launch_bounds__(TC_THREADS, 1)
           }
           if (b_mode == 0) {
             tma_load_3d_pair(bt, &p.tb[0], fb, 0, k0, n0 >> 6, pol_b);
-          } else if (b_mode == 1) {
-            tma_load_2d_pair(bt, &p.tb[0], fb, n0, k0, pol_b);
+          } else if (b_mode == 1) {  // 64-column MN-major atoms
+            for (int hb = 0; hb < BNI / 128; ++hb)
+              tma_load_2d_pair(bt + hb * 8192, &p.tb[0], fb, n0 + 64 * hb, k0, pol_b);
           } else {
             tma_load_2d_pair(bt, &p.tb[0], fb, k0, n0, pol_b);
           }
@@ -181,7 +187,7 @@ __global__ void __cluster_dims__(4 * NT, 1, 1) __launch_bounds__(TC_THREADS, 1)
         if (!p.c_zero && (kb - kb0 + KPS >= STAGES * KPS || kb + KPS >= kb1) && !c_issued) {
           c_issued = true;
           const uint64_t pol_c = policy_code(p.pol_c);
-          for (int w = 0; w < TC_EPI_WARPS; ++w) {
+          for (int w = 0; w < PL::BOXES; ++w) {
             mbar_arrive_expect_tx(&cfull[w], TC_CBOX_BYTES);
             tma_load_2d(cring + w * (TC_CBOX_BYTES / 4), &p.tcmap, &cfull[w], row0 + (w & 3) * 32,
                         nb * BNI + int(q) * PL::HALF_COLS + (w >> 2) * 32, pol_c);
@@ -218,14 +224,14 @@ __global__ void __cluster_dims__(4 * NT, 1, 1) __launch_bounds__(TC_THREADS, 1)
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ reduce-scatter + epilogue
+    // warp ew owns boxes b = ew + 8i (i < CPW): TMEM lane quarter b & 3 (= warp & 3), 32-column
+    // chunk b >> 2 of the finalised half
     const int ew = warp - 4;
     const int quarter = warp & 3;  // TMEM lane quarter of this warp
-    const int chunk = ew >> 2;     // 32-column chunk of the finalised half
     const int row_local = quarter * 32 + lane;
     const uint32_t tlane = tmem_base + (uint32_t(quarter * 32) << 16);
-    // partial layout (per CTA): chunk c at c*16 KB, row r at r*128 B, 16-byte granule g at
-    // (g ^ (r & 7)) -- conflict-free for the 8-lane phases of both the v4 stores and loads
-    const uint32_t xrow = uint32_t(chunk * 16384 + row_local * 128);
+    // partial layout (per CTA): box b at b*4 KB (chunk c at c*16 KB, row r at r*128 B), 16-byte
+    // granule g at (g ^ (r & 7)) -- conflict-free for the 8-lane phases of the v4 stores / loads
     const int sw = row_local & 7;
     mbar_wait_sleep(tfull, 0);
     TK_TS_EPI(4);
@@ -236,80 +242,92 @@ __global__ void __cluster_dims__(4 * NT, 1, 1) __launch_bounds__(TC_THREADS, 1)
       mbar_arrive_cluster(mapa_shared(smem_u32(xready), partner));
     }
     tc_fence_after();
-    {  // ship the partner's columns of this warp's chunk: stage them (swizzled like the
-       // partner's buffer) in this CTA's operand ring -- free once the accumulator is full, all
-       // MMAs and hence all operand reads having completed -- and move the warp's 4 KB with one
-       // bulk copy into the partner's ring (once it is idle too) that completes on its barrier
+    // ship the partner's columns of this warp's boxes: stage them (swizzled like the partner's
+    // buffer, at the same offsets) in this CTA's operand ring -- free once the accumulator is
+    // full, all MMAs and hence all operand reads having completed -- and move each 4 KB box with
+    // one bulk copy into the partner's ring (once it is idle too) that completes on its barrier
+#pragma unroll 1
+    for (int i = 0; i < PL::CPW; ++i) {
+      const int bx = ew + TC_EPI_WARPS * i, chunk = bx >> 2;
       uint32_t r[32];
       tmem_ld_32x32b_x32(tlane + uint32_t((q ^ 1u) * PL::HALF_COLS + chunk * 32), r);
       tmem_ld_wait();
-      const uint32_t stg = smem_u32(smem) + uint32_t(ew * 4096 + lane * 128);
+      const uint32_t stg = smem_u32(smem) + uint32_t(bx * 4096 + lane * 128);
 #pragma unroll
       for (int g = 0; g < 8; ++g)
         asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(stg + uint32_t((g ^ sw) << 4)), "r"(r[4 * g]),
                      "r"(r[4 * g + 1]), "r"(r[4 * g + 2]), "r"(r[4 * g + 3])
                      : "memory");
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) {
-        mbar_wait(xready, 0);  // the partner's ring is idle
-        asm volatile(
-            "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], 4096, [%2];" ::"r"(
-                mapa_shared(xbuf + uint32_t(chunk * 16384 + quarter * 4096), partner)),
-            "r"(smem_u32(smem) + uint32_t(ew * 4096)), "r"(mapa_shared(smem_u32(xfull), partner))
-            : "memory");
-      }
-      TK_TS_EPI(3);
     }
-    const int j0 = nb * BNI + int(q) * PL::HALF_COLS + chunk * 32;
-    const int i = row0 + row_local;
-    uint32_t r[32];
-    tmem_ld_32x32b_x32(tlane + uint32_t(q * PL::HALF_COLS + chunk * 32), r);
-    const bool row_ok = i < p.m;
-    const int jl = j0 + lane;
-    const float bcol = (p.bias_axis == 1 && jl < p.n) ? p.bias[jl] : 0.f;
-    const float bias_m = (p.bias_axis == 2 && row_ok) ? p.bias[i] : 0.f;
-    const uint32_t box_s = smem_u32(cring + ew * (TC_CBOX_BYTES / 4));
-    float cv[32];
-    if (!p.c_zero) {
-      mbar_wait(&cfull[ew], 0);
-#pragma unroll
-      for (int jj = 0; jj < 32; ++jj) cv[jj] = lds_f32(box_s + uint32_t(jj * 32 + lane) * 4u);
-    }
-    float pv[32];
-    mbar_wait(xfull, 0);
-    TK_TS_EPI(5);
-#pragma unroll
-    for (int g = 0; g < 8; ++g) {
-      uint32_t v0, v1, v2, v3;
-      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                   : "=r"(v0), "=r"(v1), "=r"(v2), "=r"(v3)
-                   : "r"(xbuf + xrow + uint32_t((g ^ sw) << 4)));
-      pv[4 * g] = __uint_as_float(v0);
-      pv[4 * g + 1] = __uint_as_float(v1);
-      pv[4 * g + 2] = __uint_as_float(v2);
-      pv[4 * g + 3] = __uint_as_float(v3);
-    }
-    tmem_ld_wait();
-    TK_TS_EPI(14);
-    float out[32];
-    epi_math_real<true>(p, r, cv, pv, !p.c_zero, bias_m, bcol, out);
-    float* box = cring + ew * (TC_CBOX_BYTES / 4);
-    __syncwarp();  // every lane has read its C column before the box is overwritten
-#pragma unroll
-    for (int jj = 0; jj < 32; ++jj) sts_f32(box_s + uint32_t(jj * 32 + lane) * 4u, out[jj]);
     fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) {
-      // (per-thread st.global of the same 32 KB per CTA measured ~0.5 us slower to retire)
-      if (p.pol_d)
-        tma_store_2d_hint(&p.tdmap, box, row0 + quarter * 32, j0, policy_code(p.pol_d));
-      else
-        tma_store_2d(&p.tdmap, box, row0 + quarter * 32, j0);  // clips rows >= M, columns >= N
-      bulk_commit();
+      mbar_wait(xready, 0);  // the partner's ring is idle
+      for (int i = 0; i < PL::CPW; ++i) {
+        const int bx = ew + TC_EPI_WARPS * i;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], 4096, [%2];" ::"r"(
+                mapa_shared(xbuf + uint32_t(bx * 4096), partner)),
+            "r"(smem_u32(smem) + uint32_t(bx * 4096)), "r"(mapa_shared(smem_u32(xfull), partner))
+            : "memory");
+      }
+    }
+    TK_TS_EPI(3);
+    const int i_row = row0 + row_local;
+    const bool row_ok = i_row < p.m;
+    const float bias_m = (p.bias_axis == 2 && row_ok) ? p.bias[i_row] : 0.f;
+#pragma unroll 1
+    for (int i = 0; i < PL::CPW; ++i) {
+      const int bx = ew + TC_EPI_WARPS * i, chunk = bx >> 2;
+      const int j0 = nb * BNI + int(q) * PL::HALF_COLS + chunk * 32;
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(tlane + uint32_t(q * PL::HALF_COLS + chunk * 32), r);
+      const int jl = j0 + lane;
+      const float bcol = (p.bias_axis == 1 && jl < p.n) ? p.bias[jl] : 0.f;
+      float* box = cring + bx * (TC_CBOX_BYTES / 4);
+      const uint32_t box_s = smem_u32(box);
+      float cv[32];
+      if (!p.c_zero) {
+        mbar_wait(&cfull[bx], 0);
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) cv[jj] = lds_f32(box_s + uint32_t(jj * 32 + lane) * 4u);
+      }
+      float pv[32];
+      mbar_wait(xfull, 0);
+      if (i == 0) TK_TS_EPI(5);
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        uint32_t v0, v1, v2, v3;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v0), "=r"(v1), "=r"(v2), "=r"(v3)
+                     : "r"(xbuf + uint32_t(bx * 4096 + lane * 128) + uint32_t((g ^ sw) << 4)));
+        pv[4 * g] = __uint_as_float(v0);
+        pv[4 * g + 1] = __uint_as_float(v1);
+        pv[4 * g + 2] = __uint_as_float(v2);
+        pv[4 * g + 3] = __uint_as_float(v3);
+      }
+      tmem_ld_wait();
+      if (i == 0) TK_TS_EPI(14);
+      float out[32];
+      epi_math_real<true>(p, r, cv, pv, !p.c_zero, bias_m, bcol, out);
+      __syncwarp();  // every lane has read its C column before the box is overwritten
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) sts_f32(box_s + uint32_t(jj * 32 + lane) * 4u, out[jj]);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        // (per-thread st.global of the same 32 KB per CTA measured ~0.5 us slower to retire)
+        if (p.pol_d)
+          tma_store_2d_hint(&p.tdmap, box, row0 + quarter * 32, j0, policy_code(p.pol_d));
+        else
+          tma_store_2d(&p.tdmap, box, row0 + quarter * 32, j0);  // clips rows >= M, columns >= N
+        bulk_commit();
+      }
+    }
+    if (lane == 0) {
       TK_TS_EPI(6);
       if (warp == 4) TK_TSMAX(10);
-      bulk_wait_read<0>();  // the box is read; grid completion performs the store
+      bulk_wait_read<0>();  // the boxes are read; grid completion performs the stores
       TK_TS_EPI(8);
     }
   }

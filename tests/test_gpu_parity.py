@@ -134,7 +134,7 @@ def test_narrow_tiles_ring_stages(cuda, bni, kps, grid, knob):
         assert np.array_equal(got, want), (m, n, k, float(np.abs(got - want).max()))
 
 
-@pytest.mark.parametrize("nt", ["1", "2"])
+@pytest.mark.parametrize("nt", ["1", "2", "w"])
 @pytest.mark.parametrize("kps", ["1", "2"])
 @pytest.mark.parametrize("case", [
     (1024, 1024, 1024, False, False, "f16"),      # the C2 low end: 32 tiles of 256 x 128
@@ -147,14 +147,18 @@ def test_narrow_tiles_ring_stages(cuda, bni, kps, grid, knob):
 def test_ksplit_on_chip(cuda, case, kps, nt, knob):
     """On-chip split-K (two CTA pairs per 256 x 128 tile, one K half each, partials
     reduce-scattered through distributed shared memory; 4-CTA clusters, or 8 with two tiles
-    sharing multicast A atoms -- the shapes include a second tile wholly past N): integer inputs
+    sharing multicast A atoms -- the shapes include a second tile wholly past N -- or, `w`,
+    256 x 256 tiles on 4-CTA clusters, two boxes per epilogue warp): integer inputs
     bitwise equal to the oracle with bias + ReLU, random inputs within the sqrt(K) bound with the
     C3 alpha/beta scaling, and the plan really is the k-split kernel."""
     m, n, k, ta, tb, dt = case
     dtype = tk.BFLOAT16 if dt == "bf16" else np.dtype(np.float16)
     knob("TK_KSPLIT", "2")
     knob("TK_KSPLIT_KPS", kps)
-    knob("TK_KSPLIT_NT", nt)
+    if nt == "w":
+        knob("TK_KSPLIT_BNI", "256")
+    else:
+        knob("TK_KSPLIT_NT", nt)
     rng = np.random.default_rng(23)
     for integer in (True, False):
         a, b = _half(rng, (m, k), dtype, integer), _half(rng, (k, n), dtype, integer)
@@ -173,7 +177,8 @@ def test_ksplit_on_chip(cuda, case, kps, nt, knob):
         if plan["kernel"] == "pair":  # 8-CTA clusters: only ~15 are co-resident on a B200
             assert nt == "2" and ((m + 255) // 256) * ((n + 255) // 256) >= 15, plan
         else:
-            assert plan["kernel"] == "ksplit" and plan["cluster"] == 4 * int(nt), plan
+            assert plan["kernel"] == "ksplit" and plan["cluster"] == (8 if nt == "2" else 4), plan
+            assert plan["mma_n"] == (256 if nt == "w" else 128), plan
             assert plan["tile_k"] == 64 * int(kps), plan
         got = _host(d, (m, n))
         if integer:

@@ -61,11 +61,13 @@ def main():
         row = []
         ref = None
         for label, ks, kps, pdl in (("pair", "0", None, None), ("ks-nt1", "2", "1", None), ("ks-nt2", "2", "2", None),
-                                    ("auto", None, None, None)):
+                                    ("ks-w256", "2", "w", None), ("auto", None, None, None)):
             _lib.tune_reset()
             if ks is not None:
                 _lib.tune("TK_KSPLIT", ks)
-            if kps is not None:
+            if kps == "w":
+                _lib.tune("TK_KSPLIT_BNI", "256")
+            elif kps is not None:
                 _lib.tune("TK_KSPLIT_NT", kps)
             if pdl is not None:
                 _lib.tune("TK_PDL", pdl)
