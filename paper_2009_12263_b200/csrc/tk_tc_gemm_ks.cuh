@@ -40,8 +40,9 @@ struct KsPlan {
   static constexpr int BOXES = 4 * HALF_COLS / 32;              // 32x32 C/D boxes per CTA
   static constexpr int CRING_BYTES = BOXES * TC_CBOX_BYTES;     // one C box per box, prefetched
   static constexpr int XBUF_BYTES = 128 * HALF_COLS * 4;        // partner's partial (FP32)
-  // the partner's partial lands in this CTA's operand ring once that is idle (XBUF, after the
-  // 32 KB where the outgoing half is staged): the ring gets the room (8 stages instead of 6)
+  // the partner's partial lands in this CTA's operand ring once that is idle (at XBUF, after the
+  // XBUF_BYTES where the outgoing half is staged): the ring gets the room (BNI 128: 8 stages
+  // instead of 6)
   static constexpr int FIXED = CRING_BYTES + 512 + 1024;
   static constexpr int MAX_STAGES = (227 * 1024 - FIXED) / STAGE_BYTES;
 #ifndef TK_KS_MAX_STAGES
