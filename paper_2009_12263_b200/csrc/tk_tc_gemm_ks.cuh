@@ -28,6 +28,10 @@
 #pragma once
 #include "tk_tc_gemm2.cuh"
 
+#ifndef TK_KS_ROLE_WAIT
+#define TK_KS_ROLE_WAIT 0
+#endif
+
 namespace tk {
 
 template <int BNI, int KPS>
@@ -127,7 +131,9 @@ __global__ void __cluster_dims__(4 * NT, 1, 1) __launch_bounds__(TC_THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
   if (p.pdl) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // (TK_KS_ROLE_WAIT builds: the producer waits right before its first load and the
+    // epilogue warps before their first global access instead -- an experiment)
+    if (!TK_KS_ROLE_WAIT) asm volatile("griddepcontrol.wait;" ::: "memory");
   }
   // stamps (TK_STAMPS builds): 15 = the previous launch's exit, 1 = inputs may be read
   if (TK_STAMPS && threadIdx.x == 0 && blockIdx.x == p.dbg_cta) g_dbg_ts[15] = g_dbg_ts[7];
@@ -153,6 +159,7 @@ __global__ void __cluster_dims__(4 * NT, 1, 1) __launch_bounds__(TC_THREADS, 1)
       for (int kb = kb0; kb < kb1; kb += KPS) {
         const int cnt = kb1 - kb < KPS ? kb1 - kb : KPS;
         mbar_wait(&empty[stage], phase ^ 1);
+        if (TK_KS_ROLE_WAIT && kb == kb0 && p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
         const uint32_t fb = fb0 + uint32_t(stage * 8);
         if (h == 0) mbar_arrive_expect_tx(&full[stage], uint32_t(2 * cnt * PL::KB_BYTES));
         for (int hh = 0; hh < cnt; ++hh) {
@@ -225,6 +232,7 @@ __global__ void __cluster_dims__(4 * NT, 1, 1) __launch_bounds__(TC_THREADS, 1)
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ reduce-scatter + epilogue
+    if (TK_KS_ROLE_WAIT && p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
     // warp ew owns boxes b = ew + 8i (i < CPW): TMEM lane quarter b & 3 (= warp & 3), 32-column
     // chunk b >> 2 of the finalised half
     const int ew = warp - 4;
